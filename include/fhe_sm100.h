@@ -1,0 +1,126 @@
+/*
+ * fhe_sm100.h - C ABI of the B200 (sm_100a) RNS-FHE hot path.
+ *
+ * This is the drop-in boundary for the reference's optional compiled-kernel
+ * seam, the numba module rnsfhe.coremath._kernels, which the reference
+ * imports behind try/except at coremath/ntt.py:24-27, rnspoly.py:21-24,
+ * keys.py:22-25, schemes/ckks.py:33-36 and schemes/behz.py:22-25, plus the
+ * scheme-level operations built on it.  Each entry point names the reference
+ * interface it replaces.  INTEGRATION.md shows the ctypes binding.
+ *
+ * Conventions (all entry points):
+ *  - plain pointers and sizes; polynomials are uint64 residues in the
+ *    reference CData layout: word ((p * size_modulus) + j) * n + i
+ *    (rnspoly.py:1-8), evaluation (NTT) domain unless stated;
+ *  - every "uint64_t *" data pointer is DEVICE memory owned by the caller;
+ *    the library never allocates on the hot path (work buffers are passed in);
+ *  - "stream" is a cudaStream_t (NULL = legacy default stream); calls are
+ *    asynchronous on it and thread-safe across streams;
+ *  - return 0 on success, a negative code on error; fhe_last_error() returns
+ *    the thread-local message of the last failure.  Shape/level validation
+ *    stays in the host layer (as in the reference, e.g. ntt.py:280-282).
+ */
+#ifndef FHE_SM100_H
+#define FHE_SM100_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct FheChain FheChain;     /* NTT + reduction tables of one prime chain */
+typedef struct FheContext FheContext; /* chain Q|P plus rescale / key-switch plans */
+
+/* element-wise op codes for fhe_ewise (rnspoly.py:214-308, vecmod.py:114-165) */
+enum {
+  FHE_EW_ADD = 0,     /* a + b            poly_add / add_arr          */
+  FHE_EW_SUB = 1,     /* a - b            poly_sub / sub_arr          */
+  FHE_EW_NEG = 2,     /* -a               poly_negate / neg_arr       */
+  FHE_EW_MUL = 3,     /* a * b            _kernels.mul_batch          */
+  FHE_EW_NEG_MUL = 4, /* -(a * b)         _kernels.neg_mul_batch      */
+  FHE_EW_MUL_ADD = 5, /* a * b + c        _kernels.mul_add_batch      */
+  FHE_EW_MUL_SUB = 6, /* c - a * b                                    */
+  FHE_EW_REDUCE = 7   /* a mod q_j (a any 64-bit word)  x % q_col      */
+};
+/* how operand b is addressed in fhe_ewise */
+enum {
+  FHE_B_FULL = 0,  /* same shape as a                                   */
+  FHE_B_BCAST = 1, /* one poly of `limbs` rows, broadcast over polys   */
+  FHE_B_CONST = 2  /* one word per chain position: b[mod_idx(row)]      */
+};
+
+const char* fhe_last_error(void);
+int fhe_device_sm_count(void);
+
+/* ---- chains: NttTables / NttChain precompute (coremath/ntt.py:52-137,
+ *      240-275; primes.py:60-71 for psi; rnspoly.py:47-67) ---------------- */
+int fhe_chain_create(const uint64_t* primes, int count, int log_n, FheChain** out);
+int fhe_chain_destroy(FheChain* ch);
+/* host copies of one prime's tables, for parity tests:
+ * psi (scalar), psi_br[N], ipsi_br[N], n_inv (scalar) */
+int fhe_chain_tables(const FheChain* ch, int idx, uint64_t* psi, uint64_t* psi_br,
+                     uint64_t* ipsi_br, uint64_t* n_inv);
+
+/* ---- batched NTT: NttChain.forward / .inverse (ntt.py:277-351),
+ *      _kernels.ntt_batch / intt_batch (_kernels.py:88-99).  In place over
+ *      `rows` contiguous rows of n words.  Row r uses chain position
+ *      mod_idx[r % limbs] + offset (mod_idx: device int32[limbs]; NULL means
+ *      the identity, i.e. (r % limbs) + offset; pass limbs = rows for a full
+ *      per-row map). */
+int fhe_ntt_fwd(const FheChain* ch, uint64_t* data, int64_t rows, const int32_t* mod_idx,
+                int limbs, int offset, void* stream);
+int fhe_ntt_inv(const FheChain* ch, uint64_t* data, int64_t rows, const int32_t* mod_idx,
+                int limbs, int offset, void* stream);
+
+/* ---- element-wise family: _kernels.mul_batch/neg_mul_batch/mul_add_batch
+ *      (_kernels.py:141-173), fused_neg_multiply / fused_mul_add
+ *      (rnspoly.py:295-308), add_arr/sub_arr/neg_arr (vecmod.py:155-165).
+ *      out may alias a, b or c. */
+int fhe_ewise(const FheChain* ch, int op, uint64_t* out, const uint64_t* a, const uint64_t* b,
+              const uint64_t* c, int64_t rows, const int32_t* mod_idx, int limbs, int offset,
+              int b_mode, void* stream);
+
+/* ---- fused tensor product: ckks_multiply / ckks_square (ckks.py:308-366),
+ *      bgv_multiply (bgv.py:171-186).  x, y: batch x (2, limbs, n);
+ *      out: batch x (3, limbs, n); strides in words between batch items. */
+int fhe_tensor(const FheChain* ch, uint64_t* out, const uint64_t* x, const uint64_t* y, int limbs,
+               int64_t batch, int64_t x_stride, int64_t y_stride, int64_t out_stride, int square,
+               void* stream);
+
+/* ---- Galois automorphism gather: _apply_galois (ckks.py:413-422) with the
+ *      index of Context.galois_perm (context.py:222-234).  out != in. */
+int fhe_automorph(uint64_t* out, const uint64_t* in, int64_t rows, int log_n, uint64_t elt,
+                  void* stream);
+
+/* ---- context: chain Q = q_0..q_{L-1} followed by P = p_0..p_{K-1};
+ *      key-switch digits of `alpha` consecutive Q primes.  (alpha=1, K=0)
+ *      is exactly the reference gadget (keys.py:1-7, 128-141, 186-237). */
+int fhe_context_create(const uint64_t* q_primes, int L, const uint64_t* p_primes, int K,
+                       int alpha, int log_n, FheContext** out);
+int fhe_context_destroy(FheContext* ctx);
+const FheChain* fhe_context_chain(const FheContext* ctx);
+
+/* ---- rescale: ckks_rescale (ckks.py:382-410); with t_plain != 0 the BGV
+ *      modulus switch (bgv.py:215-260).  in: (polys, level, n) eval;
+ *      out: (polys, level-1, n) eval; out must not alias in. */
+size_t fhe_rescale_workspace(const FheContext* ctx, int polys, int level);
+int fhe_rescale(const FheContext* ctx, uint64_t* out, const uint64_t* in, int polys, int level,
+                uint64_t t_plain, void* workspace, size_t ws_bytes, void* stream);
+
+/* ---- key switching: key_switch (keys.py:186-237) generalised to hybrid
+ *      (ModUp -> inner product -> ModDown).  d: batch x (level, n) eval,
+ *      stride d_stride words.  key: digits x (2, L+K, n) eval, contiguous.
+ *      out0 = add0 + b, out1 = add1 + a (add0/add1 may be NULL, may alias
+ *      out0/out1); batch items are add/out_stride words apart. */
+size_t fhe_keyswitch_workspace(const FheContext* ctx, int level, int batch);
+int fhe_keyswitch(const FheContext* ctx, int level, const uint64_t* d, int64_t d_stride,
+                  const uint64_t* key, const uint64_t* add0, const uint64_t* add1,
+                  uint64_t* out0, uint64_t* out1, int64_t io_stride, int batch, void* workspace,
+                  size_t ws_bytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FHE_SM100_H */

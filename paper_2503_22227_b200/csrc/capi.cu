@@ -1,0 +1,245 @@
+// extern "C" boundary (include/fhe_sm100.h).  Argument checking that needs
+// no device access happens here; everything else is forwarded to the
+// launchers, which enqueue asynchronously on the caller's stream.
+#include <exception>
+
+#include "fhe_context.cuh"
+
+static thread_local std::string g_err;
+
+void fhe_set_error(const std::string& msg) { g_err = msg; }
+
+#define FHE_TRY(body)                   \
+  try {                                 \
+    body                                \
+  } catch (const std::exception& e) {   \
+    fhe_set_error(e.what());            \
+    return -9;                          \
+  }
+
+extern "C" {
+
+const char* fhe_last_error(void) { return g_err.c_str(); }
+
+int fhe_device_sm_count(void) {
+  int dev = 0, n = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return -1;
+  if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return -1;
+  return n;
+}
+
+int fhe_chain_create(const uint64_t* primes, int count, int log_n, FheChain** out) {
+  FHE_TRY({
+    if (!out || !primes || count < 1 || log_n < 1 || log_n > 17) {
+      fhe_set_error("fhe_chain_create: bad arguments (need count >= 1, 1 <= log_n <= 17)");
+      return -1;
+    }
+    FheChain* ch = new FheChain();
+    int rc = build_chain(primes, count, log_n, ch);
+    if (rc) {
+      free_chain(ch);
+      delete ch;
+      return rc;
+    }
+    *out = ch;
+    return 0;
+  })
+}
+
+int fhe_chain_destroy(FheChain* ch) {
+  if (!ch) return 0;
+  free_chain(ch);
+  delete ch;
+  return 0;
+}
+
+int fhe_chain_tables(const FheChain* ch, int idx, uint64_t* psi, uint64_t* psi_br,
+                     uint64_t* ipsi_br, uint64_t* n_inv) {
+  if (!ch || idx < 0 || idx >= (int)ch->primes.size()) {
+    fhe_set_error("fhe_chain_tables: bad index");
+    return -1;
+  }
+  const size_t n = (size_t)1 << ch->log_n;
+  if (psi) *psi = ch->psi[idx];
+  std::vector<WPair> tmp(n);
+  if (psi_br) {
+    FHE_CUDA_CHECK(cudaMemcpy(tmp.data(), ch->dev.tw + idx * n, n * sizeof(WPair),
+                              cudaMemcpyDeviceToHost));
+    for (size_t i = 0; i < n; ++i) psi_br[i] = tmp[i].w;
+  }
+  if (ipsi_br) {
+    FHE_CUDA_CHECK(cudaMemcpy(tmp.data(), ch->dev.itw + idx * n, n * sizeof(WPair),
+                              cudaMemcpyDeviceToHost));
+    for (size_t i = 0; i < n; ++i) ipsi_br[i] = tmp[i].w;
+  }
+  if (n_inv) {
+    WPair w;
+    FHE_CUDA_CHECK(cudaMemcpy(&w, ch->dev.ninv + idx, sizeof(WPair), cudaMemcpyDeviceToHost));
+    *n_inv = w.w;
+  }
+  return 0;
+}
+
+static int check_map(const FheChain* ch, int64_t rows, const int32_t* mod_idx, int limbs,
+                     int offset) {
+  if (!ch) {
+    fhe_set_error("null chain");
+    return -1;
+  }
+  if (rows < 0 || rows > (int64_t)0x7fffffff) {
+    fhe_set_error("row count out of range");
+    return -1;
+  }
+  if (limbs < 1 || offset < 0 || (!mod_idx && offset + limbs > ch->dev.count)) {
+    fhe_set_error("limbs/offset exceed the chain length");
+    return -1;
+  }
+  return 0;
+}
+
+int fhe_ntt_fwd(const FheChain* ch, uint64_t* data, int64_t rows, const int32_t* mod_idx,
+                int limbs, int offset, void* stream) {
+  int rc = check_map(ch, rows, mod_idx, limbs, offset);
+  if (rc) return rc;
+  return launch_ntt(ch->dev, data, data, (int)rows, RowMap{mod_idx, limbs, offset}, false,
+                    (cudaStream_t)stream);
+}
+
+int fhe_ntt_inv(const FheChain* ch, uint64_t* data, int64_t rows, const int32_t* mod_idx,
+                int limbs, int offset, void* stream) {
+  int rc = check_map(ch, rows, mod_idx, limbs, offset);
+  if (rc) return rc;
+  return launch_ntt(ch->dev, data, data, (int)rows, RowMap{mod_idx, limbs, offset}, true,
+                    (cudaStream_t)stream);
+}
+
+int fhe_ewise(const FheChain* ch, int op, uint64_t* out, const uint64_t* a, const uint64_t* b,
+              const uint64_t* c, int64_t rows, const int32_t* mod_idx, int limbs, int offset,
+              int b_mode, void* stream) {
+  int rc = check_map(ch, rows, mod_idx, limbs, offset);
+  if (rc) return rc;
+  if (op < FHE_EW_ADD || op > FHE_EW_REDUCE) {
+    fhe_set_error("unknown element-wise op");
+    return -1;
+  }
+  const bool needs_b = !(op == FHE_EW_NEG || op == FHE_EW_REDUCE);
+  const bool needs_c = (op == FHE_EW_MUL_ADD || op == FHE_EW_MUL_SUB);
+  if (!out || !a || (needs_b && !b) || (needs_c && !c)) {
+    fhe_set_error("missing operand for element-wise op");
+    return -1;
+  }
+  if (b_mode == FHE_B_BCAST && mod_idx) {
+    fhe_set_error("broadcast operand requires the layout-order row map");
+    return -1;
+  }
+  if (ch->log_n < 1) {
+    fhe_set_error("element-wise ops need n >= 2");
+    return -1;
+  }
+  return launch_ewise(ch->dev, op, out, a, b, c, rows, RowMap{mod_idx, limbs, offset}, b_mode,
+                      (cudaStream_t)stream);
+}
+
+int fhe_tensor(const FheChain* ch, uint64_t* out, const uint64_t* x, const uint64_t* y, int limbs,
+               int64_t batch, int64_t x_stride, int64_t y_stride, int64_t out_stride, int square,
+               void* stream) {
+  if (!ch || limbs < 1 || limbs > ch->dev.count || !out || !x || (!square && !y)) {
+    fhe_set_error("fhe_tensor: bad arguments");
+    return -1;
+  }
+  return launch_tensor(ch->dev, out, x, y, limbs, batch, x_stride, y_stride, out_stride, square,
+                       (cudaStream_t)stream);
+}
+
+int fhe_automorph(uint64_t* out, const uint64_t* in, int64_t rows, int log_n, uint64_t elt,
+                  void* stream) {
+  if (!out || !in || out == in || log_n < 1 || log_n > 17 || !(elt & 1)) {
+    fhe_set_error("fhe_automorph: bad arguments (out != in, odd elt)");
+    return -1;
+  }
+  return launch_automorph(out, in, rows, log_n, elt, (cudaStream_t)stream);
+}
+
+int fhe_context_create(const uint64_t* q_primes, int L, const uint64_t* p_primes, int K,
+                       int alpha, int log_n, FheContext** out) {
+  FHE_TRY({
+    if (!out || !q_primes || L < 1 || K < 0 || (K > 0 && !p_primes) || alpha < 1 ||
+        log_n < 1 || log_n > 17) {
+      fhe_set_error("fhe_context_create: bad arguments");
+      return -1;
+    }
+    if (alpha > 16 || K > 16) {
+      fhe_set_error("fhe_context_create: alpha and K must be <= 16");
+      return -1;
+    }
+    std::vector<u64> all(q_primes, q_primes + L);
+    for (int k = 0; k < K; ++k) all.push_back(p_primes[k]);
+    FheContext* ctx = new FheContext();
+    ctx->L = L;
+    ctx->K = K;
+    ctx->alpha = alpha;
+    ctx->chain = new FheChain();
+    int rc = build_chain(all.data(), (int)all.size(), log_n, ctx->chain);
+    if (!rc) rc = build_levels(ctx);
+    if (rc) {
+      fhe_context_destroy(ctx);
+      return rc;
+    }
+    *out = ctx;
+    return 0;
+  })
+}
+
+int fhe_context_destroy(FheContext* ctx) {
+  if (!ctx) return 0;
+  for (auto& lp : ctx->levels)
+    if (lp.dmem) cudaFree(lp.dmem);
+  for (auto& kv : ctx->plain)
+    for (void* p : kv.second->dmem)
+      if (p) cudaFree(p);
+  if (ctx->chain) {
+    free_chain(ctx->chain);
+    delete ctx->chain;
+  }
+  delete ctx;
+  return 0;
+}
+
+const FheChain* fhe_context_chain(const FheContext* ctx) { return ctx ? ctx->chain : nullptr; }
+
+size_t fhe_rescale_workspace(const FheContext* ctx, int polys, int level) {
+  return ctx ? rescale_workspace(*ctx, polys, level) : 0;
+}
+
+int fhe_rescale(const FheContext* ctx, uint64_t* out, const uint64_t* in, int polys, int level,
+                uint64_t t_plain, void* workspace, size_t ws_bytes, void* stream) {
+  if (!ctx || !out || !in || out == in || polys < 1) {
+    fhe_set_error("fhe_rescale: bad arguments");
+    return -1;
+  }
+  FHE_TRY({
+    return run_rescale(*const_cast<FheContext*>(ctx), out, in, polys, level, t_plain, workspace,
+                       ws_bytes, (cudaStream_t)stream);
+  })
+}
+
+size_t fhe_keyswitch_workspace(const FheContext* ctx, int level, int batch) {
+  if (!ctx || level < 1 || level > ctx->L || batch < 1) return 0;
+  return keyswitch_workspace(*ctx, level, batch);
+}
+
+int fhe_keyswitch(const FheContext* ctx, int level, const uint64_t* d, int64_t d_stride,
+                  const uint64_t* key, const uint64_t* add0, const uint64_t* add1,
+                  uint64_t* out0, uint64_t* out1, int64_t io_stride, int batch, void* workspace,
+                  size_t ws_bytes, void* stream) {
+  if (!ctx || !d || !key || !out0 || !out1 || batch < 1) {
+    fhe_set_error("fhe_keyswitch: bad arguments");
+    return -1;
+  }
+  FHE_TRY({
+    return run_keyswitch(*ctx, level, d, d_stride, key, add0, add1, out0, out1, io_stride, batch,
+                         workspace, ws_bytes, (cudaStream_t)stream);
+  })
+}
+
+}  // extern "C"

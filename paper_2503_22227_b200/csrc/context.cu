@@ -1,0 +1,275 @@
+// Host precompute for chains and contexts, uploaded once to HBM.
+//
+// Mirrors the reference's one-off precompute:
+//   NttTables (coremath/ntt.py:52-137): psi = smallest primitive 2N-th root
+//     (primes.py:60-71), bit-reversed powers of psi and psi^-1, Shoup
+//     companions floor(w 2^64 / q) (vecmod.py:141-145), n^-1;
+//   Context.last_inv (context.py:186-198) for rescale;
+//   key-switch constants: for the hybrid gadget the punctured products of
+//     each digit (the fast-base-conversion weights of behz.py:131-153 applied
+//     to Q_d and to P); for (alpha=1, K=0) they degenerate to the identity,
+//     which is the reference's per-prime gadget (keys.py:186-237).
+// All arithmetic is exact unsigned __int128 host code.
+#include <algorithm>
+#include <cstring>
+#include <stdexcept>
+
+#include "fhe_context.cuh"
+
+namespace {
+
+typedef unsigned __int128 u128;
+
+u64 mulmod_h(u64 a, u64 b, u64 q) { return (u64)((u128)a * b % q); }
+u64 powmod_h(u64 a, u64 e, u64 q) {
+  u64 r = 1 % q;
+  a %= q;
+  while (e) {
+    if (e & 1) r = mulmod_h(r, a, q);
+    a = mulmod_h(a, a, q);
+    e >>= 1;
+  }
+  return r;
+}
+u64 invmod_h(u64 a, u64 q) {
+  if (a % q == 0) throw std::runtime_error("non-invertible value");
+  return powmod_h(a, q - 2, q);
+}
+u64 shoup_h(u64 w, u64 q) { return (u64)(((u128)w << 64) / q); }
+WPair wpair(u64 w, u64 q) { return WPair{w, shoup_h(w, q)}; }
+int bitlen(u64 x) { return 64 - __builtin_clzll(x); }
+
+ModConst make_mc(u64 q) {
+  ModConst m;
+  m.q = q;
+  m.s = (u32)(bitlen(q) - 1);
+  m.mu = (u64)(((u128)1 << (64 + m.s)) / q);
+  m.r64 = (u64)(((u128)1 << 64) % q);
+  m.pad = 0;
+  return m;
+}
+
+u32 bitrev(u32 x, int bits) {
+  u32 r = 0;
+  for (int i = 0; i < bits; ++i) {
+    r = (r << 1) | (x & 1);
+    x >>= 1;
+  }
+  return r;
+}
+
+// primes.py:45-71: first g whose cofactor power is a primitive root, then
+// the numerically smallest odd power of it.
+u64 min_primitive_root_h(u64 q, u64 order) {
+  if ((q - 1) % order != 0) throw std::runtime_error("prime is not NTT friendly for this degree");
+  const u64 cof = (q - 1) / order;
+  u64 root = 0;
+  for (u64 g = 2; g < q; ++g) {
+    const u64 r = powmod_h(g, cof, q);
+    if (powmod_h(r, order / 2, q) == q - 1) {
+      root = r;
+      break;
+    }
+  }
+  if (!root) throw std::runtime_error("no primitive root");
+  u64 best = root, cur = root;
+  const u64 gsq = mulmod_h(root, root, q);
+  for (u64 k = 0; k + 1 < order / 2; ++k) {
+    cur = mulmod_h(cur, gsq, q);
+    if (cur < best) best = cur;
+  }
+  return best;
+}
+
+// simple bump allocator for packing constants into one device upload
+struct Packer {
+  std::vector<unsigned char> buf;
+  size_t add(const void* p, size_t bytes) {
+    size_t off = (buf.size() + 255) & ~(size_t)255;
+    buf.resize(off + bytes);
+    if (bytes) std::memcpy(buf.data() + off, p, bytes);
+    return off;
+  }
+  template <class T>
+  size_t addv(const std::vector<T>& v) {
+    return add(v.data(), v.size() * sizeof(T));
+  }
+};
+
+}  // namespace
+
+int build_chain(const u64* primes, int count, int log_n, FheChain* ch) {
+  const size_t n = (size_t)1 << log_n;
+  ch->log_n = log_n;
+  ch->primes.assign(primes, primes + count);
+  ch->psi.resize(count);
+  std::vector<ModConst> mc(count);
+  std::vector<WPair> tw(count * n), itw(count * n), ninv(count), ninv_w1(count);
+  for (int p = 0; p < count; ++p) {
+    const u64 q = primes[p];
+    if (q < 3 || q >= ((u64)1 << 62) || !(q & 1)) {
+      fhe_set_error("modulus out of supported range [3, 2^62) or even");
+      return -1;
+    }
+    mc[p] = make_mc(q);
+    u64 psi;
+    try {
+      psi = min_primitive_root_h(q, 2 * n);
+    } catch (const std::exception& e) {
+      fhe_set_error(e.what());
+      return -1;
+    }
+    ch->psi[p] = psi;
+    const u64 ipsi = invmod_h(psi, q);
+    std::vector<u64> fw(n), iv(n);
+    u64 a = 1, ia = 1;
+    for (size_t i = 0; i < n; ++i) {
+      fw[i] = a;
+      iv[i] = ia;
+      a = mulmod_h(a, psi, q);
+      ia = mulmod_h(ia, ipsi, q);
+    }
+    for (size_t i = 0; i < n; ++i) {
+      const u32 br = bitrev((u32)i, log_n);
+      tw[p * n + i] = wpair(fw[br], q);
+      itw[p * n + i] = wpair(iv[br], q);
+    }
+    const u64 ni = invmod_h(n % q, q);
+    ninv[p] = wpair(ni, q);
+    const u64 w1 = n >= 2 ? itw[p * n + 1].w : 1;
+    ninv_w1[p] = wpair(mulmod_h(w1, ni, q), q);
+  }
+  Packer pk;
+  const size_t o_mc = pk.addv(mc), o_tw = pk.addv(tw), o_itw = pk.addv(itw),
+               o_ni = pk.addv(ninv), o_nw = pk.addv(ninv_w1);
+  void* d = nullptr;
+  FHE_CUDA_CHECK(cudaMalloc(&d, pk.buf.size()));
+  FHE_CUDA_CHECK(cudaMemcpy(d, pk.buf.data(), pk.buf.size(), cudaMemcpyHostToDevice));
+  unsigned char* b = (unsigned char*)d;
+  ch->dmem = d;
+  ch->dbytes = pk.buf.size();
+  ch->dev.count = count;
+  ch->dev.log_n = log_n;
+  ch->dev.mc = (const ModConst*)(b + o_mc);
+  ch->dev.tw = (const WPair*)(b + o_tw);
+  ch->dev.itw = (const WPair*)(b + o_itw);
+  ch->dev.ninv = (const WPair*)(b + o_ni);
+  ch->dev.ninv_w1 = (const WPair*)(b + o_nw);
+  return 0;
+}
+
+void free_chain(FheChain* ch) {
+  if (ch && ch->dmem) cudaFree(ch->dmem);
+  if (ch) ch->dmem = nullptr;
+}
+
+// Product of primes[idx] for idx in [lo, hi) except `skip`, reduced mod m.
+static u64 punct_mod(const std::vector<u64>& primes, int lo, int hi, int skip, u64 m) {
+  u64 r = 1 % m;
+  for (int i = lo; i < hi; ++i)
+    if (i != skip) r = mulmod_h(r, primes[i] % m, m);
+  return r;
+}
+
+int build_levels(FheContext* ctx) {
+  const int L = ctx->L, K = ctx->K, A = ctx->alpha;
+  const std::vector<u64>& pr = ctx->chain->primes;  // Q then P
+  ctx->levels.resize(L + 1);
+  for (int l = 1; l <= L; ++l) {
+    LevelPlan& lp = ctx->levels[l];
+    lp.level = l;
+    lp.digits = (l + A - 1) / A;
+    const int D = lp.digits;
+    std::vector<WPair> up_inv(l);
+    std::vector<u64> up_w;
+    std::vector<int32_t> ext_prime;
+    std::vector<int> info(4 * D);
+    int row_off = 0;
+    auto cp = [&](int m) { return m < l ? m : L + (m - l); };
+    for (int di = 0; di < D; ++di) {
+      const int s0 = di * A, na = std::min(A, l - s0), nt = l + K - na;
+      lp.dig_s0.push_back(s0);
+      lp.dig_na.push_back(na);
+      lp.dig_row_off.push_back(row_off);
+      lp.dig_w_off.push_back((int)up_w.size());
+      info[4 * di + 0] = s0;
+      info[4 * di + 1] = na;
+      info[4 * di + 2] = row_off;
+      info[4 * di + 3] = (int)up_w.size();
+      for (int s = s0; s < s0 + na; ++s)
+        up_inv[s] = wpair(invmod_h(punct_mod(pr, s0, s0 + na, s, pr[s]), pr[s]), pr[s]);
+      for (int s = s0; s < s0 + na; ++s)
+        for (int t = 0; t < nt; ++t) {
+          const int m = t < s0 ? t : t + na;
+          up_w.push_back(punct_mod(pr, s0, s0 + na, s, pr[cp(m)]));
+        }
+      for (int t = 0; t < nt; ++t) {
+        const int m = t < s0 ? t : t + na;
+        ext_prime.push_back(cp(m));
+      }
+      row_off += nt;
+    }
+    lp.ext_rows = row_off;
+    std::vector<WPair> down_inv(K), p_inv(l);
+    std::vector<u64> down_w((size_t)K * l);
+    for (int k = 0; k < K; ++k) {
+      const u64 pk = pr[L + k];
+      down_inv[k] = wpair(invmod_h(punct_mod(pr, L, L + K, L + k, pk), pk), pk);
+      for (int j = 0; j < l; ++j) down_w[(size_t)k * l + j] = punct_mod(pr, L, L + K, L + k, pr[j]);
+    }
+    for (int j = 0; j < l; ++j) {
+      const u64 pm = punct_mod(pr, L, L + K, -1, pr[j]);
+      p_inv[j] = wpair(invmod_h(pm, pr[j]), pr[j]);
+    }
+    std::vector<WPair> rs_inv(std::max(l - 1, 0));
+    std::vector<u64> rs_qlast(std::max(l - 1, 0));
+    for (int j = 0; j + 1 < l; ++j) {
+      rs_inv[j] = wpair(invmod_h(pr[l - 1] % pr[j], pr[j]), pr[j]);
+      rs_qlast[j] = pr[l - 1] % pr[j];
+    }
+    Packer pk;
+    const size_t o1 = pk.addv(up_inv), o2 = pk.addv(up_w), o3 = pk.addv(ext_prime),
+                 o4 = pk.addv(info), o5 = pk.addv(down_inv), o6 = pk.addv(down_w),
+                 o7 = pk.addv(p_inv), o8 = pk.addv(rs_inv), o9 = pk.addv(rs_qlast);
+    void* d = nullptr;
+    FHE_CUDA_CHECK(cudaMalloc(&d, pk.buf.size()));
+    FHE_CUDA_CHECK(cudaMemcpy(d, pk.buf.data(), pk.buf.size(), cudaMemcpyHostToDevice));
+    unsigned char* b = (unsigned char*)d;
+    lp.dmem = d;
+    lp.up_inv = (const WPair*)(b + o1);
+    lp.up_w = (const u64*)(b + o2);
+    lp.ext_prime = (const int32_t*)(b + o3);
+    lp.dig_info = (const int*)(b + o4);
+    lp.down_inv = (const WPair*)(b + o5);
+    lp.down_w = (const u64*)(b + o6);
+    lp.p_inv = (const WPair*)(b + o7);
+    lp.rs_inv = (const WPair*)(b + o8);
+    lp.rs_qlast = (const u64*)(b + o9);
+  }
+  return 0;
+}
+
+const PlainPlan* get_plain_plan(FheContext* ctx, u64 t) {
+  std::lock_guard<std::mutex> g(ctx->plain_mu);
+  auto it = ctx->plain.find(t);
+  if (it != ctx->plain.end()) return it->second.get();
+  auto pp = std::make_unique<PlainPlan>();
+  const std::vector<u64>& pr = ctx->chain->primes;
+  pp->dmem.assign(ctx->L + 1, nullptr);
+  pp->t_mod.assign(ctx->L + 1, nullptr);
+  pp->tinv_last.assign(ctx->L + 1, WPair{0, 0});
+  for (int l = 2; l <= ctx->L; ++l) {
+    std::vector<u64> tm(l - 1);
+    for (int j = 0; j + 1 < l; ++j) tm[j] = t % pr[j];
+    const u64 ql = pr[l - 1];
+    pp->tinv_last[l] = wpair(invmod_h(t % ql, ql), ql);
+    void* d = nullptr;
+    if (cudaMalloc(&d, tm.size() * 8) != cudaSuccess) return nullptr;
+    cudaMemcpy(d, tm.data(), tm.size() * 8, cudaMemcpyHostToDevice);
+    pp->dmem[l] = d;
+    pp->t_mod[l] = (const u64*)d;
+  }
+  PlainPlan* raw = pp.get();
+  ctx->plain[t] = std::move(pp);
+  return raw;
+}

@@ -1,0 +1,66 @@
+// Host-side objects behind the opaque C-ABI handles.
+#pragma once
+#include <map>
+#include <memory>
+#include <mutex>
+#include <vector>
+
+#include "fhe_kernels.cuh"
+
+struct FheChain {
+  DevChain dev{};
+  int log_n = 0;
+  std::vector<u64> primes;
+  std::vector<u64> psi;  // smallest primitive 2N-th root per prime
+  void* dmem = nullptr;  // one allocation for all tables
+  size_t dbytes = 0;
+};
+
+// Per-level key-switch and rescale constants, resident in HBM.
+// Level l = number of active Q primes (1..L).
+struct LevelPlan {
+  int level = 0;
+  int digits = 0;        // active digits D = ceil(l / alpha)
+  int ext_rows = 0;      // sum over digits of (l + K - |digit|)
+  std::vector<int> dig_s0, dig_na, dig_row_off, dig_w_off;
+  // device pointers into LevelPlan::dmem
+  const WPair* up_inv = nullptr;     // [l]   ((Q_d / q_s)^-1 mod q_s) per Q prime
+  const u64* up_w = nullptr;         // per digit [na][l+K-na]: [Q_d/q_s] mod target
+  const int32_t* ext_prime = nullptr;  // [ext_rows] chain position of each ext row
+  const int* dig_info = nullptr;     // [4*digits] s0, na, row_off, w_off
+  const WPair* down_inv = nullptr;   // [K] (P/p_k)^-1 mod p_k
+  const u64* down_w = nullptr;       // [K][l] [P/p_k] mod q_j
+  const WPair* p_inv = nullptr;      // [l] P^-1 mod q_j
+  const WPair* rs_inv = nullptr;     // [l-1] q_{l-1}^-1 mod q_j
+  const u64* rs_qlast = nullptr;     // [l-1] q_{l-1} mod q_j
+  void* dmem = nullptr;
+};
+
+// BGV modulus-switch constants for one plain modulus t.
+struct PlainPlan {
+  std::vector<void*> dmem;                 // per level
+  std::vector<const u64*> t_mod;           // per level: [l-1] t mod q_j
+  std::vector<WPair> tinv_last;            // per level: t^-1 mod q_{l-1}
+};
+
+struct FheContext {
+  FheChain* chain = nullptr;  // Q then P
+  int L = 0, K = 0, alpha = 1;
+  std::vector<LevelPlan> levels;  // index l (0 unused)
+  std::mutex plain_mu;
+  std::map<u64, std::unique_ptr<PlainPlan>> plain;
+};
+
+int build_chain(const u64* primes, int count, int log_n, FheChain* ch);
+int build_levels(FheContext* ctx);
+void free_chain(FheChain* ch);
+const PlainPlan* get_plain_plan(FheContext* ctx, u64 t);
+
+// keyswitch.cu
+size_t keyswitch_workspace(const FheContext& ctx, int level, int batch);
+int run_keyswitch(const FheContext& ctx, int level, const u64* d, long d_stride, const u64* key,
+                  const u64* add0, const u64* add1, u64* out0, u64* out1, long io_stride,
+                  int batch, void* ws, size_t ws_bytes, cudaStream_t st);
+size_t rescale_workspace(const FheContext& ctx, int polys, int level);
+int run_rescale(FheContext& ctx, u64* out, const u64* in, int polys, int level, u64 t_plain,
+                void* ws, size_t ws_bytes, cudaStream_t st);

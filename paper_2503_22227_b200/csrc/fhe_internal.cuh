@@ -1,0 +1,65 @@
+// Internal device-side structures shared by the kernels and the C-ABI layer.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string>
+#include <vector>
+
+#include "modarith.cuh"
+
+// Shoup pair: a constant and its floor(w * 2^64 / q) companion, loaded with a
+// single 16-byte access.
+struct __align__(16) WPair {
+  u64 w;
+  u64 sh;
+};
+
+// NTT tables for one modulus chain, resident in HBM (built once per context).
+// Forward twiddles follow coremath/ntt.py:86-98 (powers of the smallest
+// primitive 2N-th root psi in bit-reversed order, plus Shoup companions);
+// inverse twiddles are the bit-reversed powers of psi^-1.
+struct DevChain {
+  int count;             // primes in the chain
+  int log_n;
+  const ModConst* mc;    // [count]
+  const WPair* tw;       // [count][N]   (psi_br[i], shoup)
+  const WPair* itw;      // [count][N]   (ipsi_br[i], shoup)
+  const WPair* ninv;     // [count]      (n^-1, shoup)
+  const WPair* ninv_w1;  // [count]      (ipsi_br[1] * n^-1, shoup)
+};
+
+// Row -> chain position mapping used by every batched kernel.  The
+// reference passes an explicit per-row mod_idx (coremath/ntt.py:257-264);
+// here a NULL pointer means the layout-order pattern (row % limbs) + offset
+// that CData.mod_idx() produces (rnspoly.py:109-111).
+struct RowMap {
+  const int32_t* idx;  // device int32[limbs], may be null (identity)
+  int limbs;
+  int offset;
+  __device__ __forceinline__ int operator()(int row) const {
+    const int r = row % limbs;
+    return (idx ? idx[r] : r) + offset;
+  }
+};
+
+// thread-local error text for fhe_last_error()
+void fhe_set_error(const std::string& msg);
+
+#define FHE_CUDA_CHECK(expr)                                                   \
+  do {                                                                         \
+    cudaError_t _e = (expr);                                                   \
+    if (_e != cudaSuccess) {                                                   \
+      fhe_set_error(std::string(#expr) + ": " + cudaGetErrorString(_e));       \
+      return -2;                                                               \
+    }                                                                          \
+  } while (0)
+
+#define FHE_LAUNCH_CHECK()                                                     \
+  do {                                                                         \
+    cudaError_t _e = cudaGetLastError();                                       \
+    if (_e != cudaSuccess) {                                                   \
+      fhe_set_error(std::string("kernel launch: ") + cudaGetErrorString(_e));  \
+      return -3;                                                               \
+    }                                                                          \
+  } while (0)
+

@@ -1,0 +1,337 @@
+// Key switching (ModUp -> key inner product -> ModDown) and rescale on the
+// device.
+//
+// Reference: key_switch (keys.py:186-237) is the per-prime gadget: INTT the
+// input, re-reduce every residue polynomial against every prime of the level
+// (digit_rows[i, j] = coeff[i] mod q_j), NTT the level^2 rows, multiply-
+// accumulate against the level digit keys.  That is the hybrid algorithm with
+// alpha = 1 and no special modulus (K = 0):
+//   ModUp     digit d (primes S_d): y_s = [c_s (Q_d/q_s)^-1]_{q_s},
+//             ext_m = sum_s y_s [Q_d/q_s]_m   (fast base conversion, the
+//             formula of behz.py:131-153); with alpha = 1, ext_m = c_s mod m.
+//   inner     b_m = sum_d ext_d,m * kb_d,m ; a_m = sum_d ext_d,m * ka_d,m
+//   ModDown   (K > 0): b_j <- (b_j - BConv_{P->q_j}(b_P)) * P^-1  (same for a)
+// The digit's own primes are not converted: their evaluation-domain values
+// are the input itself, so the INTT/NTT round trip of the reference
+// (NTT(INTT(d) mod q_i) = d) is skipped without changing a bit.
+#include "fhe_context.cuh"
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kMaxAlpha = 16;
+
+// Reduce a chain of multiply-accumulates every `chunk` terms so the 128-bit
+// accumulator stays below 2^126 (reduce_fold's domain).
+struct Acc {
+  u64 hi = 0, lo = 0, r = 0;
+  int cnt = 0;
+  __device__ __forceinline__ void mac(u64 a, u64 b, int chunk, const ModConst& m) {
+    mac_wide(hi, lo, a, b);
+    if (++cnt == chunk) {
+      r = add_mod(r, reduce_fold(hi, lo, m), m.q);
+      hi = lo = 0;
+      cnt = 0;
+    }
+  }
+  __device__ __forceinline__ u64 done(const ModConst& m) {
+    return cnt ? add_mod(r, reduce_fold(hi, lo, m), m.q) : r;
+  }
+};
+
+// ModUp basis extension of one digit: grid (coef blocks, digits, batch).
+__global__ void __launch_bounds__(kThreads)
+    modup_kernel(const DevChain ch, const u64* __restrict__ c, long c_stride,
+                 u64* __restrict__ ext, long ext_stride, const int* __restrict__ dig_info,
+                 const WPair* __restrict__ up_inv, const u64* __restrict__ up_w, int level, int K,
+                 int L, int chunk) {
+  const int di = blockIdx.y, b = blockIdx.z;
+  const int s0 = dig_info[4 * di], na = dig_info[4 * di + 1];
+  const int row_off = dig_info[4 * di + 2], w_off = dig_info[4 * di + 3];
+  const int nt = level + K - na;
+  extern __shared__ u64 sw[];
+  for (int i = threadIdx.x; i < na * nt; i += blockDim.x) sw[i] = up_w[w_off + i];
+  __syncthreads();
+  const int log_n = ch.log_n;
+  const long n = 1L << log_n;
+  const u64* cb = c + b * c_stride;
+  u64* eb = ext + b * ext_stride + (long)row_off * n;
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n;
+       i += (long)gridDim.x * blockDim.x) {
+    u64 y[kMaxAlpha];
+#pragma unroll
+    for (int s = 0; s < kMaxAlpha; ++s) {
+      if (s < na) {
+        const WPair w = up_inv[s0 + s];
+        y[s] = shoup_mul(cb[(long)(s0 + s) * n + i], w.w, w.sh, ch.mc[s0 + s].q);
+      }
+    }
+    for (int t = 0; t < nt; ++t) {
+      const int m = t < s0 ? t : t + na;
+      const int p = m < level ? m : L + (m - level);
+      const ModConst mc = ch.mc[p];
+      Acc acc;
+#pragma unroll
+      for (int s = 0; s < kMaxAlpha; ++s)
+        if (s < na) acc.mac(y[s], sw[s * nt + t], chunk, mc);
+      eb[(long)t * n + i] = acc.done(mc);
+    }
+  }
+}
+
+// Key inner product over all digits: one thread per (target limb m, coeff i).
+__global__ void __launch_bounds__(kThreads)
+    ks_inner_kernel(const DevChain ch, const u64* __restrict__ d, long d_stride,
+                    const u64* __restrict__ ext, long ext_stride, const u64* __restrict__ key,
+                    int keyL, const int* __restrict__ dig_info, int D, int level, int K, int L,
+                    u64* __restrict__ accQ, u64* __restrict__ accP, const u64* add0,
+                    const u64* add1, u64* out0, u64* out1, long io_stride, int batch,
+                    int chunk) {
+  extern __shared__ int sinfo[];
+  for (int i = threadIdx.x; i < 4 * D; i += blockDim.x) sinfo[i] = dig_info[i];
+  __syncthreads();
+  const int log_n = ch.log_n;
+  const long n = 1L << log_n;
+  const long total = (long)(level + K) << log_n;
+  for (long t = blockIdx.x * (long)blockDim.x + threadIdx.x; t < total;
+       t += (long)gridDim.x * blockDim.x) {
+    const int m = (int)(t >> log_n);
+    const long i = t & (n - 1);
+    const int p = m < level ? m : L + (m - level);
+    const ModConst mc = ch.mc[p];
+    for (int b = 0; b < batch; ++b) {
+      Acc ab, aa;
+      for (int di = 0; di < D; ++di) {
+        const int s0 = sinfo[4 * di], na = sinfo[4 * di + 1], ro = sinfo[4 * di + 2];
+        u64 v;
+        if (m >= s0 && m < s0 + na) {
+          v = d[b * d_stride + (long)m * n + i];
+        } else {
+          const int row = ro + (m < s0 ? m : m - na);
+          v = ext[b * ext_stride + (long)row * n + i];
+        }
+        const u64 kb = key[((long)(2 * di) * keyL + p) * n + i];
+        const u64 ka = key[((long)(2 * di + 1) * keyL + p) * n + i];
+        ab.mac(v, kb, chunk, mc);
+        aa.mac(v, ka, chunk, mc);
+      }
+      const u64 rb = ab.done(mc), ra = aa.done(mc);
+      if (K == 0) {
+        const long o = b * io_stride + (long)m * n + i;
+        out0[o] = add0 ? add_mod(add0[o], rb, mc.q) : rb;
+        out1[o] = add1 ? add_mod(add1[o], ra, mc.q) : ra;
+      } else if (m < level) {
+        accQ[((long)(b * 2 + 0) * level + m) * n + i] = rb;
+        accQ[((long)(b * 2 + 1) * level + m) * n + i] = ra;
+      } else {
+        accP[((long)(b * 2 + 0) * K + (m - level)) * n + i] = rb;
+        accP[((long)(b * 2 + 1) * K + (m - level)) * n + i] = ra;
+      }
+    }
+  }
+}
+
+// ModDown base conversion P -> Q_level: grid (coef blocks, batch*2).
+__global__ void __launch_bounds__(kThreads)
+    moddown_conv_kernel(const DevChain ch, const u64* __restrict__ accP, u64* __restrict__ conv,
+                        const WPair* __restrict__ down_inv, const u64* __restrict__ down_w,
+                        int level, int K, int L, int chunk) {
+  extern __shared__ u64 sw[];
+  for (int i = threadIdx.x; i < K * level; i += blockDim.x) sw[i] = down_w[i];
+  __syncthreads();
+  const int bp = blockIdx.y;
+  const int log_n = ch.log_n;
+  const long n = 1L << log_n;
+  const u64* src = accP + (long)bp * K * n;
+  u64* dst = conv + (long)bp * level * n;
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n;
+       i += (long)gridDim.x * blockDim.x) {
+    u64 y[kMaxAlpha];
+#pragma unroll
+    for (int k = 0; k < kMaxAlpha; ++k) {
+      if (k < K) {
+        const WPair w = down_inv[k];
+        y[k] = shoup_mul(src[(long)k * n + i], w.w, w.sh, ch.mc[L + k].q);
+      }
+    }
+    for (int j = 0; j < level; ++j) {
+      const ModConst mc = ch.mc[j];
+      Acc acc;
+#pragma unroll
+      for (int k = 0; k < kMaxAlpha; ++k)
+        if (k < K) acc.mac(y[k], sw[k * level + j], chunk, mc);
+      dst[(long)j * n + i] = acc.done(mc);
+    }
+  }
+}
+
+// out_p = add_p + (accQ_p - conv_p) * P^-1, p in {0 (b), 1 (a)}.
+__global__ void __launch_bounds__(kThreads)
+    moddown_finish_kernel(const DevChain ch, const u64* __restrict__ accQ,
+                          const u64* __restrict__ conv, const WPair* __restrict__ p_inv,
+                          const u64* add0, const u64* add1, u64* out0, u64* out1, long io_stride,
+                          int level, int batch) {
+  const int log_n = ch.log_n;
+  const long n = 1L << log_n;
+  const long per = (long)level << log_n;
+  const long total = (long)batch * 2 * per;
+  for (long t = blockIdx.x * (long)blockDim.x + threadIdx.x; t < total;
+       t += (long)gridDim.x * blockDim.x) {
+    const long bp = t / per;
+    const long w = t - bp * per;
+    const int j = (int)(w >> log_n);
+    const int b = (int)(bp >> 1), poly = (int)(bp & 1);
+    const u64 q = ch.mc[j].q;
+    const WPair pi = p_inv[j];
+    const u64 v = shoup_mul(sub_mod(accQ[t], conv[t], q), pi.w, pi.sh, q);
+    const long o = b * io_stride + w;
+    const u64* add = poly ? add1 : add0;
+    u64* out = poly ? out1 : out0;
+    out[o] = add ? add_mod(add[o], v, q) : v;
+  }
+}
+
+int mac_chunk(const std::vector<u64>& primes) {
+  u64 mx = 0;
+  for (u64 p : primes) mx = p > mx ? p : mx;
+  const int bits = 64 - __builtin_clzll(mx);
+  const int room = 126 - 2 * bits;  // accumulator headroom in bits
+  if (room >= 20) return 1 << 20;
+  return room <= 0 ? 1 : (1 << room);
+}
+
+}  // namespace
+
+size_t keyswitch_workspace(const FheContext& ctx, int level, int batch) {
+  const LevelPlan& lp = ctx.levels[level];
+  const size_t n = (size_t)1 << ctx.chain->log_n;
+  size_t rows = (size_t)batch * (level + lp.ext_rows);
+  if (ctx.K > 0) rows += (size_t)batch * (2 * level + 2 * ctx.K + 2 * level);
+  return rows * n * sizeof(u64);
+}
+
+int run_keyswitch(const FheContext& ctx, int level, const u64* d, long d_stride, const u64* key,
+                  const u64* add0, const u64* add1, u64* out0, u64* out1, long io_stride,
+                  int batch, void* ws, size_t ws_bytes, cudaStream_t st) {
+  if (level < 1 || level > ctx.L) {
+    fhe_set_error("keyswitch level out of range");
+    return -1;
+  }
+  if (ctx.alpha > kMaxAlpha || ctx.K > kMaxAlpha) {
+    fhe_set_error("alpha and K must be <= 16");
+    return -1;
+  }
+  if (ws_bytes < keyswitch_workspace(ctx, level, batch)) {
+    fhe_set_error("keyswitch workspace too small");
+    return -1;
+  }
+  const LevelPlan& lp = ctx.levels[level];
+  const DevChain& ch = ctx.chain->dev;
+  const int log_n = ch.log_n, K = ctx.K, L = ctx.L;
+  const long n = 1L << log_n;
+  const int chunk = mac_chunk(ctx.chain->primes);
+  u64* c = (u64*)ws;
+  u64* ext = c + (long)batch * level * n;
+  u64* accQ = ext + (long)batch * lp.ext_rows * n;
+  u64* accP = accQ + (long)batch * 2 * level * n;
+  u64* conv = accP + (long)batch * 2 * K * n;
+  int rc;
+  // 1. coefficient form of the input
+  if (d_stride == (long)level * n) {
+    rc = launch_ntt(ch, c, d, batch * level, RowMap{nullptr, level, 0}, true, st);
+    if (rc) return rc;
+  } else {
+    for (int b = 0; b < batch; ++b) {
+      rc = launch_ntt(ch, c + (long)b * level * n, d + b * d_stride, level,
+                      RowMap{nullptr, level, 0}, true, st);
+      if (rc) return rc;
+    }
+  }
+  // 2. ModUp: basis extension of every digit, then NTT of the extended rows
+  {
+    int max_w = 0;
+    for (int di = 0; di < lp.digits; ++di)
+      max_w = std::max(max_w, lp.dig_na[di] * (level + K - lp.dig_na[di]));
+    const size_t smem = (size_t)max_w * sizeof(u64);
+    dim3 grid((unsigned)std::max<long>(1, std::min<long>(n / kThreads, 1024)), lp.digits, batch);
+    if (smem > 48 * 1024)
+      cudaFuncSetAttribute(modup_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    modup_kernel<<<grid, kThreads, smem, st>>>(ch, c, (long)level * n, ext,
+                                               (long)lp.ext_rows * n, lp.dig_info, lp.up_inv,
+                                               lp.up_w, level, K, L, chunk);
+    FHE_LAUNCH_CHECK();
+    if (lp.ext_rows > 0) {
+      rc = launch_ntt(ch, ext, ext, batch * lp.ext_rows,
+                      RowMap{lp.ext_prime, lp.ext_rows, 0}, false, st);
+      if (rc) return rc;
+    }
+  }
+  // 3. inner product with the key digits (K == 0 writes the result directly)
+  {
+    const long work = (long)(level + K) << log_n;
+    ks_inner_kernel<<<grid_for(work), kThreads, 4 * lp.digits * sizeof(int), st>>>(
+        ch, d, d_stride, ext, (long)lp.ext_rows * n, key, L + K, lp.dig_info, lp.digits, level,
+        K, L, accQ, accP, add0, add1, out0, out1, io_stride, batch, chunk);
+    FHE_LAUNCH_CHECK();
+  }
+  if (K == 0) return 0;
+  // 4. ModDown
+  rc = launch_ntt(ch, accP, accP, batch * 2 * K, RowMap{nullptr, K, L}, true, st);
+  if (rc) return rc;
+  {
+    const size_t smem = (size_t)K * level * sizeof(u64);
+    dim3 grid((unsigned)std::max<long>(1, std::min<long>(n / kThreads, 1024)), batch * 2);
+    moddown_conv_kernel<<<grid, kThreads, smem, st>>>(ch, accP, conv, lp.down_inv, lp.down_w,
+                                                      level, K, L, chunk);
+    FHE_LAUNCH_CHECK();
+  }
+  rc = launch_ntt(ch, conv, conv, batch * 2 * level, RowMap{nullptr, level, 0}, false, st);
+  if (rc) return rc;
+  moddown_finish_kernel<<<grid_for((long)batch * 2 * level * n), kThreads, 0, st>>>(
+      ch, accQ, conv, lp.p_inv, add0, add1, out0, out1, io_stride, level, batch);
+  FHE_LAUNCH_CHECK();
+  return 0;
+}
+
+size_t rescale_workspace(const FheContext& ctx, int polys, int level) {
+  const size_t n = (size_t)1 << ctx.chain->log_n;
+  return (size_t)polys * level * n * sizeof(u64);
+}
+
+int run_rescale(FheContext& ctx, u64* out, const u64* in, int polys, int level, u64 t_plain,
+                void* ws, size_t ws_bytes, cudaStream_t st) {
+  if (level < 2 || level > ctx.L) {
+    fhe_set_error("rescale needs 2 <= level <= L");
+    return -1;
+  }
+  if (ws_bytes < rescale_workspace(ctx, polys, level)) {
+    fhe_set_error("rescale workspace too small");
+    return -1;
+  }
+  const LevelPlan& lp = ctx.levels[level];
+  const DevChain& ch = ctx.chain->dev;
+  const long n = 1L << ch.log_n;
+  u64* last = (u64*)ws;
+  u64* corr = last + (long)polys * n;
+  WPair tinv{0, 0};
+  const u64* t_mod = nullptr;
+  if (t_plain) {
+    const PlainPlan* pp = get_plain_plan(&ctx, t_plain);
+    if (!pp) {
+      fhe_set_error("plain-modulus plan allocation failed");
+      return -2;
+    }
+    tinv = pp->tinv_last[level];
+    t_mod = pp->t_mod[level];
+  }
+  int rc = launch_gather_last(last, in, polys, level, ch.log_n, st);
+  if (rc) return rc;
+  rc = launch_ntt(ch, last, last, polys, RowMap{nullptr, 1, level - 1}, true, st);
+  if (rc) return rc;
+  rc = launch_modswitch_expand(ch, corr, last, polys, level - 1, level - 1, t_plain, tinv, t_mod,
+                               lp.rs_qlast, st);
+  if (rc) return rc;
+  rc = launch_ntt(ch, corr, corr, polys * (level - 1), RowMap{nullptr, level - 1, 0}, false, st);
+  if (rc) return rc;
+  return launch_modswitch_finish(ch, out, in, corr, polys, level, lp.rs_inv, st);
+}

@@ -1,0 +1,70 @@
+"""Batched NTT/INTT on the B200 vs the reference's golden vectors (config 2
+sweep shapes) - bit-exact residues, checked through the C ABI."""
+
+import numpy as np
+import pytest
+
+from fhe_testutil import digest, to_u64
+
+pytestmark = pytest.mark.gpu
+
+
+def _inputs(primes, n, rows, seed):
+    rng = np.random.default_rng(seed)
+    L = len(primes)
+    return np.stack([rng.integers(0, primes[r % L], n, dtype=np.uint64) for r in range(rows)])
+
+
+def _cases(golden):
+    return [(c["key"], c) for c in golden["ntt"]]
+
+
+def test_ntt_matches_reference_golden(golden, golden_arrays):
+    import torch
+
+    from paper_2503_22227_b200.coremath.ntt import DeviceChain
+
+    arrs = golden_arrays["ntt"]
+    for key, c in _cases(golden):
+        primes = [int(p) for p in c["primes"]]
+        n = 1 << c["log_n"]
+        ch = DeviceChain(primes, c["log_n"])
+        # tables: psi is the smallest primitive 2n-th root, twiddles bit-reversed
+        psi, fw, iv, _ = ch.tables(0)
+        assert psi == int(c["psi"][0]), key
+        assert fw[:64].tolist() == arrs[key + "_psi_br"].tolist()[: min(64, n)], key
+        assert iv[:64].tolist() == arrs[key + "_ipsi_br"].tolist()[: min(64, n)], key
+        a = _inputs(primes, n, c["rows"], c["seed"])
+        assert digest(a) == c["in_sha"]
+        dev = torch.from_numpy(a.view(np.int64)).cuda()
+        f = dev.clone()
+        ch.transform(f, c["rows"], False, limbs=c["L"], offset=0)
+        i = dev.clone()
+        ch.transform(i, c["rows"], True, limbs=c["L"], offset=0)
+        torch.cuda.synchronize()
+        assert digest(f) == c["fwd_sha"], f"forward mismatch {key}"
+        assert digest(i) == c["inv_sha"], f"inverse mismatch {key}"
+        if key + "_fwd" in arrs:
+            assert (to_u64(f) == arrs[key + "_fwd"]).all()
+
+
+@pytest.mark.parametrize("log_n", [4, 10, 12, 13, 14, 15, 16])
+def test_roundtrip_and_explicit_mod_idx(log_n):
+    import torch
+
+    from paper_2503_22227_b200.coremath.ntt import NttChain
+    from paper_2503_22227_b200.coremath.primes import gen_ntt_prime_chain
+
+    n = 1 << log_n
+    primes = [m.value for m in gen_ntt_prime_chain(50, n, 4)]
+    chain = NttChain(primes, n)
+    rng = np.random.default_rng(log_n)
+    midx = rng.integers(0, 4, 9)
+    a = np.stack([rng.integers(0, primes[m], n, dtype=np.uint64) for m in midx])
+    f = chain.forward(a, midx)
+    back = chain.inverse(f, midx)
+    assert back.tolist() == a.tolist()
+    # per-row equals single-row transforms
+    for r in (0, 5):
+        one = NttChain([primes[midx[r]]], n).forward(a[r:r + 1], [0])
+        assert one[0].tolist() == f[r].tolist()
