@@ -1,0 +1,382 @@
+"""Benchmark: CKKS HMult+Relin ops/s at N=2^16, L=30 (hybrid dnum=3) plus the
+batched-NTT HBM roofline, on 1..8 B200s (one process per GPU).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--batch B] [--impl ours|reference]
+
+A step = one fused tensor product + one batched hybrid key switch over B
+ciphertext pairs already resident in HBM (B HMult+Relin ops).  Each rank runs
+its own batch (weak scaling, no data-path collective: HMult+Relin of
+independent ciphertexts is replicas-only); the step time is the
+max over ranks.  B pairs of 60 MiB exceed the 126 MB L2, so no flush is needed.
+
+--impl reference times the CPU restatement of the reference's own algorithm
+(per-prime gadget key switch, oracle/c/fhe_oracle.c, all host threads) on the
+same metric, rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+N_LOG = 16
+LEVELS = 30
+DNUM = 3
+SPECIAL = 10
+METRIC = "CKKS HMult+Relin ops/s at N=2^16,L=30"
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi SM clocks and throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(
+                    ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                     "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                vals = [v.strip() for v in out.stdout.strip().split(",")]
+                if len(vals) == 6:
+                    self.rows.append(vals)
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4) if r[2 + k] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def dist_init():
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    return rank, world, local
+
+
+def barrier(world):
+    import torch
+
+    torch.cuda.synchronize()
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def max_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ---------------------------------------------------------------------------
+
+def build_workload(batch: int):
+    """Config 4: Q = 30 x 50-bit, P = 10 x 60-bit, dnum = 3, Delta = 2^49;
+    keys from Rng((4).to_bytes(32)), slots ~ U(-1,1) from default_rng(9)."""
+    import torch
+
+    from paper_2503_22227_b200.context import Context, PoolConfig, hybrid_params
+    from paper_2503_22227_b200.coremath.sampling import Rng
+    from paper_2503_22227_b200.keys import keygen, pk_gen, relin_keygen
+    from paper_2503_22227_b200.schemes import ckks
+
+    params = hybrid_params(1 << N_LOG, LEVELS, bits=50, special=SPECIAL, special_bits=60,
+                           dnum=DNUM, scale=float(2 ** 49))
+    ctx = Context(params, PoolConfig(unit_mb=200, cap_mb=4096))
+    seed = lambda s: Rng(int(s).to_bytes(32, "little"))  # noqa: E731
+    sk = keygen(ctx, seed(4))
+    pk = pk_gen(ctx, sk, seed(41))
+    rlk = relin_keygen(ctx, sk, seed(42))
+    vr = np.random.default_rng(9)
+    x = vr.uniform(-1, 1, ctx.n // 2)
+    y = vr.uniform(-1, 1, ctx.n // 2)
+    cx = ckks.ckks_encrypt(ctx, ckks.ckks_encode(ctx, x), pk, seed(43))
+    cy = ckks.ckks_encrypt(ctx, ckks.ckks_encode(ctx, y), pk, seed(44))
+    # correctness gate before any timing: HMult+Relin+Rescale decrypts to x*y
+    res = ckks.ckks_rescale(ctx, ckks.ckks_relinearize(ctx, ckks.ckks_multiply(ctx, cx, cy), rlk))
+    err = float(np.max(np.abs(ckks.ckks_decode(ctx, ckks.ckks_decrypt(ctx, res, sk)) - x * y)))
+    if not err < 1e-4:
+        raise AssertionError(f"HMult+Relin+Rescale error {err} too large")
+    L, n = LEVELS, ctx.n
+    X = torch.empty((batch, 2, L, n), dtype=torch.int64, device="cuda")
+    Y = torch.empty_like(X)
+    X[:] = cx.data.view()
+    Y[:] = cy.data.view()
+    T3 = torch.empty((batch, 3, L, n), dtype=torch.int64, device="cuda")
+    OUT = torch.empty((batch, 2, L, n), dtype=torch.int64, device="cuda")
+    return {"ctx": ctx, "rlk": rlk, "X": X, "Y": Y, "T3": T3, "OUT": OUT, "err": err,
+            "cx": cx, "cy": cy, "sk": sk, "x": x, "y": y}
+
+
+def hmult_relin_step(w, batch: int):
+    """One step: batched fused tensor + batched hybrid key switch (2 calls)."""
+    from paper_2503_22227_b200 import _native
+    from paper_2503_22227_b200.keys import key_switch_into
+
+    ctx, lib = w["ctx"], _native.lib()
+    L, n = LEVELS, ctx.n
+    X, Y, T3, OUT = w["X"], w["Y"], w["T3"], w["OUT"]
+    _native.check(lib.fhe_tensor(ctx.chain.handle, T3.data_ptr(), X.data_ptr(), Y.data_ptr(), L,
+                                 batch, 2 * L * n, 2 * L * n, 3 * L * n, 0,
+                                 _native.stream_handle()), "fhe_tensor")
+    key_switch_into(ctx, L, T3[:, 2], w["rlk"], OUT[:, 0], OUT[:, 1], add0=T3[:, 0],
+                    add1=T3[:, 1], batch=batch, d_stride=3 * L * n, add_stride=3 * L * n,
+                    out_stride=2 * L * n)
+
+
+def launches_per_step(level: int) -> int:
+    # tensor 1; key switch: INTT 2, ModUp 1, NTT 2, inner 1, INTT(P) 2, conv 1, NTT 2, finish 1
+    return 1 + 12
+
+
+def time_steps(fn, steps: int, warmup: int, world: int):
+    import torch
+
+    for _ in range(warmup):
+        fn()
+    barrier(world)
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    start.record()
+    for _ in range(steps):
+        fn()
+    end.record()
+    end.synchronize()
+    barrier(world)
+    return start.elapsed_time(end) / steps  # ms per step
+
+
+def ntt_roofline(steps: int, warmup: int):
+    """Batched NTT, config-2 largest shape: N=2^16, L=40, 64 ct x 2 polys
+    (5120 rows, 2.68 GB).  Algorithmic bytes per launch = 2 * rows * N * 8
+    (read + write once); the dominant kernel of the key-switch step."""
+    import torch
+
+    from paper_2503_22227_b200.coremath.ntt import DeviceChain
+    from paper_2503_22227_b200.coremath.primes import gen_ntt_prime_chain
+
+    n, L, rows = 1 << N_LOG, 40, 64 * 2 * 40
+    primes = [m.value for m in gen_ntt_prime_chain(50, n, L)]
+    ch = DeviceChain(primes, N_LOG)
+    buf = torch.empty((rows, n), dtype=torch.int64, device="cuda")
+    # uniform residues per row (device-generated: the content does not change timing)
+    qv = torch.tensor([p for p in primes], dtype=torch.float64, device="cuda")
+    buf.copy_((torch.rand((rows, n), dtype=torch.float64, device="cuda")
+               * qv.repeat(rows // L).unsqueeze(1)).to(torch.int64))
+    out = {}
+    for name, inv in (("forward", False), ("inverse", True)):
+        t = time_steps(lambda: ch.transform(buf, rows, inv, limbs=L, offset=0), steps, warmup, 1)
+        out[name] = t
+    algo = 2.0 * rows * n * 8
+    return out, algo, rows
+
+
+def e2e_step(w, batch: int, host_in, host_out):
+    """Public API end to end: per pair, H2D of both ciphertexts from pinned
+    host memory, ckks_multiply -> ckks_relinearize, D2H of the result."""
+    from paper_2503_22227_b200.rnspoly import CData, Domain
+    from paper_2503_22227_b200.schemes import ckks
+
+    ctx = w["ctx"]
+    L, n = LEVELS, ctx.n
+    for b in range(batch):
+        xa = CData(ctx.pool, 2, L, n, Domain.EVALUATION, zero=False)
+        ya = CData(ctx.pool, 2, L, n, Domain.EVALUATION, zero=False)
+        xa.view().copy_(host_in[b, 0], non_blocking=True)
+        ya.view().copy_(host_in[b, 1], non_blocking=True)
+        a = ckks.CkksCiphertext(xa, w["cx"].scale, L)
+        c = ckks.CkksCiphertext(ya, w["cy"].scale, L)
+        r = ckks.ckks_relinearize(ctx, ckks.ckks_multiply(ctx, a, c), w["rlk"])
+        host_out[b].copy_(r.data.view(), non_blocking=True)
+
+
+def cpu_baseline_hmult(seconds_budget: float = 20.0):
+    """The oracle port of the reference algorithm (per-prime gadget key switch,
+    keys.py:186-237, alpha=1, K=0) at N=2^16, L=30 on all host threads."""
+    from oracle import fast
+    from oracle import rns_oracle as orc
+
+    n = 1 << N_LOG
+    Q = orc.prime_chain(50, n, LEVELS)
+    rng = np.random.default_rng(1)
+    ct = lambda: np.stack([np.stack([rng.integers(0, q, n, dtype=np.uint64) for q in Q])  # noqa
+                           for _ in range(2)])
+    x, y = ct(), ct()
+    # random per-prime-gadget key (L digits x (b, a) x L limbs); content does not change cost
+    keys = rng.integers(0, Q[0], (LEVELS, 2, LEVELS, n), dtype=np.uint64)
+    times = []
+    t_all = time.perf_counter()
+    while True:
+        t0 = time.perf_counter()
+        d0, d1, d2 = fast.tensor(x, y, Q)
+        b, a = fast.key_switch(d2, keys, Q)
+        fast.add(d0, b, Q)
+        fast.add(d1, a, Q)
+        times.append(time.perf_counter() - t0)
+        if time.perf_counter() - t_all > seconds_budget or len(times) >= 8:
+            break
+    med = statistics.median(times)
+    return {"value": 1.0 / med, "unit": "ops/s", "cores": fast.threads(), "kind": "port",
+            "sample": f"{len(times)} HMult+Relin ops (per-prime gadget, reference algorithm) "
+                      f"at N=2^16, L=30, median {med:.2f} s/op"}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    base = cpu_baseline_hmult(seconds_budget=max(20.0, 3.0 * args.steps))
+    v = base["value"]
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "ops/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1000.0 / v, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+            "config": {"workload": "config 4: CKKS HMult+Relin N=2^16 L=30 (reference per-prime "
+                                   "gadget on CPU)"},
+            "cpu_baseline": base,
+            "e2e": {"value": v, "unit": "ops/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--batch", type=int, default=8)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+
+    rank, world, local = dist_init()
+    peak, peak_kind = _peaks()
+    B = args.batch
+    w = build_workload(B)
+    step = lambda: hmult_relin_step(w, B)  # noqa: E731
+    with ClockSampler(local) as clk:
+        ms = time_steps(step, args.steps, max(args.warmup, 3), world)
+    ms = max_over_ranks(ms, world)
+    ops = B * world / (ms / 1000.0)
+    # parity of the timed path itself: batch item 0 equals the public-API result
+    from paper_2503_22227_b200.schemes import ckks
+
+    ref = ckks.ckks_relinearize(w["ctx"], ckks.ckks_multiply(w["ctx"], w["cx"], w["cy"]), w["rlk"])
+    if not torch.equal(w["OUT"][0], ref.data.view()):
+        raise AssertionError("batched step differs from the public API result")
+
+    # end to end through the public API with host buffers
+    L, n = LEVELS, 1 << N_LOG
+    host_in = torch.empty((B, 2, 2, L, n), dtype=torch.int64).pin_memory()
+    host_in[:, 0] = w["X"][0].cpu()
+    host_in[:, 1] = w["Y"][0].cpu()
+    host_out = torch.empty((B, 2, L, n), dtype=torch.int64).pin_memory()
+    e2e_ms = time_steps(lambda: e2e_step(w, B, host_in, host_out), max(2, args.steps // 4),
+                        2, world)
+    e2e_ms = max_over_ranks(e2e_ms, world)
+    h2d = B * 2 * 2 * L * n * 8
+    d2h = B * 2 * L * n * 8
+
+    # roofline: batched NTT (dominant kernel family of the key-switch step)
+    ntt_ms, algo, rows = ntt_roofline(max(3, args.steps // 4), 3)
+    fwd_gbs = algo / (ntt_ms["forward"] / 1000.0) / 1e9
+    inv_gbs = algo / (ntt_ms["inverse"] / 1000.0) / 1e9
+    decrypt_err = w["err"]
+    del w
+    line = {
+        "metric": METRIC, "value": ops, "unit": "ops/s", "n_gpus": world, "steps": args.steps,
+        "warmup": max(args.warmup, 3), "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+        "config": {"workload": "config 4: CKKS HMult+Relin, N=2^16, L=30 x 50-bit, "
+                               "P=10 x 60-bit, dnum=3 (hybrid), Delta=2^49",
+                   "batch_per_gpu": B, "ops_per_step": B * world,
+                   "l2": "inputs larger than L2 (8 x 60 MiB pairs + 120 MiB key)"},
+        "e2e": {"value": B * world / (e2e_ms / 1000.0), "unit": "ops/s",
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "path": "ckks_multiply + ckks_relinearize per pair, pinned host buffers"},
+        "roofline": {"bound": "hbm", "kernel": "batched NTT forward (cols+chunks passes), "
+                     f"N=2^16, {rows} rows", "achieved": fwd_gbs, "peak": peak,
+                     "peak_kind": peak_kind, "unit": "GB/s", "frac": fwd_gbs / peak,
+                     "traffic": None, "inverse_achieved": inv_gbs,
+                     "algorithmic_bytes_per_launch": algo},
+        "ntt": {"forward_ms": ntt_ms["forward"], "inverse_ms": ntt_ms["inverse"],
+                "forward_gbs": fwd_gbs, "inverse_gbs": inv_gbs, "rows": rows, "N": n},
+        "gpu_launches": launches_per_step(LEVELS) * args.steps,
+        "clocks": clk.summary(),
+        "decrypt_err_hmult_relin_rescale": decrypt_err,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline_hmult()
+    if rank == 0:
+        print(json.dumps(line))
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -113,12 +113,13 @@ int fhe_rescale(const FheContext* ctx, uint64_t* out, const uint64_t* in, int po
  *      (ModUp -> inner product -> ModDown).  d: batch x (level, n) eval,
  *      stride d_stride words.  key: digits x (2, L+K, n) eval, contiguous.
  *      out0 = add0 + b, out1 = add1 + a (add0/add1 may be NULL, may alias
- *      out0/out1); batch items are add/out_stride words apart. */
+ *      out0/out1); batch items are add_stride / out_stride words apart.
+ *      One key read serves the whole batch. */
 size_t fhe_keyswitch_workspace(const FheContext* ctx, int level, int batch);
 int fhe_keyswitch(const FheContext* ctx, int level, const uint64_t* d, int64_t d_stride,
                   const uint64_t* key, const uint64_t* add0, const uint64_t* add1,
-                  uint64_t* out0, uint64_t* out1, int64_t io_stride, int batch, void* workspace,
-                  size_t ws_bytes, void* stream);
+                  int64_t add_stride, uint64_t* out0, uint64_t* out1, int64_t out_stride,
+                  int batch, void* workspace, size_t ws_bytes, void* stream);
 
 #ifdef __cplusplus
 }

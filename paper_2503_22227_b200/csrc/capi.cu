@@ -230,15 +230,15 @@ size_t fhe_keyswitch_workspace(const FheContext* ctx, int level, int batch) {
 
 int fhe_keyswitch(const FheContext* ctx, int level, const uint64_t* d, int64_t d_stride,
                   const uint64_t* key, const uint64_t* add0, const uint64_t* add1,
-                  uint64_t* out0, uint64_t* out1, int64_t io_stride, int batch, void* workspace,
-                  size_t ws_bytes, void* stream) {
+                  int64_t add_stride, uint64_t* out0, uint64_t* out1, int64_t out_stride,
+                  int batch, void* workspace, size_t ws_bytes, void* stream) {
   if (!ctx || !d || !key || !out0 || !out1 || batch < 1) {
     fhe_set_error("fhe_keyswitch: bad arguments");
     return -1;
   }
   FHE_TRY({
-    return run_keyswitch(*ctx, level, d, d_stride, key, add0, add1, out0, out1, io_stride, batch,
-                         workspace, ws_bytes, (cudaStream_t)stream);
+    return run_keyswitch(*ctx, level, d, d_stride, key, add0, add1, add_stride, out0, out1,
+                         out_stride, batch, workspace, ws_bytes, (cudaStream_t)stream);
   })
 }
 

@@ -155,6 +155,8 @@ int build_chain(const u64* primes, int count, int log_n, FheChain* ch) {
   ch->dev.itw = (const WPair*)(b + o_itw);
   ch->dev.ninv = (const WPair*)(b + o_ni);
   ch->dev.ninv_w1 = (const WPair*)(b + o_nw);
+  ch->dev.lazy_ok = true;
+  for (int p = 0; p < count; ++p) ch->dev.lazy_ok &= primes[p] < ((u64)1 << 58);
   return 0;
 }
 

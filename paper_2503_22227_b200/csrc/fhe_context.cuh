@@ -59,8 +59,8 @@ const PlainPlan* get_plain_plan(FheContext* ctx, u64 t);
 // keyswitch.cu
 size_t keyswitch_workspace(const FheContext& ctx, int level, int batch);
 int run_keyswitch(const FheContext& ctx, int level, const u64* d, long d_stride, const u64* key,
-                  const u64* add0, const u64* add1, u64* out0, u64* out1, long io_stride,
-                  int batch, void* ws, size_t ws_bytes, cudaStream_t st);
+                  const u64* add0, const u64* add1, long add_stride, u64* out0, u64* out1,
+                  long out_stride, int batch, void* ws, size_t ws_bytes, cudaStream_t st);
 size_t rescale_workspace(const FheContext& ctx, int polys, int level);
 int run_rescale(FheContext& ctx, u64* out, const u64* in, int polys, int level, u64 t_plain,
                 void* ws, size_t ws_bytes, cudaStream_t st);

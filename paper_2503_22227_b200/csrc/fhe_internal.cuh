@@ -26,6 +26,7 @@ struct DevChain {
   const WPair* itw;      // [count][N]   (ipsi_br[i], shoup)
   const WPair* ninv;     // [count]      (n^-1, shoup)
   const WPair* ninv_w1;  // [count]      (ipsi_br[1] * n^-1, shoup)
+  bool lazy_ok;          // every prime < 2^58: lazy forward butterflies allowed
 };
 
 // Row -> chain position mapping used by every batched kernel.  The

@@ -5,9 +5,22 @@
 
 int grid_for(long work);
 
-// ntt.cu: `in` may equal `data` (in place); rows are contiguous.
-int launch_ntt(const DevChain& ch, u64* data, const u64* in, int rows, RowMap map, bool inverse,
-               cudaStream_t st);
+// ntt.cu: transform `rows` rows of src into dst (may alias).  Row r uses
+// chain position map(r) and lives at (r / map.limbs) * bstride +
+// (r % map.limbs) * N words (bstride 0: contiguous rows).
+struct NttArgs {
+  u64* dst;
+  const u64* src;
+  int rows;
+  RowMap map;
+  long src_bstride;
+  long dst_bstride;
+};
+int launch_ntt(const DevChain& ch, const NttArgs& a, bool inverse, cudaStream_t st);
+inline int launch_ntt(const DevChain& ch, u64* data, const u64* in, int rows, RowMap map,
+                      bool inverse, cudaStream_t st) {
+  return launch_ntt(ch, NttArgs{data, in, rows, map, 0, 0}, inverse, st);
+}
 
 // poly.cu
 int launch_ewise(const DevChain& ch, int op, u64* out, const u64* a, const u64* b, const u64* c,

@@ -66,7 +66,25 @@ __global__ void __launch_bounds__(kThreads)
         y[s] = shoup_mul(cb[(long)(s0 + s) * n + i], w.w, w.sh, ch.mc[s0 + s].q);
       }
     }
-    for (int t = 0; t < nt; ++t) {
+    // four targets per iteration: independent 128-bit accumulation chains
+    int t = 0;
+    for (; na <= chunk && t + 4 <= nt; t += 4) {
+      u64 hi[4] = {0, 0, 0, 0}, lo[4] = {0, 0, 0, 0};
+#pragma unroll
+      for (int s = 0; s < kMaxAlpha; ++s) {
+        if (s < na) {
+#pragma unroll
+          for (int u = 0; u < 4; ++u) mac_wide(hi[u], lo[u], y[s], sw[s * nt + t + u]);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int m = t + u < s0 ? t + u : t + u + na;
+        const int p = m < level ? m : L + (m - level);
+        eb[(long)(t + u) * n + i] = reduce_fold(hi[u], lo[u], ch.mc[p]);
+      }
+    }
+    for (; t < nt; ++t) {
       const int m = t < s0 ? t : t + na;
       const int p = m < level ? m : L + (m - level);
       const ModConst mc = ch.mc[p];
@@ -85,8 +103,8 @@ __global__ void __launch_bounds__(kThreads)
                     const u64* __restrict__ ext, long ext_stride, const u64* __restrict__ key,
                     int keyL, const int* __restrict__ dig_info, int D, int level, int K, int L,
                     u64* __restrict__ accQ, u64* __restrict__ accP, const u64* add0,
-                    const u64* add1, u64* out0, u64* out1, long io_stride, int batch,
-                    int chunk) {
+                    const u64* add1, long add_stride, u64* out0, u64* out1, long out_stride,
+                    int batch, int chunk) {
   extern __shared__ int sinfo[];
   for (int i = threadIdx.x; i < 4 * D; i += blockDim.x) sinfo[i] = dig_info[i];
   __syncthreads();
@@ -99,27 +117,61 @@ __global__ void __launch_bounds__(kThreads)
     const long i = t & (n - 1);
     const int p = m < level ? m : L + (m - level);
     const ModConst mc = ch.mc[p];
-    for (int b = 0; b < batch; ++b) {
-      Acc ab, aa;
-      for (int di = 0; di < D; ++di) {
-        const int s0 = sinfo[4 * di], na = sinfo[4 * di + 1], ro = sinfo[4 * di + 2];
-        u64 v;
-        if (m >= s0 && m < s0 + na) {
-          v = d[b * d_stride + (long)m * n + i];
-        } else {
-          const int row = ro + (m < s0 ? m : m - na);
-          v = ext[b * ext_stride + (long)row * n + i];
+    // small digit counts (hybrid): keep the key words in registers across the
+    // batch so each key word is read from HBM once per call
+    constexpr int kCache = 4;
+    u64 kbc[kCache], kac[kCache];
+    const bool cached = D <= kCache && D <= chunk;
+    if (cached) {
+#pragma unroll
+      for (int di = 0; di < kCache; ++di) {
+        if (di < D) {
+          kbc[di] = key[((long)(2 * di) * keyL + p) * n + i];
+          kac[di] = key[((long)(2 * di + 1) * keyL + p) * n + i];
         }
-        const u64 kb = key[((long)(2 * di) * keyL + p) * n + i];
-        const u64 ka = key[((long)(2 * di + 1) * keyL + p) * n + i];
-        ab.mac(v, kb, chunk, mc);
-        aa.mac(v, ka, chunk, mc);
       }
-      const u64 rb = ab.done(mc), ra = aa.done(mc);
+    }
+    for (int b = 0; b < batch; ++b) {
+      u64 rb, ra;
+      if (cached) {
+        u64 bh = 0, bl = 0, ah = 0, al = 0;
+#pragma unroll
+        for (int di = 0; di < kCache; ++di) {
+          if (di < D) {
+            const int s0 = sinfo[4 * di], na = sinfo[4 * di + 1], ro = sinfo[4 * di + 2];
+            const u64 v = (m >= s0 && m < s0 + na)
+                              ? d[b * d_stride + (long)m * n + i]
+                              : ext[b * ext_stride + (long)(ro + (m < s0 ? m : m - na)) * n + i];
+            mac_wide(bh, bl, v, kbc[di]);
+            mac_wide(ah, al, v, kac[di]);
+          }
+        }
+        rb = reduce_fold(bh, bl, mc);
+        ra = reduce_fold(ah, al, mc);
+      } else {
+        Acc ab, aa;
+        for (int di = 0; di < D; ++di) {
+          const int s0 = sinfo[4 * di], na = sinfo[4 * di + 1], ro = sinfo[4 * di + 2];
+          u64 v;
+          if (m >= s0 && m < s0 + na) {
+            v = d[b * d_stride + (long)m * n + i];
+          } else {
+            const int row = ro + (m < s0 ? m : m - na);
+            v = ext[b * ext_stride + (long)row * n + i];
+          }
+          const u64 kb = key[((long)(2 * di) * keyL + p) * n + i];
+          const u64 ka = key[((long)(2 * di + 1) * keyL + p) * n + i];
+          ab.mac(v, kb, chunk, mc);
+          aa.mac(v, ka, chunk, mc);
+        }
+        rb = ab.done(mc);
+        ra = aa.done(mc);
+      }
       if (K == 0) {
-        const long o = b * io_stride + (long)m * n + i;
-        out0[o] = add0 ? add_mod(add0[o], rb, mc.q) : rb;
-        out1[o] = add1 ? add_mod(add1[o], ra, mc.q) : ra;
+        const long o = b * out_stride + (long)m * n + i;
+        const long ai = b * add_stride + (long)m * n + i;
+        out0[o] = add0 ? add_mod(add0[ai], rb, mc.q) : rb;
+        out1[o] = add1 ? add_mod(add1[ai], ra, mc.q) : ra;
       } else if (m < level) {
         accQ[((long)(b * 2 + 0) * level + m) * n + i] = rb;
         accQ[((long)(b * 2 + 1) * level + m) * n + i] = ra;
@@ -154,7 +206,20 @@ __global__ void __launch_bounds__(kThreads)
         y[k] = shoup_mul(src[(long)k * n + i], w.w, w.sh, ch.mc[L + k].q);
       }
     }
-    for (int j = 0; j < level; ++j) {
+    int j = 0;
+    for (; K <= chunk && j + 4 <= level; j += 4) {
+      u64 hi[4] = {0, 0, 0, 0}, lo[4] = {0, 0, 0, 0};
+#pragma unroll
+      for (int k = 0; k < kMaxAlpha; ++k) {
+        if (k < K) {
+#pragma unroll
+          for (int u = 0; u < 4; ++u) mac_wide(hi[u], lo[u], y[k], sw[k * level + j + u]);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) dst[(long)(j + u) * n + i] = reduce_fold(hi[u], lo[u], ch.mc[j + u]);
+    }
+    for (; j < level; ++j) {
       const ModConst mc = ch.mc[j];
       Acc acc;
 #pragma unroll
@@ -169,8 +234,8 @@ __global__ void __launch_bounds__(kThreads)
 __global__ void __launch_bounds__(kThreads)
     moddown_finish_kernel(const DevChain ch, const u64* __restrict__ accQ,
                           const u64* __restrict__ conv, const WPair* __restrict__ p_inv,
-                          const u64* add0, const u64* add1, u64* out0, u64* out1, long io_stride,
-                          int level, int batch) {
+                          const u64* add0, const u64* add1, long add_stride, u64* out0,
+                          u64* out1, long out_stride, int level, int batch) {
   const int log_n = ch.log_n;
   const long n = 1L << log_n;
   const long per = (long)level << log_n;
@@ -184,10 +249,9 @@ __global__ void __launch_bounds__(kThreads)
     const u64 q = ch.mc[j].q;
     const WPair pi = p_inv[j];
     const u64 v = shoup_mul(sub_mod(accQ[t], conv[t], q), pi.w, pi.sh, q);
-    const long o = b * io_stride + w;
     const u64* add = poly ? add1 : add0;
     u64* out = poly ? out1 : out0;
-    out[o] = add ? add_mod(add[o], v, q) : v;
+    out[b * out_stride + w] = add ? add_mod(add[b * add_stride + w], v, q) : v;
   }
 }
 
@@ -211,8 +275,8 @@ size_t keyswitch_workspace(const FheContext& ctx, int level, int batch) {
 }
 
 int run_keyswitch(const FheContext& ctx, int level, const u64* d, long d_stride, const u64* key,
-                  const u64* add0, const u64* add1, u64* out0, u64* out1, long io_stride,
-                  int batch, void* ws, size_t ws_bytes, cudaStream_t st) {
+                  const u64* add0, const u64* add1, long add_stride, u64* out0, u64* out1,
+                  long out_stride, int batch, void* ws, size_t ws_bytes, cudaStream_t st) {
   if (level < 1 || level > ctx.L) {
     fhe_set_error("keyswitch level out of range");
     return -1;
@@ -237,16 +301,9 @@ int run_keyswitch(const FheContext& ctx, int level, const u64* d, long d_stride,
   u64* conv = accP + (long)batch * 2 * K * n;
   int rc;
   // 1. coefficient form of the input
-  if (d_stride == (long)level * n) {
-    rc = launch_ntt(ch, c, d, batch * level, RowMap{nullptr, level, 0}, true, st);
-    if (rc) return rc;
-  } else {
-    for (int b = 0; b < batch; ++b) {
-      rc = launch_ntt(ch, c + (long)b * level * n, d + b * d_stride, level,
-                      RowMap{nullptr, level, 0}, true, st);
-      if (rc) return rc;
-    }
-  }
+  rc = launch_ntt(ch, NttArgs{c, d, batch * level, RowMap{nullptr, level, 0}, d_stride, 0},
+                  true, st);
+  if (rc) return rc;
   // 2. ModUp: basis extension of every digit, then NTT of the extended rows
   {
     int max_w = 0;
@@ -271,7 +328,7 @@ int run_keyswitch(const FheContext& ctx, int level, const u64* d, long d_stride,
     const long work = (long)(level + K) << log_n;
     ks_inner_kernel<<<grid_for(work), kThreads, 4 * lp.digits * sizeof(int), st>>>(
         ch, d, d_stride, ext, (long)lp.ext_rows * n, key, L + K, lp.dig_info, lp.digits, level,
-        K, L, accQ, accP, add0, add1, out0, out1, io_stride, batch, chunk);
+        K, L, accQ, accP, add0, add1, add_stride, out0, out1, out_stride, batch, chunk);
     FHE_LAUNCH_CHECK();
   }
   if (K == 0) return 0;
@@ -288,7 +345,7 @@ int run_keyswitch(const FheContext& ctx, int level, const u64* d, long d_stride,
   rc = launch_ntt(ch, conv, conv, batch * 2 * level, RowMap{nullptr, level, 0}, false, st);
   if (rc) return rc;
   moddown_finish_kernel<<<grid_for((long)batch * 2 * level * n), kThreads, 0, st>>>(
-      ch, accQ, conv, lp.p_inv, add0, add1, out0, out1, io_stride, level, batch);
+      ch, accQ, conv, lp.p_inv, add0, add1, add_stride, out0, out1, out_stride, level, batch);
   FHE_LAUNCH_CHECK();
   return 0;
 }

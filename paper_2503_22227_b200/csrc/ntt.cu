@@ -10,29 +10,35 @@
 // NttChain.forward/inverse (ntt.py:277-351).
 //
 // B200 design:
+//  * persistent CTAs (two per SM) walking tiles; each tile is brought into
+//    shared memory with cp.async while the previous tile computes (double
+//    buffer), so HBM latency overlaps the integer work;
 //  * radix-2^e register passes (e = 4..5): each thread owns 2^e elements and
-//    runs e butterfly stages in registers between shared-memory exchanges,
-//    so shared memory is touched once per e stages, not once per stage;
-//  * Harvey lazy butterflies (values kept in [0,4q) forward / [0,2q)
-//    inverse; valid because q < 2^62, modmath.py:36) - one conditional
-//    subtraction per butterfly instead of two;
-//  * n^-1 folded into the last inverse stage (no separate scaling pass);
-//  * XOR-swizzled shared memory so both the strided and the contiguous
-//    register passes are bank-conflict free;
-//  * N <= 2^13: whole rows in shared memory, one HBM round trip.
-//    N >= 2^14: four-step split N = N1 * N2: a column kernel runs the first
-//    log N1 stages on 16-column tiles (128-byte coalesced segments), a chunk
-//    kernel runs the remaining log N2 stages on contiguous N2-chunks.
+//    runs e butterfly stages in registers between shared-memory exchanges;
+//    the last pass writes straight from registers to HBM;
+//  * lazy butterflies: for chains whose primes are < 2^58 the forward
+//    transform never reduces inside the butterfly (values grow by < 2q per
+//    stage, < 33q after 16 stages) and reduces once at the end; otherwise
+//    Harvey's [0,4q) forward / [0,2q) inverse butterflies (q < 2^62,
+//    modmath.py:36);
+//  * n^-1 folded into the last inverse stage;
+//  * 16-byte-granular XOR swizzle: strided passes (8-byte accesses) and
+//    contiguous passes (16-byte accesses) are both bank-conflict free;
+//  * N <= 2^12: whole rows per tile (one HBM round trip).  N >= 2^13:
+//    four-step split N = N1 * N2: a column kernel runs the first log N1
+//    stages on [N1 x 16]-column tiles (128-byte segments), a chunk kernel
+//    the remaining log N2 stages on contiguous N2-chunks.
 #include "fhe_kernels.cuh"
 
 namespace {
 
 constexpr int kThreads = 256;
+constexpr int kTile = 4096;  // elements per tile (32 KB)
+constexpr int kCols = 16;    // columns per column tile (one 128-byte segment)
 
-__device__ __forceinline__ int swz(int i) { return i ^ ((i >> 4) & 15); }
+// XOR swizzle at 16-byte granularity inside 16-element (128-byte) rows.
+__device__ __forceinline__ int swz(int i) { return i ^ (((i >> 4) & 7) << 1); }
 
-// Pass schedule: ceil(log_s / 5) passes, the remainder spread over the first
-// passes (larger passes first keeps the contiguous last pass at e <= 4).
 constexpr int npass(int log_s) { return (log_s + 4) / 5; }
 constexpr int pass_e(int log_s, int p) {
   return log_s / npass(log_s) + (p < log_s % npass(log_s) ? 1 : 0);
@@ -43,58 +49,189 @@ constexpr int pass_r0(int log_s, int p) {
   return r;
 }
 
-// Arrays stored contiguously (array b element k at swz(b*S + k)); groups
-// enumerate arrays slowest so a warp stays inside one array.
-template <int LOG_S>
-struct RowLayout {
-  __device__ __forceinline__ int idx(int b, int k) const { return swz((b << LOG_S) + k); }
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n"); }
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+}
+
+// Per-array context of one local transform.
+struct ArrCtx {
+  const WPair* tw;  // table of the array's prime (forward or inverse)
+  u64 q;
+  int m0;           // global group base: twiddle index = (m0 << r) + g_local
+  int prime;        // chain position (final reduction / n^-1 folding)
+  bool fold;        // inverse: fold n^-1 into global stage 0
+};
+
+// Logical row -> word offset of its first coefficient (batched strided rows:
+// row r lives at (r / limbs) * bstride + (r % limbs) * N; bstride 0 means
+// contiguous rows).
+struct RowAddr {
+  long bstride;
+  int limbs;
+  int log_n;
+  __device__ __forceinline__ long operator()(int r) const {
+    return bstride ? (long)(r / limbs) * bstride + ((long)(r % limbs) << log_n)
+                   : ((long)r << log_n);
+  }
+};
+
+// ---------------------------------------------------------------------------
+// Tile policies.  A tile holds arrays() local arrays of S = 2^LOG_S elements.
+// tile_index(b, k) is an element's slot in the tile before swizzling;
+// gsrc/gdst its global address.
+
+// Whole rows (N <= 2^12): NB = 4096 / N rows per tile.
+template <int LOG_N>
+struct RowsTile {
+  static constexpr int LOG_S = LOG_N;
+  static constexpr int S = 1 << LOG_N;
+  static constexpr int NB = S >= kTile ? 1 : (kTile / S > 32 ? 32 : kTile / S);
+  static constexpr bool COLS = false;
+  int rows;
+  RowMap map;
+  RowAddr src, dst;
+  bool fwd;
+  int row0, nb;
+  int prime[NB];
+  __device__ __forceinline__ void setup(int t) {
+    row0 = t * NB;
+    nb = min(NB, rows - row0);
+    for (int b = 0; b < NB; ++b) prime[b] = b < nb ? map(row0 + b) : 0;
+  }
+  __device__ __forceinline__ int tile_index(int b, int k) const { return (b << LOG_S) + k; }
   __device__ __forceinline__ void split(int G, int gpa_log, int& b, int& g) const {
     b = G >> gpa_log;
     g = G & ((1 << gpa_log) - 1);
   }
-};
-
-// Column tile: array b (a column) element k at k*NB + b; groups enumerate
-// columns fastest so consecutive lanes touch consecutive words.
-template <int NB>
-struct ColLayout {
-  __device__ __forceinline__ int idx(int b, int k) const { return k * NB + b; }
-  __device__ __forceinline__ void split(int G, int, int& b, int& g) const {
-    b = G % NB;
-    g = G / NB;
+  __device__ __forceinline__ const u64* gsrc(const u64* base, int b, int k) const {
+    return base + src(row0 + b) + k;
   }
+  __device__ __forceinline__ u64* gdst(u64* base, int b, int k) const {
+    return base + dst(row0 + b) + k;
+  }
+  __device__ __forceinline__ ArrCtx ctx(int b, const DevChain& ch) const {
+    const int p = prime[b];
+    return ArrCtx{(fwd ? ch.tw : ch.itw) + ((size_t)p << LOG_N), ch.mc[p].q, 1, p, !fwd};
+  }
+  __device__ __forceinline__ int arrays() const { return nb; }
 };
 
-// Per-array twiddle context.
-struct ArrCtx {
-  const WPair* tw;   // table of the array's prime (forward or inverse)
-  u64 q;
-  int m0;            // global group base: twiddle index = (m0 << r) + g_local
-  const WPair* sn;   // inverse only: n^-1 folded into global stage 0 (or null)
-  const WPair* sw1;  // inverse only: ipsi_br[1] * n^-1
+// First log N1 stages on a [N1][16] column tile of one row.
+template <int LOG_N, int LOG_N1>
+struct ColsTile {
+  static constexpr int LOG_S = LOG_N1;
+  static constexpr bool COLS = true;
+  static constexpr int N2 = 1 << (LOG_N - LOG_N1);
+  static constexpr int TILES = N2 / kCols;
+  int rows;
+  RowMap map;
+  RowAddr src, dst;
+  bool fwd;
+  int row, j0, p;
+  __device__ __forceinline__ void setup(int t) {
+    row = t / TILES;
+    j0 = (t % TILES) * kCols;
+    p = map(row);
+  }
+  __device__ __forceinline__ int tile_index(int b, int k) const { return k * kCols + b; }
+  __device__ __forceinline__ void split(int G, int, int& b, int& g) const {
+    b = G % kCols;
+    g = G / kCols;
+  }
+  __device__ __forceinline__ const u64* gsrc(const u64* base, int b, int k) const {
+    return base + src(row) + (long)k * N2 + j0 + b;
+  }
+  __device__ __forceinline__ u64* gdst(u64* base, int b, int k) const {
+    return base + dst(row) + (long)k * N2 + j0 + b;
+  }
+  __device__ __forceinline__ ArrCtx ctx(int, const DevChain& ch) const {
+    return ArrCtx{(fwd ? ch.tw : ch.itw) + ((size_t)p << LOG_N), ch.mc[p].q, 1, p, !fwd};
+  }
+  __device__ __forceinline__ int arrays() const { return kCols; }
+};
+
+// Remaining stages on NB contiguous N2-chunks of one row.
+template <int LOG_N, int LOG_N1>
+struct ChunksTile {
+  static constexpr int LOG_S = LOG_N - LOG_N1;
+  static constexpr int S = 1 << LOG_S;
+  static constexpr int NB = kTile / S;
+  static constexpr bool COLS = false;
+  static constexpr int N1 = 1 << LOG_N1;
+  static constexpr int TILES = N1 / NB;
+  int rows;
+  RowMap map;
+  RowAddr src, dst;
+  bool fwd;
+  int row, c0, p;
+  __device__ __forceinline__ void setup(int t) {
+    row = t / TILES;
+    c0 = (t % TILES) * NB;
+    p = map(row);
+  }
+  __device__ __forceinline__ int tile_index(int b, int k) const { return (b << LOG_S) + k; }
+  __device__ __forceinline__ void split(int G, int gpa_log, int& b, int& g) const {
+    b = G >> gpa_log;
+    g = G & ((1 << gpa_log) - 1);
+  }
+  __device__ __forceinline__ const u64* gsrc(const u64* base, int b, int k) const {
+    return base + src(row) + (long)(c0 + b) * S + k;
+  }
+  __device__ __forceinline__ u64* gdst(u64* base, int b, int k) const {
+    return base + dst(row) + (long)(c0 + b) * S + k;
+  }
+  __device__ __forceinline__ ArrCtx ctx(int b, const DevChain& ch) const {
+    return ArrCtx{(fwd ? ch.tw : ch.itw) + ((size_t)p << LOG_N), ch.mc[p].q, N1 + c0 + b, p,
+                  false};
+  }
+  __device__ __forceinline__ int arrays() const { return NB; }
+};
+
+// Output handling of the final pass of a kernel.
+enum OutMode {
+  OUT_RAW = 0,     // store values as they are (intermediate of a split transform)
+  OUT_CANON4 = 1,  // forward Harvey: [0, 4q) -> [0, q)
+  OUT_REDUCE = 2   // forward lazy: [0, 33q) -> [0, q) by Barrett
 };
 
 // One register pass covering local stages R0 .. R0+E_LOG-1.
-template <int LOG_S, int R0, int E_LOG, bool FWD, class Lay, class CtxFn>
-__device__ __forceinline__ void run_pass(u64* sm, int nb, const Lay& lay, const CtxFn& ctx) {
+// LAST: values go straight to global memory instead of back to the tile.
+template <int LOG_S, int R0, int E_LOG, bool FWD, bool LAZY, bool LAST, int OUT, class Tile>
+__device__ __forceinline__ void run_pass(u64* sm, const Tile& tl, u64* gout,
+                                         const DevChain& ch) {
   constexpr int E = 1 << E_LOG;
-  constexpr int S = 1 << LOG_S;
-  constexpr int T0 = S >> (R0 + 1);
+  constexpr int T0 = (1 << LOG_S) >> (R0 + 1);
   constexpr int TMIN_LOG = LOG_S - R0 - E_LOG;
   constexpr int GPA_LOG = LOG_S - E_LOG;
-  const int total = nb << GPA_LOG;
+  constexpr bool VEC = (TMIN_LOG == 0) && !Tile::COLS;
+  const int total = tl.arrays() << GPA_LOG;
   for (int G = threadIdx.x; G < total; G += blockDim.x) {
     int b, g;
-    lay.split(G, GPA_LOG, b, g);
+    tl.split(G, GPA_LOG, b, g);
     const int hi = g >> TMIN_LOG;
     const int lo = g & ((1 << TMIN_LOG) - 1);
     const int base = hi * 2 * T0 + lo;
-    const ArrCtx cx = ctx(b);
+    const ArrCtx cx = tl.ctx(b, ch);
     const u64 q = cx.q;
     const u64 q2 = 2 * q;
     u64 x[E];
+    if (VEC) {
 #pragma unroll
-    for (int i = 0; i < E; ++i) x[i] = sm[lay.idx(b, base + (i << TMIN_LOG))];
+      for (int i = 0; i < E; i += 2) {
+        const ulonglong2 v =
+            *reinterpret_cast<const ulonglong2*>(&sm[swz(tl.tile_index(b, base + i))]);
+        x[i] = v.x;
+        x[i + 1] = v.y;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < E; ++i) x[i] = sm[swz(tl.tile_index(b, base + (i << TMIN_LOG)))];
+    }
     if (FWD) {
 #pragma unroll
       for (int rr = 0; rr < E_LOG; ++rr) {
@@ -106,7 +243,7 @@ __device__ __forceinline__ void run_pass(u64* sm, int nb, const Lay& lay, const 
           for (int i = 0; i < half; ++i) {
             const int a = blk * 2 * half + i, c = a + half;
             u64 u = x[a];
-            u = u >= q2 ? u - q2 : u;
+            if (!LAZY) u = u >= q2 ? u - q2 : u;
             const u64 v = shoup_lazy(x[c], w.w, w.sh, q);
             x[a] = u + v;
             x[c] = u - v + q2;
@@ -117,20 +254,21 @@ __device__ __forceinline__ void run_pass(u64* sm, int nb, const Lay& lay, const 
 #pragma unroll
       for (int rr = E_LOG - 1; rr >= 0; --rr) {
         const int half = E >> (rr + 1);
-        const bool fold_ninv = (R0 == 0) && (rr == 0) && (cx.sn != nullptr);
+        const bool fold = (R0 == 0) && (rr == 0) && cx.fold;
 #pragma unroll
         for (int blk = 0; blk < (1 << rr); ++blk) {
-          const WPair w = cx.tw[(cx.m0 << (R0 + rr)) + (hi << rr) + blk];
+          const WPair w = fold ? ch.ninv_w1[cx.prime]
+                               : cx.tw[(cx.m0 << (R0 + rr)) + (hi << rr) + blk];
+          const WPair sn = fold ? ch.ninv[cx.prime] : w;
 #pragma unroll
           for (int i = 0; i < half; ++i) {
             const int a = blk * 2 * half + i, c = a + half;
             const u64 u = x[a], v = x[c];
             const u64 s = u + v;
             const u64 d = u - v + q2;
-            if (fold_ninv) {
-              // last GS stage with n^-1 folded in; outputs canonical
-              x[a] = shoup_mul(s, cx.sn->w, cx.sn->sh, q);
-              x[c] = shoup_mul(d, cx.sw1->w, cx.sw1->sh, q);
+            if (fold) {
+              x[a] = shoup_mul(s, sn.w, sn.sh, q);
+              x[c] = shoup_mul(d, w.w, w.sh, q);
             } else {
               x[a] = s >= q2 ? s - q2 : s;
               x[c] = shoup_lazy(d, w.w, w.sh, q);
@@ -139,224 +277,223 @@ __device__ __forceinline__ void run_pass(u64* sm, int nb, const Lay& lay, const 
         }
       }
     }
+    if (LAST) {
+      if (OUT == OUT_CANON4) {
 #pragma unroll
-    for (int i = 0; i < E; ++i) sm[lay.idx(b, base + (i << TMIN_LOG))] = x[i];
+        for (int i = 0; i < E; ++i) x[i] = csub(csub(x[i], q2), q);
+      } else if (OUT == OUT_REDUCE) {
+        const ModConst mc = ch.mc[cx.prime];
+#pragma unroll
+        for (int i = 0; i < E; ++i) x[i] = reduce_word(x[i], mc);
+      }
+      if (VEC) {
+        u64* o = tl.gdst(gout, b, base);
+#pragma unroll
+        for (int i = 0; i < E; i += 2)
+          *reinterpret_cast<ulonglong2*>(o + i) = make_ulonglong2(x[i], x[i + 1]);
+      } else {
+#pragma unroll
+        for (int i = 0; i < E; ++i) *tl.gdst(gout, b, base + (i << TMIN_LOG)) = x[i];
+      }
+    } else {
+      if (VEC) {
+#pragma unroll
+        for (int i = 0; i < E; i += 2)
+          *reinterpret_cast<ulonglong2*>(&sm[swz(tl.tile_index(b, base + i))]) =
+              make_ulonglong2(x[i], x[i + 1]);
+      } else {
+#pragma unroll
+        for (int i = 0; i < E; ++i) sm[swz(tl.tile_index(b, base + (i << TMIN_LOG)))] = x[i];
+      }
+    }
   }
 }
 
-template <int LOG_S, int P, class Lay, class CtxFn>
-__device__ __forceinline__ void fwd_passes(u64* sm, int nb, const Lay& lay, const CtxFn& ctx) {
-  if constexpr (P < npass(LOG_S)) {
-    run_pass<LOG_S, pass_r0(LOG_S, P), pass_e(LOG_S, P), true>(sm, nb, lay, ctx);
-    __syncthreads();
-    fwd_passes<LOG_S, P + 1>(sm, nb, lay, ctx);
+// Forward passes P .. npass-1; the last one stores to global.
+template <int LOG_S, int P, bool LAZY, int OUT, class Tile>
+__device__ __forceinline__ void fwd_passes(u64* sm, const Tile& tl, u64* gout,
+                                           const DevChain& ch) {
+  constexpr int NP = npass(LOG_S);
+  if constexpr (P < NP) {
+    constexpr bool last = (P == NP - 1);
+    run_pass<LOG_S, pass_r0(LOG_S, P), pass_e(LOG_S, P), true, LAZY, last, OUT>(sm, tl, gout,
+                                                                                ch);
+    if constexpr (!last) {
+      __syncthreads();
+      fwd_passes<LOG_S, P + 1, LAZY, OUT>(sm, tl, gout, ch);
+    }
   }
 }
 
-template <int LOG_S, int P, class Lay, class CtxFn>
-__device__ __forceinline__ void inv_passes(u64* sm, int nb, const Lay& lay, const CtxFn& ctx) {
+// Inverse passes P .. 0 (reverse order); pass 0 stores to global.
+template <int LOG_S, int P, class Tile>
+__device__ __forceinline__ void inv_passes(u64* sm, const Tile& tl, u64* gout,
+                                           const DevChain& ch) {
   if constexpr (P >= 0) {
-    run_pass<LOG_S, pass_r0(LOG_S, P), pass_e(LOG_S, P), false>(sm, nb, lay, ctx);
+    constexpr bool last = (P == 0);
+    run_pass<LOG_S, pass_r0(LOG_S, P), pass_e(LOG_S, P), false, false, last, OUT_RAW>(sm, tl,
+                                                                                      gout, ch);
+    if constexpr (!last) {
+      __syncthreads();
+      inv_passes<LOG_S, P - 1>(sm, tl, gout, ch);
+    }
+  }
+}
+
+// Issue the cp.async copies of one tile (16 bytes per copy).
+template <class Tile>
+__device__ __forceinline__ void load_tile(u64* sm, const Tile& tl, const u64* src) {
+  constexpr int LOG_S = Tile::LOG_S;
+  const int nel = tl.arrays() << LOG_S;
+  for (int e = 2 * threadIdx.x; e < nel; e += 2 * blockDim.x) {
+    int b, k;
+    if (Tile::COLS) {
+      k = e / kCols;
+      b = e % kCols;
+    } else {
+      b = e >> LOG_S;
+      k = e & ((1 << LOG_S) - 1);
+    }
+    cp_async16(&sm[swz(e)], tl.gsrc(src, b, k));
+  }
+  cp_async_commit();
+}
+
+// Persistent, double-buffered transform kernel over the tiles of one policy.
+template <class Tile, bool FWD, bool LAZY, int OUT>
+__global__ void __launch_bounds__(kThreads, 2)
+    ntt_tiles_kernel(const DevChain ch, u64* dst, const u64* src, Tile tl, int ntiles) {
+  extern __shared__ __align__(16) u64 smem_raw[];
+  u64* smem[2] = {smem_raw, smem_raw + kTile};
+  int t = blockIdx.x;
+  if (t >= ntiles) return;
+  Tile cur = tl;
+  cur.setup(t);
+  load_tile(smem[0], cur, src);
+  int buf = 0;
+  for (; t < ntiles; t += gridDim.x) {
+    cp_async_wait_all();
     __syncthreads();
-    inv_passes<LOG_S, P - 1>(sm, nb, lay, ctx);
+    const int tn = t + gridDim.x;
+    if (tn < ntiles) {
+      Tile nxt = tl;
+      nxt.setup(tn);
+      load_tile(smem[buf ^ 1], nxt, src);
+    }
+    if (FWD)
+      fwd_passes<Tile::LOG_S, 0, LAZY, OUT>(smem[buf], cur, dst, ch);
+    else
+      inv_passes<Tile::LOG_S, npass(Tile::LOG_S) - 1>(smem[buf], cur, dst, ch);
+    if (tn < ntiles) cur.setup(tn);
+    buf ^= 1;
   }
 }
 
-// ---------------------------------------------------------------------------
-// Whole rows in shared memory (N <= 2^13).  NB rows per CTA.
-template <int LOG_N, bool FWD>
-__global__ void __launch_bounds__(kThreads) ntt_rows_kernel(DevChain ch, u64* data, const u64* src,
-                                                            int rows, RowMap map) {
-  constexpr int S = 1 << LOG_N;
-  constexpr int NB = S >= 2048 ? 1 : 2048 / S;
-  extern __shared__ u64 sm[];
-  const int row0 = blockIdx.x * NB;
-  const int nb = min(NB, rows - row0);
-  __shared__ int prime[NB];
-  for (int i = threadIdx.x; i < nb; i += blockDim.x) prime[i] = map(row0 + i);
-  u64* g = data + (size_t)row0 * S;
-  const int nel = nb * S;
-  if (S >= 2) {
-    const ulonglong2* g2 = reinterpret_cast<const ulonglong2*>(src + (size_t)row0 * S);
-    for (int i = threadIdx.x; i < nel / 2; i += blockDim.x) {
-      const ulonglong2 v = g2[i];
-      sm[swz(2 * i)] = v.x;
-      sm[swz(2 * i + 1)] = v.y;
-    }
+int g_sm_count = 0;
+int sm_count() {
+  if (!g_sm_count) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_sm_count, cudaDevAttrMultiProcessorCount, dev);
+    if (g_sm_count <= 0) g_sm_count = 148;
   }
-  __syncthreads();
-  RowLayout<LOG_N> lay;
-  const WPair* table = FWD ? ch.tw : ch.itw;
-  auto ctx = [&](int b) {
-    const int p = prime[b];
-    return ArrCtx{table + ((size_t)p << LOG_N), ch.mc[p].q, 1, FWD ? nullptr : &ch.ninv[p],
-                  FWD ? nullptr : &ch.ninv_w1[p]};
-  };
-  if (FWD)
-    fwd_passes<LOG_N, 0>(sm, nb, lay, ctx);
-  else
-    inv_passes<LOG_N, npass(LOG_N) - 1>(sm, nb, lay, ctx);
-  ulonglong2* o2 = reinterpret_cast<ulonglong2*>(g);
-  for (int i = threadIdx.x; i < nel / 2; i += blockDim.x) {
-    u64 a = sm[swz(2 * i)], b = sm[swz(2 * i + 1)];
-    if (FWD) {
-      const u64 q = ch.mc[prime[(2 * i) >> LOG_N]].q;
-      a = csub(csub(a, 2 * q), q);
-      b = csub(csub(b, 2 * q), q);
-    }
-    o2[i] = make_ulonglong2(a, b);
-  }
+  return g_sm_count;
 }
 
-// ---------------------------------------------------------------------------
-// Four-step split for N >= 2^14: N = N1 * N2, N1 = 2^LOG_N1.
-constexpr int kCols = 16;  // columns per tile: 16 x 8 B = one 128-byte segment
-
-// Column stages (global stages 0 .. LOG_N1-1) on a [N1][kCols] tile.
-template <int LOG_N, int LOG_N1, bool FWD>
-__global__ void __launch_bounds__(kThreads) ntt_cols_kernel(DevChain ch, u64* data, const u64* src,
-                                                            RowMap map) {
-  constexpr int N = 1 << LOG_N;
-  constexpr int N1 = 1 << LOG_N1;
-  constexpr int N2 = N / N1;
-  constexpr int TILES = N2 / kCols;
-  __shared__ __align__(16) u64 sm[N1 * kCols];
-  const int row = blockIdx.x / TILES;
-  const int j0 = (blockIdx.x % TILES) * kCols;
-  const int p = map(row);
-  const u64 q = ch.mc[p].q;
-  u64* g = data + (size_t)row * N + j0;
-  const u64* gs = src + (size_t)row * N + j0;
-  for (int i = threadIdx.x; i < N1 * kCols / 2; i += blockDim.x) {
-    const int e = 2 * i, k = e / kCols, b = e % kCols;
-    const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(gs + (size_t)k * N2 + b);
-    sm[k * kCols + b] = v.x;
-    sm[k * kCols + b + 1] = v.y;
+template <class Tile, bool FWD, bool LAZY, int OUT>
+int launch_tiles(const DevChain& ch, u64* dst, const u64* src, const Tile& tl, int ntiles,
+                 cudaStream_t st) {
+  if (ntiles <= 0) return 0;
+  const int grid = std::min(ntiles, 2 * sm_count());
+  constexpr int smem = 2 * kTile * sizeof(u64);
+  static bool attr = false;  // once per instantiation
+  if (!attr) {
+    cudaFuncSetAttribute(ntt_tiles_kernel<Tile, FWD, LAZY, OUT>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr = true;
   }
-  __syncthreads();
-  ColLayout<kCols> lay;
-  const WPair* table = (FWD ? ch.tw : ch.itw) + ((size_t)p << LOG_N);
-  const WPair* sn = FWD ? nullptr : &ch.ninv[p];
-  const WPair* sw1 = FWD ? nullptr : &ch.ninv_w1[p];
-  auto ctx = [&](int) { return ArrCtx{table, q, 1, sn, sw1}; };
-  if (FWD)
-    fwd_passes<LOG_N1, 0>(sm, kCols, lay, ctx);
-  else
-    inv_passes<LOG_N1, npass(LOG_N1) - 1>(sm, kCols, lay, ctx);
-  for (int i = threadIdx.x; i < N1 * kCols / 2; i += blockDim.x) {
-    const int e = 2 * i, k = e / kCols, b = e % kCols;
-    *reinterpret_cast<ulonglong2*>(g + (size_t)k * N2 + b) =
-        make_ulonglong2(sm[k * kCols + b], sm[k * kCols + b + 1]);
-  }
-}
-
-// Chunk stages (global stages LOG_N1 .. LOG_N-1) on NB contiguous N2-chunks.
-template <int LOG_N, int LOG_N1, bool FWD>
-__global__ void __launch_bounds__(kThreads) ntt_chunks_kernel(DevChain ch, u64* data, const u64* src,
-                                                              RowMap map) {
-  constexpr int N = 1 << LOG_N;
-  constexpr int N1 = 1 << LOG_N1;
-  constexpr int LOG_N2 = LOG_N - LOG_N1;
-  constexpr int N2 = 1 << LOG_N2;
-  constexpr int NB = 4096 / N2 > 0 ? 4096 / N2 : 1;
-  constexpr int TILES = N1 / NB;
-  __shared__ __align__(16) u64 sm[NB * N2];
-  const int row = blockIdx.x / TILES;
-  const int c0 = (blockIdx.x % TILES) * NB;
-  const int p = map(row);
-  const u64 q = ch.mc[p].q;
-  u64* g = data + (size_t)row * N + (size_t)c0 * N2;
-  const ulonglong2* g2 =
-      reinterpret_cast<const ulonglong2*>(src + (size_t)row * N + (size_t)c0 * N2);
-  for (int i = threadIdx.x; i < NB * N2 / 2; i += blockDim.x) {
-    const ulonglong2 v = g2[i];
-    sm[swz(2 * i)] = v.x;
-    sm[swz(2 * i + 1)] = v.y;
-  }
-  __syncthreads();
-  RowLayout<LOG_N2> lay;
-  const WPair* table = (FWD ? ch.tw : ch.itw) + ((size_t)p << LOG_N);
-  auto ctx = [&](int b) { return ArrCtx{table, q, N1 + c0 + b, nullptr, nullptr}; };
-  if (FWD)
-    fwd_passes<LOG_N2, 0>(sm, NB, lay, ctx);
-  else
-    inv_passes<LOG_N2, npass(LOG_N2) - 1>(sm, NB, lay, ctx);
-  ulonglong2* o2 = reinterpret_cast<ulonglong2*>(g);
-  for (int i = threadIdx.x; i < NB * N2 / 2; i += blockDim.x) {
-    u64 a = sm[swz(2 * i)], b = sm[swz(2 * i + 1)];
-    if (FWD) {
-      a = csub(csub(a, 2 * q), q);
-      b = csub(csub(b, 2 * q), q);
-    }
-    o2[i] = make_ulonglong2(a, b);
-  }
+  ntt_tiles_kernel<Tile, FWD, LAZY, OUT><<<grid, kThreads, smem, st>>>(ch, dst, src, tl, ntiles);
+  FHE_LAUNCH_CHECK();
+  return 0;
 }
 
 template <int LOG_N>
-int launch_rows(const DevChain& ch, u64* data, const u64* in, int rows, RowMap map,
-                bool inverse, cudaStream_t st) {
-  constexpr int S = 1 << LOG_N;
-  constexpr int NB = S >= 2048 ? 1 : 2048 / S;
-  const int grid = (rows + NB - 1) / NB;
-  const size_t smem = (size_t)NB * S * sizeof(u64);
-  if (inverse) {
-    if (smem > 48 * 1024)
-      cudaFuncSetAttribute(ntt_rows_kernel<LOG_N, false>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    ntt_rows_kernel<LOG_N, false><<<grid, kThreads, smem, st>>>(ch, data, in, rows, map);
-  } else {
-    if (smem > 48 * 1024)
-      cudaFuncSetAttribute(ntt_rows_kernel<LOG_N, true>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    ntt_rows_kernel<LOG_N, true><<<grid, kThreads, smem, st>>>(ch, data, in, rows, map);
-  }
-  FHE_LAUNCH_CHECK();
-  return 0;
+int launch_rows(const DevChain& ch, const NttArgs& a, bool inverse, bool lazy, cudaStream_t st) {
+  using T = RowsTile<LOG_N>;
+  T tl;
+  tl.rows = a.rows;
+  tl.map = a.map;
+  tl.src = RowAddr{a.src_bstride, a.map.limbs, LOG_N};
+  tl.dst = RowAddr{a.dst_bstride, a.map.limbs, LOG_N};
+  tl.fwd = !inverse;
+  const int ntiles = (a.rows + T::NB - 1) / T::NB;
+  if (inverse) return launch_tiles<T, false, false, OUT_RAW>(ch, a.dst, a.src, tl, ntiles, st);
+  if (lazy) return launch_tiles<T, true, true, OUT_REDUCE>(ch, a.dst, a.src, tl, ntiles, st);
+  return launch_tiles<T, true, false, OUT_CANON4>(ch, a.dst, a.src, tl, ntiles, st);
 }
 
 template <int LOG_N, int LOG_N1>
-int launch_split(const DevChain& ch, u64* data, const u64* in, int rows, RowMap map,
-                 bool inverse, cudaStream_t st) {
-  constexpr int N = 1 << LOG_N;
-  constexpr int N2 = N >> LOG_N1;
-  constexpr int NB = 4096 / N2 > 0 ? 4096 / N2 : 1;
-  const int grid_cols = rows * (N2 / kCols);
-  const int grid_chunks = rows * ((1 << LOG_N1) / NB);
+int launch_split(const DevChain& ch, const NttArgs& a, bool inverse, bool lazy,
+                 cudaStream_t st) {
+  using C = ColsTile<LOG_N, LOG_N1>;
+  using K = ChunksTile<LOG_N, LOG_N1>;
+  C ct;
+  ct.rows = a.rows;
+  ct.map = a.map;
+  ct.fwd = !inverse;
+  K kt;
+  kt.rows = a.rows;
+  kt.map = a.map;
+  kt.fwd = !inverse;
+  const RowAddr s{a.src_bstride, a.map.limbs, LOG_N}, d{a.dst_bstride, a.map.limbs, LOG_N};
+  const int nc = a.rows * C::TILES, nk = a.rows * K::TILES;
+  int rc;
   if (!inverse) {
-    ntt_cols_kernel<LOG_N, LOG_N1, true><<<grid_cols, kThreads, 0, st>>>(ch, data, in, map);
-    ntt_chunks_kernel<LOG_N, LOG_N1, true><<<grid_chunks, kThreads, 0, st>>>(ch, data, data,
-                                                                            map);
+    ct.src = s;
+    ct.dst = d;
+    kt.src = d;
+    kt.dst = d;
+    if (lazy) {
+      rc = launch_tiles<C, true, true, OUT_RAW>(ch, a.dst, a.src, ct, nc, st);
+      if (!rc) rc = launch_tiles<K, true, true, OUT_REDUCE>(ch, a.dst, a.dst, kt, nk, st);
+    } else {
+      rc = launch_tiles<C, true, false, OUT_RAW>(ch, a.dst, a.src, ct, nc, st);
+      if (!rc) rc = launch_tiles<K, true, false, OUT_CANON4>(ch, a.dst, a.dst, kt, nk, st);
+    }
   } else {
-    ntt_chunks_kernel<LOG_N, LOG_N1, false><<<grid_chunks, kThreads, 0, st>>>(ch, data, in, map);
-    ntt_cols_kernel<LOG_N, LOG_N1, false><<<grid_cols, kThreads, 0, st>>>(ch, data, data, map);
+    kt.src = s;
+    kt.dst = d;
+    ct.src = d;
+    ct.dst = d;
+    rc = launch_tiles<K, false, false, OUT_RAW>(ch, a.dst, a.src, kt, nk, st);
+    if (!rc) rc = launch_tiles<C, false, false, OUT_RAW>(ch, a.dst, a.dst, ct, nc, st);
   }
-  FHE_LAUNCH_CHECK();
-  return 0;
+  return rc;
 }
 
 }  // namespace
 
-int launch_ntt(const DevChain& ch, u64* data, const u64* in, int rows, RowMap map, bool inverse,
-               cudaStream_t st) {
-  if (rows <= 0) return 0;
+int launch_ntt(const DevChain& ch, const NttArgs& a, bool inverse, cudaStream_t st) {
+  if (a.rows <= 0) return 0;
+  const bool lazy = !inverse && ch.lazy_ok;
   switch (ch.log_n) {
-    case 1: return launch_rows<1>(ch, data, in, rows, map, inverse, st);
-    case 2: return launch_rows<2>(ch, data, in, rows, map, inverse, st);
-    case 3: return launch_rows<3>(ch, data, in, rows, map, inverse, st);
-    case 4: return launch_rows<4>(ch, data, in, rows, map, inverse, st);
-    case 5: return launch_rows<5>(ch, data, in, rows, map, inverse, st);
-    case 6: return launch_rows<6>(ch, data, in, rows, map, inverse, st);
-    case 7: return launch_rows<7>(ch, data, in, rows, map, inverse, st);
-    case 8: return launch_rows<8>(ch, data, in, rows, map, inverse, st);
-    case 9: return launch_rows<9>(ch, data, in, rows, map, inverse, st);
-    case 10: return launch_rows<10>(ch, data, in, rows, map, inverse, st);
-    case 11: return launch_rows<11>(ch, data, in, rows, map, inverse, st);
-    case 12: return launch_rows<12>(ch, data, in, rows, map, inverse, st);
-    case 13: return launch_rows<13>(ch, data, in, rows, map, inverse, st);
-    case 14: return launch_split<14, 7>(ch, data, in, rows, map, inverse, st);
-    case 15: return launch_split<15, 7>(ch, data, in, rows, map, inverse, st);
-    case 16: return launch_split<16, 8>(ch, data, in, rows, map, inverse, st);
-    case 17: return launch_split<17, 8>(ch, data, in, rows, map, inverse, st);
+    case 1: return launch_rows<1>(ch, a, inverse, lazy, st);
+    case 2: return launch_rows<2>(ch, a, inverse, lazy, st);
+    case 3: return launch_rows<3>(ch, a, inverse, lazy, st);
+    case 4: return launch_rows<4>(ch, a, inverse, lazy, st);
+    case 5: return launch_rows<5>(ch, a, inverse, lazy, st);
+    case 6: return launch_rows<6>(ch, a, inverse, lazy, st);
+    case 7: return launch_rows<7>(ch, a, inverse, lazy, st);
+    case 8: return launch_rows<8>(ch, a, inverse, lazy, st);
+    case 9: return launch_rows<9>(ch, a, inverse, lazy, st);
+    case 10: return launch_rows<10>(ch, a, inverse, lazy, st);
+    case 11: return launch_rows<11>(ch, a, inverse, lazy, st);
+    case 12: return launch_rows<12>(ch, a, inverse, lazy, st);
+    case 13: return launch_split<13, 6>(ch, a, inverse, lazy, st);
+    case 14: return launch_split<14, 7>(ch, a, inverse, lazy, st);
+    case 15: return launch_split<15, 7>(ch, a, inverse, lazy, st);
+    case 16: return launch_split<16, 8>(ch, a, inverse, lazy, st);
+    case 17: return launch_split<17, 8>(ch, a, inverse, lazy, st);
     default:
       fhe_set_error("unsupported ring degree 2^" + std::to_string(ch.log_n));
       return -1;

@@ -201,7 +201,8 @@ def galois_keygen(ctx: Context, sk: SecretKey, steps, rng: Rng | None = None,
 
 def key_switch_into(ctx: Context, level: int, d, ksk: KSwitchKey, out0, out1, add0=None,
                     add1=None, batch: int = 1, d_stride: int | None = None,
-                    io_stride: int | None = None, stream=None):
+                    add_stride: int | None = None, out_stride: int | None = None,
+                    stream=None):
     """Device key switch: out0 = add0 + b, out1 = add1 + a (fhe_keyswitch)."""
     if level > ctx.L or level < 1:
         raise LevelMismatch(f"polynomial level {level} exceeds key level")
@@ -211,8 +212,9 @@ def key_switch_into(ctx: Context, level: int, d, ksk: KSwitchKey, out0, out1, ad
     ws = ctx.workspace(ws_bytes, "keyswitch")
     _native.check(lib.fhe_keyswitch(
         ctx.handle, level, _native.ptr(d), d_stride or level * n, ksk.data._buf.data_ptr(),
-        _native.ptr(add0), _native.ptr(add1), _native.ptr(out0), _native.ptr(out1),
-        io_stride or level * n, batch, ws.data_ptr(), ws_bytes, _native.stream_handle(stream)),
+        _native.ptr(add0), _native.ptr(add1), add_stride or level * n, _native.ptr(out0),
+        _native.ptr(out1), out_stride or level * n, batch, ws.data_ptr(), ws_bytes,
+        _native.stream_handle(stream)),
         "fhe_keyswitch")
 
 

@@ -1,0 +1,117 @@
+"""Config 4 at full size (N=2^16, L=30) on the B200.
+
+* reference gadget (alpha=1, K=0): keys, ciphertexts, product, relinearised
+  and rescaled ciphertexts bit-identical to the reference's own run
+  (tests/golden/digests.json "ckks_c4", MAX_CHAIN_LEN patched to 30 exactly
+  as the reference needs);
+* hybrid dnum=3 (alpha=10, K=10 x 60-bit): bit-exact against the C oracle's
+  restatement (oracle/c/fhe_oracle.c) and decryption error within the
+  tolerance of BASELINE.md: max|dec - x*y| <= reference error + 2^-20.
+"""
+
+import numpy as np
+import pytest
+
+from fhe_testutil import digest, seeded_rng
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+
+@pytest.fixture(scope="module")
+def ref_gadget(golden):
+    import paper_2503_22227_b200.context as pctx
+    from paper_2503_22227_b200.context import Context, EncryptionParams, PoolConfig, Scheme
+
+    g = golden["ckks_c4"]
+    old = pctx.MAX_CHAIN_LEN
+    pctx.MAX_CHAIN_LEN = 30
+    try:
+        primes = tuple(int(p) for p in g["primes"])
+        ctx = Context(EncryptionParams(Scheme.CKKS, 1 << 16, primes, default_scale=g["scale"]),
+                      PoolConfig(unit_mb=200, cap_mb=4096))
+    finally:
+        pctx.MAX_CHAIN_LEN = old
+    return g, ctx
+
+
+def test_reference_gadget_bit_identical_at_config4(ref_gadget):
+    from paper_2503_22227_b200.keys import keygen, pk_gen, relin_keygen
+    from paper_2503_22227_b200.schemes import ckks
+
+    g, ctx = ref_gadget
+    sk = keygen(ctx, seeded_rng(4))
+    assert digest(sk.s.view()) == g["sk_s"]
+    pk = pk_gen(ctx, sk, seeded_rng(41))
+    rlk = relin_keygen(ctx, sk, seeded_rng(42))
+    assert digest(rlk.digits[0].view()) == g["rlk0"]
+    assert digest(rlk.digits[29].view()) == g["rlk29"]
+    vr = np.random.default_rng(9)
+    x = vr.uniform(-1, 1, ctx.n // 2)
+    y = vr.uniform(-1, 1, ctx.n // 2)
+    cx = ckks.ckks_encrypt(ctx, ckks.ckks_encode(ctx, x), pk, seeded_rng(43))
+    cy = ckks.ckks_encrypt(ctx, ckks.ckks_encode(ctx, y), pk, seeded_rng(44))
+    assert digest(cx.data.view()) == g["ct_x"] and digest(cy.data.view()) == g["ct_y"]
+    prod = ckks.ckks_multiply(ctx, cx, cy)
+    assert digest(prod.data.view()) == g["prod"]
+    lin = ckks.ckks_relinearize(ctx, prod, rlk)
+    assert digest(lin.data.view()) == g["relin"]
+    res = ckks.ckks_rescale(ctx, lin)
+    assert digest(res.data.view()) == g["rescale"]
+
+
+@pytest.fixture(scope="module")
+def hybrid():
+    from paper_2503_22227_b200.context import Context, PoolConfig, hybrid_params
+    from paper_2503_22227_b200.keys import galois_keygen, keygen, pk_gen, relin_keygen
+
+    params = hybrid_params(1 << 16, 30, bits=50, special=10, special_bits=60, dnum=3,
+                           scale=float(2 ** 49))
+    ctx = Context(params, PoolConfig(unit_mb=200, cap_mb=4096))
+    sk = keygen(ctx, seeded_rng(4))
+    return {"ctx": ctx, "sk": sk, "pk": pk_gen(ctx, sk, seeded_rng(41)),
+            "rlk": relin_keygen(ctx, sk, seeded_rng(42)),
+            "gks": galois_keygen(ctx, sk, [1], seeded_rng(45))}
+
+
+def test_hybrid_hmult_relin_rescale_bit_exact_vs_oracle(hybrid, golden):
+    from oracle import fast
+    from paper_2503_22227_b200.schemes import ckks
+
+    ctx, sk = hybrid["ctx"], hybrid["sk"]
+    vr = np.random.default_rng(9)
+    x = vr.uniform(-1, 1, ctx.n // 2)
+    y = vr.uniform(-1, 1, ctx.n // 2)
+    cx = ckks.ckks_encrypt(ctx, ckks.ckks_encode(ctx, x), hybrid["pk"], seeded_rng(43))
+    cy = ckks.ckks_encrypt(ctx, ckks.ckks_encode(ctx, y), hybrid["pk"], seeded_rng(44))
+    lin = ckks.ckks_relinearize(ctx, ckks.ckks_multiply(ctx, cx, cy), hybrid["rlk"])
+    res = ckks.ckks_rescale(ctx, lin)
+    Q, P = ctx.q_values, ctx.special_values
+    d0, d1, d2 = fast.tensor(cx.data.to_numpy(), cy.data.to_numpy(), Q)
+    keys = hybrid["rlk"].data.to_numpy().reshape(3, 2, 40, ctx.n)
+    kb, ka = fast.key_switch(d2, keys, Q, alpha=ctx.ks_alpha, special=P)
+    want = np.stack([fast.add(d0, kb, Q), fast.add(d1, ka, Q)])
+    assert np.array_equal(lin.data.to_numpy(), want)
+    assert np.array_equal(res.data.to_numpy(), fast.rescale(want, Q))
+    dec = ckks.ckks_decode(ctx, ckks.ckks_decrypt(ctx, res, sk))
+    err = float(np.max(np.abs(dec - x * y)))
+    # tolerance: reference error at these parameters + 2^-20
+    assert err <= golden["ckks_c4"]["err_mul"] + 2.0 ** -20, err
+
+
+def test_hybrid_boosted_rotate_within_tolerance(hybrid):
+    from paper_2503_22227_b200.schemes import ckks
+
+    ctx, sk = hybrid["ctx"], hybrid["sk"]
+    vr = np.random.default_rng(11)
+    x = vr.uniform(-1, 1, ctx.n // 2)
+    cx = ckks.ckks_encrypt(ctx, ckks.ckks_encode(ctx, x), hybrid["pk"], seeded_rng(46))
+    boosted = ckks.ckks_multiply_scalar(ctx, cx, 1.0, scale=float(ctx.q_values[-1]))
+    rot = ckks.ckks_rescale(ctx, ckks.ckks_rotate(ctx, boosted, 1, hybrid["gks"]))
+    dec = ckks.ckks_decode(ctx, ckks.ckks_decrypt(ctx, rot, sk))
+    # reference boosted-rotate error at config 4 is 2^-23.2
+    assert float(np.max(np.abs(dec - np.roll(x, -1)))) <= 2.0 ** -23.2 + 2.0 ** -20
+    # plain rotation is exact-permutation of slots up to key-switch noise: with
+    # hybrid key switching the noise is small enough even without boosting
+    plain = ckks.ckks_rotate(ctx, cx, 1, hybrid["gks"])
+    dec2 = ckks.ckks_decode(ctx, ckks.ckks_decrypt(ctx, plain, sk))
+    assert float(np.max(np.abs(dec2 - np.roll(x, -1)))) < 1e-6
