@@ -11,7 +11,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libfhe_sm100.so")
+LIB_PATH = os.environ.get("FHE_SM100_LIB") or os.path.join(_HERE, "lib", "libfhe_sm100.so")
 HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "fhe_sm100.h")
 
 # op codes / operand modes (mirror include/fhe_sm100.h)

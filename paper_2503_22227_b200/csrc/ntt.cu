@@ -22,8 +22,9 @@
 //    Harvey's [0,4q) forward / [0,2q) inverse butterflies (q < 2^62,
 //    modmath.py:36);
 //  * n^-1 folded into the last inverse stage;
-//  * 16-byte-granular XOR swizzle: strided passes (8-byte accesses) and
-//    contiguous passes (16-byte accesses) are both bank-conflict free;
+//  * padded shared-memory rows (16 bytes per 128): strided passes (8-byte
+//    accesses) and contiguous passes (16-byte accesses) are both
+//    bank-conflict free with immediate-offset addressing;
 //  * N <= 2^12: whole rows per tile (one HBM round trip).  N >= 2^13:
 //    four-step split N = N1 * N2: a column kernel runs the first log N1
 //    stages on [N1 x 16]-column tiles (128-byte segments), a chunk kernel
@@ -36,10 +37,14 @@ constexpr int kThreads = 256;
 constexpr int kTile = 4096;  // elements per tile (32 KB)
 constexpr int kCols = 16;    // columns per column tile (one 128-byte segment)
 
-// XOR swizzle at 16-byte granularity inside 16-element (128-byte) rows.
-__device__ __forceinline__ int swz(int i) { return i ^ (((i >> 4) & 7) << 1); }
 
-constexpr int npass(int log_s) { return (log_s + 4) / 5; }
+#ifndef FHE_NTT_MAXE
+#define FHE_NTT_MAXE 5
+#endif
+#ifndef FHE_NTT_MINB
+#define FHE_NTT_MINB 2
+#endif
+constexpr int npass(int log_s) { return (log_s + FHE_NTT_MAXE - 1) / FHE_NTT_MAXE; }
 constexpr int pass_e(int log_s, int p) {
   return log_s / npass(log_s) + (p < log_s % npass(log_s) ? 1 : 0);
 }
@@ -92,6 +97,7 @@ struct RowsTile {
   static constexpr int S = 1 << LOG_N;
   static constexpr int NB = S >= kTile ? 1 : (kTile / S > 32 ? 32 : kTile / S);
   static constexpr bool COLS = false;
+  static constexpr long GSTEP_PER_K = 1;
   int rows;
   RowMap map;
   RowAddr src, dst;
@@ -127,16 +133,20 @@ struct ColsTile {
   static constexpr int LOG_S = LOG_N1;
   static constexpr bool COLS = true;
   static constexpr int N2 = 1 << (LOG_N - LOG_N1);
+  static constexpr long GSTEP_PER_K = N2;
   static constexpr int TILES = N2 / kCols;
   int rows;
   RowMap map;
   RowAddr src, dst;
   bool fwd;
   int row, j0, p;
+  long so, dof;  // word offsets of the tile's first element in src / dst
   __device__ __forceinline__ void setup(int t) {
     row = t / TILES;
     j0 = (t % TILES) * kCols;
     p = map(row);
+    so = src(row) + j0;
+    dof = dst(row) + j0;
   }
   __device__ __forceinline__ int tile_index(int b, int k) const { return k * kCols + b; }
   __device__ __forceinline__ void split(int G, int, int& b, int& g) const {
@@ -144,10 +154,10 @@ struct ColsTile {
     g = G / kCols;
   }
   __device__ __forceinline__ const u64* gsrc(const u64* base, int b, int k) const {
-    return base + src(row) + (long)k * N2 + j0 + b;
+    return base + so + k * N2 + b;
   }
   __device__ __forceinline__ u64* gdst(u64* base, int b, int k) const {
-    return base + dst(row) + (long)k * N2 + j0 + b;
+    return base + dof + k * N2 + b;
   }
   __device__ __forceinline__ ArrCtx ctx(int, const DevChain& ch) const {
     return ArrCtx{(fwd ? ch.tw : ch.itw) + ((size_t)p << LOG_N), ch.mc[p].q, 1, p, !fwd};
@@ -162,6 +172,7 @@ struct ChunksTile {
   static constexpr int S = 1 << LOG_S;
   static constexpr int NB = kTile / S;
   static constexpr bool COLS = false;
+  static constexpr long GSTEP_PER_K = 1;
   static constexpr int N1 = 1 << LOG_N1;
   static constexpr int TILES = N1 / NB;
   int rows;
@@ -169,10 +180,13 @@ struct ChunksTile {
   RowAddr src, dst;
   bool fwd;
   int row, c0, p;
+  long so, dof;  // word offsets of the tile's first element in src / dst
   __device__ __forceinline__ void setup(int t) {
     row = t / TILES;
     c0 = (t % TILES) * NB;
     p = map(row);
+    so = src(row) + (long)c0 * S;
+    dof = dst(row) + (long)c0 * S;
   }
   __device__ __forceinline__ int tile_index(int b, int k) const { return (b << LOG_S) + k; }
   __device__ __forceinline__ void split(int G, int gpa_log, int& b, int& g) const {
@@ -180,10 +194,10 @@ struct ChunksTile {
     g = G & ((1 << gpa_log) - 1);
   }
   __device__ __forceinline__ const u64* gsrc(const u64* base, int b, int k) const {
-    return base + src(row) + (long)(c0 + b) * S + k;
+    return base + so + (b << LOG_S) + k;
   }
   __device__ __forceinline__ u64* gdst(u64* base, int b, int k) const {
-    return base + dst(row) + (long)(c0 + b) * S + k;
+    return base + dof + (b << LOG_S) + k;
   }
   __device__ __forceinline__ ArrCtx ctx(int b, const DevChain& ch) const {
     return ArrCtx{(fwd ? ch.tw : ch.itw) + ((size_t)p << LOG_N), ch.mc[p].q, N1 + c0 + b, p,
@@ -199,6 +213,14 @@ enum OutMode {
   OUT_REDUCE = 2   // forward lazy: [0, 33q) -> [0, q) by Barrett
 };
 
+// Padded shared-memory index: one 16-byte pad per 16-element (128-byte)
+// row.  Contiguous passes (16-byte accesses, lanes on different rows) and
+// strided passes (8-byte accesses, lanes on consecutive words) are both
+// bank-conflict free, and the padded index stays affine in the element
+// counter, so every shared-memory access of a pass uses an immediate offset.
+__device__ __forceinline__ int padix(int t) { return t + ((t >> 4) << 1); }
+constexpr int kTileSmem = kTile + kTile / 8;  // padded words per buffer
+
 // One register pass covering local stages R0 .. R0+E_LOG-1.
 // LAST: values go straight to global memory instead of back to the tile.
 template <int LOG_S, int R0, int E_LOG, bool FWD, bool LAZY, bool LAST, int OUT, class Tile>
@@ -207,15 +229,20 @@ __device__ __forceinline__ void run_pass(u64* sm, const Tile& tl, u64* gout,
   constexpr int E = 1 << E_LOG;
   constexpr int T0 = (1 << LOG_S) >> (R0 + 1);
   constexpr int TMIN_LOG = LOG_S - R0 - E_LOG;
+  constexpr int TMIN = 1 << TMIN_LOG;
   constexpr int GPA_LOG = LOG_S - E_LOG;
-  constexpr bool VEC = (TMIN_LOG == 0) && !Tile::COLS;
+  constexpr bool VEC = (TMIN_LOG == 0) && !Tile::COLS && E >= 2;
+  // padded stride between consecutive elements of the thread (0: not affine)
+  constexpr int PSTEP = Tile::COLS ? 18 * TMIN
+                                   : (TMIN_LOG == 0 ? 1 : (TMIN_LOG >= 4 ? TMIN + TMIN / 8 : 0));
   const int total = tl.arrays() << GPA_LOG;
   for (int G = threadIdx.x; G < total; G += blockDim.x) {
     int b, g;
     tl.split(G, GPA_LOG, b, g);
     const int hi = g >> TMIN_LOG;
-    const int lo = g & ((1 << TMIN_LOG) - 1);
+    const int lo = g & (TMIN - 1);
     const int base = hi * 2 * T0 + lo;
+    const int pb = padix(tl.tile_index(b, base));
     const ArrCtx cx = tl.ctx(b, ch);
     const u64 q = cx.q;
     const u64 q2 = 2 * q;
@@ -223,28 +250,31 @@ __device__ __forceinline__ void run_pass(u64* sm, const Tile& tl, u64* gout,
     if (VEC) {
 #pragma unroll
       for (int i = 0; i < E; i += 2) {
-        const ulonglong2 v =
-            *reinterpret_cast<const ulonglong2*>(&sm[swz(tl.tile_index(b, base + i))]);
+        const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(&sm[pb + i]);
         x[i] = v.x;
         x[i + 1] = v.y;
       }
+    } else if (PSTEP) {
+#pragma unroll
+      for (int i = 0; i < E; ++i) x[i] = sm[pb + i * PSTEP];
     } else {
 #pragma unroll
-      for (int i = 0; i < E; ++i) x[i] = sm[swz(tl.tile_index(b, base + (i << TMIN_LOG)))];
+      for (int i = 0; i < E; ++i) x[i] = sm[padix(tl.tile_index(b, base + i * TMIN))];
     }
     if (FWD) {
 #pragma unroll
       for (int rr = 0; rr < E_LOG; ++rr) {
         const int half = E >> (rr + 1);
+        const WPair* twr = cx.tw + (cx.m0 << (R0 + rr)) + (hi << rr);
 #pragma unroll
         for (int blk = 0; blk < (1 << rr); ++blk) {
-          const WPair w = cx.tw[(cx.m0 << (R0 + rr)) + (hi << rr) + blk];
+          const ulonglong2 wv = __ldg(reinterpret_cast<const ulonglong2*>(twr + blk));
 #pragma unroll
           for (int i = 0; i < half; ++i) {
             const int a = blk * 2 * half + i, c = a + half;
             u64 u = x[a];
             if (!LAZY) u = u >= q2 ? u - q2 : u;
-            const u64 v = shoup_lazy(x[c], w.w, w.sh, q);
+            const u64 v = shoup_lazy(x[c], wv.x, wv.y, q);
             x[a] = u + v;
             x[c] = u - v + q2;
           }
@@ -255,11 +285,13 @@ __device__ __forceinline__ void run_pass(u64* sm, const Tile& tl, u64* gout,
       for (int rr = E_LOG - 1; rr >= 0; --rr) {
         const int half = E >> (rr + 1);
         const bool fold = (R0 == 0) && (rr == 0) && cx.fold;
+        const WPair* twr = cx.tw + (cx.m0 << (R0 + rr)) + (hi << rr);
 #pragma unroll
         for (int blk = 0; blk < (1 << rr); ++blk) {
-          const WPair w = fold ? ch.ninv_w1[cx.prime]
-                               : cx.tw[(cx.m0 << (R0 + rr)) + (hi << rr) + blk];
-          const WPair sn = fold ? ch.ninv[cx.prime] : w;
+          const ulonglong2 wv =
+              __ldg(reinterpret_cast<const ulonglong2*>(fold ? &ch.ninv_w1[cx.prime] : twr + blk));
+          const ulonglong2 sn =
+              fold ? __ldg(reinterpret_cast<const ulonglong2*>(&ch.ninv[cx.prime])) : wv;
 #pragma unroll
           for (int i = 0; i < half; ++i) {
             const int a = blk * 2 * half + i, c = a + half;
@@ -267,11 +299,11 @@ __device__ __forceinline__ void run_pass(u64* sm, const Tile& tl, u64* gout,
             const u64 s = u + v;
             const u64 d = u - v + q2;
             if (fold) {
-              x[a] = shoup_mul(s, sn.w, sn.sh, q);
-              x[c] = shoup_mul(d, w.w, w.sh, q);
+              x[a] = shoup_mul(s, sn.x, sn.y, q);
+              x[c] = shoup_mul(d, wv.x, wv.y, q);
             } else {
               x[a] = s >= q2 ? s - q2 : s;
-              x[c] = shoup_lazy(d, w.w, w.sh, q);
+              x[c] = shoup_lazy(d, wv.x, wv.y, q);
             }
           }
         }
@@ -286,24 +318,27 @@ __device__ __forceinline__ void run_pass(u64* sm, const Tile& tl, u64* gout,
 #pragma unroll
         for (int i = 0; i < E; ++i) x[i] = reduce_word(x[i], mc);
       }
+      u64* o = tl.gdst(gout, b, base);
       if (VEC) {
-        u64* o = tl.gdst(gout, b, base);
 #pragma unroll
         for (int i = 0; i < E; i += 2)
           *reinterpret_cast<ulonglong2*>(o + i) = make_ulonglong2(x[i], x[i + 1]);
       } else {
+        constexpr long GSTEP = Tile::GSTEP_PER_K * TMIN;
 #pragma unroll
-        for (int i = 0; i < E; ++i) *tl.gdst(gout, b, base + (i << TMIN_LOG)) = x[i];
+        for (int i = 0; i < E; ++i) o[i * GSTEP] = x[i];
       }
     } else {
       if (VEC) {
 #pragma unroll
         for (int i = 0; i < E; i += 2)
-          *reinterpret_cast<ulonglong2*>(&sm[swz(tl.tile_index(b, base + i))]) =
-              make_ulonglong2(x[i], x[i + 1]);
+          *reinterpret_cast<ulonglong2*>(&sm[pb + i]) = make_ulonglong2(x[i], x[i + 1]);
+      } else if (PSTEP) {
+#pragma unroll
+        for (int i = 0; i < E; ++i) sm[pb + i * PSTEP] = x[i];
       } else {
 #pragma unroll
-        for (int i = 0; i < E; ++i) sm[swz(tl.tile_index(b, base + (i << TMIN_LOG)))] = x[i];
+        for (int i = 0; i < E; ++i) sm[padix(tl.tile_index(b, base + i * TMIN))] = x[i];
       }
     }
   }
@@ -345,6 +380,7 @@ template <class Tile>
 __device__ __forceinline__ void load_tile(u64* sm, const Tile& tl, const u64* src) {
   constexpr int LOG_S = Tile::LOG_S;
   const int nel = tl.arrays() << LOG_S;
+#pragma unroll 4
   for (int e = 2 * threadIdx.x; e < nel; e += 2 * blockDim.x) {
     int b, k;
     if (Tile::COLS) {
@@ -354,17 +390,17 @@ __device__ __forceinline__ void load_tile(u64* sm, const Tile& tl, const u64* sr
       b = e >> LOG_S;
       k = e & ((1 << LOG_S) - 1);
     }
-    cp_async16(&sm[swz(e)], tl.gsrc(src, b, k));
+    cp_async16(&sm[padix(e)], tl.gsrc(src, b, k));
   }
   cp_async_commit();
 }
 
 // Persistent, double-buffered transform kernel over the tiles of one policy.
 template <class Tile, bool FWD, bool LAZY, int OUT>
-__global__ void __launch_bounds__(kThreads, 2)
+__global__ void __launch_bounds__(kThreads, FHE_NTT_MINB)
     ntt_tiles_kernel(const DevChain ch, u64* dst, const u64* src, Tile tl, int ntiles) {
   extern __shared__ __align__(16) u64 smem_raw[];
-  u64* smem[2] = {smem_raw, smem_raw + kTile};
+  u64* smem[2] = {smem_raw, smem_raw + kTileSmem};
   int t = blockIdx.x;
   if (t >= ntiles) return;
   Tile cur = tl;
@@ -404,8 +440,8 @@ template <class Tile, bool FWD, bool LAZY, int OUT>
 int launch_tiles(const DevChain& ch, u64* dst, const u64* src, const Tile& tl, int ntiles,
                  cudaStream_t st) {
   if (ntiles <= 0) return 0;
-  const int grid = std::min(ntiles, 2 * sm_count());
-  constexpr int smem = 2 * kTile * sizeof(u64);
+  const int grid = std::min(ntiles, FHE_NTT_MINB * sm_count());
+  constexpr int smem = 2 * kTileSmem * sizeof(u64);
   static bool attr = false;  // once per instantiation
   if (!attr) {
     cudaFuncSetAttribute(ntt_tiles_kernel<Tile, FWD, LAZY, OUT>,
