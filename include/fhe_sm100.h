@@ -121,6 +121,17 @@ int fhe_keyswitch(const FheContext* ctx, int level, const uint64_t* d, int64_t d
                   int64_t add_stride, uint64_t* out0, uint64_t* out1, int64_t out_stride,
                   int batch, void* workspace, size_t ws_bytes, void* stream);
 
+/* ---- BEHZ BFV multiplication (schemes/behz.py:58-270).  `big` is the
+ *      chain Q | B | m_sk (L + S primes, S = |B| + 1).  Coefficient domain.
+ *      lift : in (polys, L, n) -> out (polys, L + S, n)   extend_to_bsk
+ *      floor: in (polys, L + S, n) tensor coefficients -> out (polys, L, n):
+ *             round(t x / Q) via fast_floor_q + fast_conv_sk_to_q.
+ *      `consts` is the device constant block documented in csrc/behz.cu. */
+int fhe_behz_lift(const FheChain* big, uint64_t* out, const uint64_t* in, int polys, int L, int S,
+                  const uint64_t* consts, void* stream);
+int fhe_behz_floor(const FheChain* big, uint64_t* out, const uint64_t* in, int polys, int L, int S,
+                   const uint64_t* consts, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

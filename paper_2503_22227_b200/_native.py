@@ -43,6 +43,8 @@ SIGNATURES = {
     "fhe_rescale_workspace": (_sz, [_vp, _int, _int]),
     "fhe_rescale": (_int, [_vp, _u64p, _u64p, _int, _int, ctypes.c_uint64, _vp, _sz, _vp]),
     "fhe_keyswitch_workspace": (_sz, [_vp, _int, _int]),
+    "fhe_behz_lift": (_int, [_vp, _u64p, _u64p, _int, _int, _int, _u64p, _vp]),
+    "fhe_behz_floor": (_int, [_vp, _u64p, _u64p, _int, _int, _int, _u64p, _vp]),
     "fhe_keyswitch": (_int, [_vp, _int, _u64p, _i64, _u64p, _u64p, _u64p, _i64, _u64p, _u64p,
                              _i64, _int, _vp, _sz, _vp]),
 }
