@@ -1,0 +1,91 @@
+"""Sharding the query's independent (atom, digit) units across GPUs.
+
+One process per GPU (torch.distributed, NCCL over NVLink/NVSwitch).  Unit i
+is computed by rank i % world; afterwards every unit's ciphertexts are
+broadcast from their owner so every rank holds the full set and the
+trees/aggregates proceed identically (one exchange of the
+per-digit ciphertexts, 0.3-0.85 MB each at N = 4096).
+
+The exchange only needs `torch.distributed` collectives, so the same code
+runs over gloo with CPU tensors (tests/test_shard_gloo.py) and over NCCL with
+the device ciphertexts in production.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+
+@dataclass
+class ShardGroup:
+    rank: int
+    world: int
+    pg: object = None          # torch.distributed process group (None: default)
+
+    @classmethod
+    def from_env(cls):
+        import torch.distributed as dist
+
+        if dist.is_available() and dist.is_initialized():
+            return cls(dist.get_rank(), dist.get_world_size())
+        return cls(0, 1)
+
+    def owner(self, i: int) -> int:
+        return i % self.world
+
+    def map_units(self, units: list, fn):
+        """Run fn(unit) for the units this rank owns, then broadcast every
+        result (a tuple of ciphertext-like objects or None) from its owner."""
+        results = [fn(u) if self.owner(i) == self.rank else None for i, u in enumerate(units)]
+        if self.world == 1:
+            return results
+        return [self._bcast(res, self.owner(i)) for i, res in enumerate(results)]
+
+    # -- exchange -------------------------------------------------------------
+    def _bcast(self, res, src: int):
+        import torch.distributed as dist
+
+        meta = [_describe(res) if self.rank == src else None]
+        dist.broadcast_object_list(meta, src=src, group=self.pg)
+        desc = meta[0]
+        out = []
+        for i, d in enumerate(desc):
+            if d is None:
+                out.append(None)
+                continue
+            ct = res[i] if self.rank == src else _allocate(d)
+            dist.broadcast(_payload(ct), src=src, group=self.pg)
+            out.append(ct)
+        return tuple(out)
+
+
+def _describe(res):
+    """Metadata needed to rebuild each ciphertext on the receivers."""
+    descs = []
+    for ct in res:
+        if ct is None:
+            descs.append(None)
+        elif hasattr(ct, "data") and hasattr(ct.data, "size_poly"):
+            d = ct.data
+            descs.append(("ckks", d.size_poly, d.size_modulus, d.n, ct.scale, ct.level,
+                          str(d._buf.device)))
+        else:  # plain tensor payloads (tests)
+            descs.append(("tensor", tuple(ct.shape), str(ct.dtype), str(ct.device)))
+    return descs
+
+
+def _allocate(d):
+    import torch
+
+    if d[0] == "tensor":
+        return torch.empty(d[1], dtype=getattr(torch, d[2].split(".")[-1]), device=d[3])
+    from ..rnspoly import CData, Domain
+    from ..schemes.ckks import CkksCiphertext
+
+    _, polys, limbs, n, scale, level, device = d
+    buf = torch.empty(polys * limbs * n, dtype=torch.int64, device=device)
+    return CkksCiphertext(CData.wrap(buf, polys, limbs, n, Domain.EVALUATION), scale, level)
+
+
+def _payload(ct):
+    return ct.data._buf if hasattr(ct, "scale") else ct

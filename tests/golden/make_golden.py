@@ -262,6 +262,7 @@ def gen_ckks_c4(out):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--big", action="store_true", help="also run config 3 and config 4")
+    ap.add_argument("--pdq", action="store_true", help="(separate entry) config 5 queries")
     args = ap.parse_args()
     path = os.path.join(HERE, "digests.json")
     out = json.load(open(path)) if os.path.exists(path) else {}
@@ -276,5 +277,68 @@ def main():
     print("wrote", path)
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and "--pdq" not in sys.argv:
     main()
+
+
+def gen_pdq(out):
+    """Config 5: the four standard queries over 1024 synthetic rows, keyed and
+    seeded exactly like the reference PdqClient (client seed 1, one Rng for
+    keys, columns and the reciprocal replies; server mask seed 20240118)."""
+    from rnsfhe.coremath.sampling import Rng as RRng
+    from rnsfhe.pdq.columns import encode_column
+    from rnsfhe.pdq.config import PdqConfig
+    from rnsfhe.pdq.dataset import make_dataset, oracle_result
+    from rnsfhe.pdq.engine import (LocalInverseClient, PdqEngine, encrypt_query_constants,
+                                   interpret_result, standard_query)
+    from rnsfhe.pdq.evaluator import CkksEval, rotation_steps
+
+    cfg = PdqConfig(base=4, digits=8, rows=1024, value_bound=1 << 16, profile="pdq")
+    ctx = Context(params_for_profile("pdq", Scheme.CKKS))
+    rng = RRng((1).to_bytes(32, "little"))
+    sk = keygen(ctx, rng)
+    pk = pk_gen(ctx, sk, rng)
+    rlk = relin_keygen(ctx, sk, rng)
+    gks = galois_keygen(ctx, sk, rotation_steps(ctx.n), rng)
+    ev = CkksEval(ctx, rlk, gks)
+    data = make_dataset(cfg, seed=20240117)
+    engine = PdqEngine(ev, cfg)
+    col_digests = {}
+    for name, vals in data.items():
+        col = encode_column(ev, cfg, name, vals, pk, rng)
+        engine.add_column(col)
+        col_digests[name] = [digest(c.data.view()) for c in col.digits] + [digest(col.value.data.view())]
+    inverse = LocalInverseClient(ev, cfg, sk, pk, rng=rng)
+    mask_rng = np.random.default_rng(20240118)
+    res = {}
+    for qid in (1, 2, 3, 4):
+        spec = standard_query(qid)
+        temps = encrypt_query_constants(ev, cfg, spec, pk, rng)
+        t0 = time.perf_counter()
+        result = engine.run(spec, channel=inverse, temps=temps, rng=mask_rng)
+        secs = time.perf_counter() - t0
+        got = interpret_result(ev, sk, result, cfg.rows)
+        want = oracle_result(spec, data)
+        rec = {"seconds": secs,
+               "cts": {k: {"sha": digest(c.data.view()), "scale": c.scale, "level": c.level}
+                       for k, c in result.cts.items()}}
+        if spec.agg == "index":
+            rec["value"] = np.asarray(got).astype(int).tolist()
+            rec["oracle_match"] = bool((np.asarray(got) == want).all())
+        elif spec.agg == "ratio":
+            rec["value_sha"] = hashlib.sha256(np.asarray(got, dtype=np.float64).tobytes()).hexdigest()
+            rec["max_err"] = float(np.max(np.abs(np.asarray(got) - want)))
+        else:
+            rec["value"] = got if not isinstance(got, tuple) else list(got)
+            rec["oracle"] = want if not isinstance(want, tuple) else list(want)
+        res[str(qid)] = rec
+    out["pdq"] = {"columns": col_digests, "queries": res, "n": ctx.n,
+                  "primes": [str(q) for q in ctx.q_values]}
+
+
+if __name__ == "__main__" and "--pdq" in sys.argv:
+    path = os.path.join(HERE, "digests.json")
+    o = json.load(open(path))
+    gen_pdq(o)
+    json.dump(o, open(path, "w"), indent=1, sort_keys=True)
+    print("wrote pdq goldens")
