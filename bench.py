@@ -34,6 +34,7 @@ N_LOG = 16
 LEVELS = 30
 DNUM = 3
 SPECIAL = 10
+SPECIAL_BITS = 50
 METRIC = "CKKS HMult+Relin ops/s at N=2^16,L=30"
 
 
@@ -140,7 +141,7 @@ def build_workload(batch: int):
     from paper_2503_22227_b200.keys import keygen, pk_gen, relin_keygen
     from paper_2503_22227_b200.schemes import ckks
 
-    params = hybrid_params(1 << N_LOG, LEVELS, bits=50, special=SPECIAL, special_bits=60,
+    params = hybrid_params(1 << N_LOG, LEVELS, bits=50, special=SPECIAL, special_bits=SPECIAL_BITS,
                            dnum=DNUM, scale=float(2 ** 49))
     ctx = Context(params, PoolConfig(unit_mb=200, cap_mb=4096))
     seed = lambda s: Rng(int(s).to_bytes(32, "little"))  # noqa: E731
@@ -351,7 +352,7 @@ def main():
         "warmup": max(args.warmup, 3), "ms_per_step": ms, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
         "config": {"workload": "config 4: CKKS HMult+Relin, N=2^16, L=30 x 50-bit, "
-                               "P=10 x 60-bit, dnum=3 (hybrid), Delta=2^49",
+                               "P=10 x 50-bit, dnum=3 (hybrid), Delta=2^49",
                    "batch_per_gpu": B, "ops_per_step": B * world,
                    "l2": "inputs larger than L2 (8 x 60 MiB pairs + 120 MiB key)"},
         "e2e": {"value": B * world / (e2e_ms / 1000.0), "unit": "ops/s",

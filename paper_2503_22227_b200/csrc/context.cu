@@ -139,9 +139,28 @@ int build_chain(const u64* primes, int count, int log_n, FheChain* ch) {
     const u64 w1 = n >= 2 ? itw[p * n + 1].w : 1;
     ninv_w1[p] = wpair(mulmod_h(w1, ni, q), q);
   }
+  bool fp64 = true;
+  for (int p = 0; p < count; ++p) fp64 &= primes[p] < ((u64)1 << 50);
+  std::vector<double2> twd, itwd, qd(count), nid(count), nwd(count);
+  if (fp64) {
+    twd.resize(count * n);
+    itwd.resize(count * n);
+    for (int p = 0; p < count; ++p) {
+      const double q = (double)primes[p];
+      for (size_t i = 0; i < n; ++i) {
+        twd[p * n + i] = make_double2((double)tw[p * n + i].w, (double)tw[p * n + i].w / q);
+        itwd[p * n + i] = make_double2((double)itw[p * n + i].w, (double)itw[p * n + i].w / q);
+      }
+      qd[p] = make_double2(q, 1.0 / q);
+      nid[p] = make_double2((double)ninv[p].w, (double)ninv[p].w / q);
+      nwd[p] = make_double2((double)ninv_w1[p].w, (double)ninv_w1[p].w / q);
+    }
+  }
   Packer pk;
   const size_t o_mc = pk.addv(mc), o_tw = pk.addv(tw), o_itw = pk.addv(itw),
                o_ni = pk.addv(ninv), o_nw = pk.addv(ninv_w1);
+  const size_t o_twd = pk.addv(twd), o_itwd = pk.addv(itwd), o_qd = pk.addv(qd),
+               o_nid = pk.addv(nid), o_nwd = pk.addv(nwd);
   void* d = nullptr;
   FHE_CUDA_CHECK(cudaMalloc(&d, pk.buf.size()));
   FHE_CUDA_CHECK(cudaMemcpy(d, pk.buf.data(), pk.buf.size(), cudaMemcpyHostToDevice));
@@ -157,6 +176,12 @@ int build_chain(const u64* primes, int count, int log_n, FheChain* ch) {
   ch->dev.ninv_w1 = (const WPair*)(b + o_nw);
   ch->dev.lazy_ok = true;
   for (int p = 0; p < count; ++p) ch->dev.lazy_ok &= primes[p] < ((u64)1 << 58);
+  ch->dev.fp64_ok = fp64;
+  ch->dev.twd = fp64 ? (const double2*)(b + o_twd) : nullptr;
+  ch->dev.itwd = fp64 ? (const double2*)(b + o_itwd) : nullptr;
+  ch->dev.qd = fp64 ? (const double2*)(b + o_qd) : nullptr;
+  ch->dev.ninv_d = fp64 ? (const double2*)(b + o_nid) : nullptr;
+  ch->dev.ninv_w1_d = fp64 ? (const double2*)(b + o_nwd) : nullptr;
   return 0;
 }
 

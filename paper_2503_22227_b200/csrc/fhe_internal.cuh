@@ -27,6 +27,13 @@ struct DevChain {
   const WPair* ninv;     // [count]      (n^-1, shoup)
   const WPair* ninv_w1;  // [count]      (ipsi_br[1] * n^-1, shoup)
   bool lazy_ok;          // every prime < 2^58: lazy forward butterflies allowed
+  // FP64-pipe tables, present when every prime is < 2^50 (fp64_ok):
+  bool fp64_ok;
+  const double2* twd;      // [count][N] (psi_br[i], psi_br[i] / q)
+  const double2* itwd;     // [count][N] (ipsi_br[i], ipsi_br[i] / q)
+  const double2* qd;       // [count]    (q, 1 / q)
+  const double2* ninv_d;   // [count]    (n^-1, n^-1 / q)
+  const double2* ninv_w1_d;// [count]    (ipsi_br[1] n^-1, ... / q)
 };
 
 // Row -> chain position mapping used by every batched kernel.  The

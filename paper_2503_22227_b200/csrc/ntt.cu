@@ -250,7 +250,7 @@ __device__ __forceinline__ void run_pass(u64* sm, const Tile& tl, u64* gout,
     if (VEC) {
 #pragma unroll
       for (int i = 0; i < E; i += 2) {
-        const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(&sm[pb + i]);
+        const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(&sm[pb + i + ((i >> 4) << 1)]);
         x[i] = v.x;
         x[i + 1] = v.y;
       }
@@ -332,7 +332,7 @@ __device__ __forceinline__ void run_pass(u64* sm, const Tile& tl, u64* gout,
       if (VEC) {
 #pragma unroll
         for (int i = 0; i < E; i += 2)
-          *reinterpret_cast<ulonglong2*>(&sm[pb + i]) = make_ulonglong2(x[i], x[i + 1]);
+          *reinterpret_cast<ulonglong2*>(&sm[pb + i + ((i >> 4) << 1)]) = make_ulonglong2(x[i], x[i + 1]);
       } else if (PSTEP) {
 #pragma unroll
         for (int i = 0; i < E; ++i) sm[pb + i * PSTEP] = x[i];
@@ -371,6 +371,183 @@ __device__ __forceinline__ void inv_passes(u64* sm, const Tile& tl, u64* gout,
     if constexpr (!last) {
       __syncthreads();
       inv_passes<LOG_S, P - 1>(sm, tl, gout, ch);
+    }
+  }
+}
+
+
+// ---------------------------------------------------------------------------
+// FP64-pipe transform for chains with every prime < 2^50.
+//
+// The integer butterfly is bound by the quarter-rate IMAD.WIDE (64-bit
+// products); B200's FP64 pipe runs DFMA at half rate.  Values are held as
+// doubles carrying signed integer representatives |x| <= q and the Shoup
+// product is done with an error-free FMA split:
+//   h = x w, l = fma(x, w, -h)            (x w = h + l exactly)
+//   k = rint(x * (w/q))                   (magic-constant rounding, |x w/q| < 2^51)
+//   t = fma(-k, q, h) + l                 (= x w - k q exactly, |t| <= q/2 + eps)
+// so every value is an exact integer and the canonical outputs are the same
+// bits as the integer path.
+constexpr double kMagic = 6755399441055744.0;  // 1.5 * 2^52
+
+__device__ __forceinline__ double fp_rint_mul(double x, double y) {
+  return __dadd_rn(__fma_rn(x, y, kMagic), -kMagic);
+}
+__device__ __forceinline__ double fp_mulmod(double x, double2 w, double q) {
+  const double h = __dmul_rn(x, w.x);
+  const double l = __fma_rn(x, w.x, -h);
+  const double k = fp_rint_mul(x, w.y);
+  return __dadd_rn(__fma_rn(-k, q, h), l);
+}
+__device__ __forceinline__ double fp_reduce(double x, double2 qd) {
+  return __fma_rn(-fp_rint_mul(x, qd.y), qd.x, x);
+}
+__device__ __forceinline__ u64 fp_canon(double x, double q) {
+  x = x < 0.0 ? __dadd_rn(x, q) : x;
+  x = x >= q ? __dadd_rn(x, -q) : x;
+  return (u64)__double2ll_rn(x);
+}
+
+enum FpIn { FPIN_DOUBLE = 0, FPIN_U64 = 1 };
+enum FpOut { FPOUT_DOUBLE = 0, FPOUT_U64 = 1 };
+
+template <int LOG_S, int R0, int E_LOG, bool FWD, bool FIRST, bool LAST, int IN, int OUT,
+          class Tile>
+__device__ __forceinline__ void run_pass_fp(u64* sm, const Tile& tl, u64* gout,
+                                            const DevChain& ch) {
+  constexpr int E = 1 << E_LOG;
+  constexpr int T0 = (1 << LOG_S) >> (R0 + 1);
+  constexpr int TMIN_LOG = LOG_S - R0 - E_LOG;
+  constexpr int TMIN = 1 << TMIN_LOG;
+  constexpr int GPA_LOG = LOG_S - E_LOG;
+  constexpr bool VEC = (TMIN_LOG == 0) && !Tile::COLS && E >= 2;
+  constexpr int PSTEP = Tile::COLS ? 18 * TMIN
+                                   : (TMIN_LOG == 0 ? 1 : (TMIN_LOG >= 4 ? TMIN + TMIN / 8 : 0));
+  const int total = tl.arrays() << GPA_LOG;
+  for (int G = threadIdx.x; G < total; G += blockDim.x) {
+    int b, g;
+    tl.split(G, GPA_LOG, b, g);
+    const int hi = g >> TMIN_LOG;
+    const int lo = g & (TMIN - 1);
+    const int base = hi * 2 * T0 + lo;
+    const int pb = padix(tl.tile_index(b, base));
+    const ArrCtx cx = tl.ctx(b, ch);
+    const double2 qd = ch.qd[cx.prime];
+    const double2* tw = (FWD ? ch.twd : ch.itwd) + ((size_t)cx.prime << ch.log_n);
+    u64 raw[E];
+    if (VEC) {
+#pragma unroll
+      for (int i = 0; i < E; i += 2) {
+        const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(&sm[pb + i + ((i >> 4) << 1)]);
+        raw[i] = v.x;
+        raw[i + 1] = v.y;
+      }
+    } else if (PSTEP) {
+#pragma unroll
+      for (int i = 0; i < E; ++i) raw[i] = sm[pb + i * PSTEP];
+    } else {
+#pragma unroll
+      for (int i = 0; i < E; ++i) raw[i] = sm[padix(tl.tile_index(b, base + i * TMIN))];
+    }
+    double x[E];
+#pragma unroll
+    for (int i = 0; i < E; ++i)
+      x[i] = (FIRST && IN == FPIN_U64) ? (double)raw[i] : __longlong_as_double((long long)raw[i]);
+    if (FWD) {
+#pragma unroll
+      for (int rr = 0; rr < E_LOG; ++rr) {
+        const int half = E >> (rr + 1);
+        const double2* twr = tw + (cx.m0 << (R0 + rr)) + (hi << rr);
+#pragma unroll
+        for (int blk = 0; blk < (1 << rr); ++blk) {
+          const double2 w = __ldg(twr + blk);
+#pragma unroll
+          for (int i = 0; i < half; ++i) {
+            const int a = blk * 2 * half + i, c = a + half;
+            const double u = fp_reduce(x[a], qd);
+            const double t = fp_mulmod(x[c], w, qd.x);
+            x[a] = __dadd_rn(u, t);
+            x[c] = __dadd_rn(u, -t);
+          }
+        }
+      }
+    } else {
+#pragma unroll
+      for (int rr = E_LOG - 1; rr >= 0; --rr) {
+        const int half = E >> (rr + 1);
+        const bool fold = (R0 == 0) && (rr == 0) && cx.fold;
+        const double2* twr = tw + (cx.m0 << (R0 + rr)) + (hi << rr);
+#pragma unroll
+        for (int blk = 0; blk < (1 << rr); ++blk) {
+          const double2 w = fold ? ch.ninv_w1_d[cx.prime] : __ldg(twr + blk);
+          const double2 sn = fold ? ch.ninv_d[cx.prime] : w;
+#pragma unroll
+          for (int i = 0; i < half; ++i) {
+            const int a = blk * 2 * half + i, c = a + half;
+            const double s = __dadd_rn(x[a], x[c]);
+            const double d = __dadd_rn(x[a], -x[c]);
+            x[a] = fold ? fp_mulmod(s, sn, qd.x) : fp_reduce(s, qd);
+            x[c] = fp_mulmod(d, w, qd.x);
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < E; ++i)
+      raw[i] = (LAST && OUT == FPOUT_U64) ? fp_canon(FWD ? fp_reduce(x[i], qd) : x[i], qd.x)
+                                          : (u64)__double_as_longlong(x[i]);
+    if (LAST) {
+      u64* o = tl.gdst(gout, b, base);
+      if (VEC) {
+#pragma unroll
+        for (int i = 0; i < E; i += 2)
+          *reinterpret_cast<ulonglong2*>(o + i) = make_ulonglong2(raw[i], raw[i + 1]);
+      } else {
+        constexpr long GSTEP = Tile::GSTEP_PER_K * TMIN;
+#pragma unroll
+        for (int i = 0; i < E; ++i) o[i * GSTEP] = raw[i];
+      }
+    } else {
+      if (VEC) {
+#pragma unroll
+        for (int i = 0; i < E; i += 2)
+          *reinterpret_cast<ulonglong2*>(&sm[pb + i + ((i >> 4) << 1)]) = make_ulonglong2(raw[i], raw[i + 1]);
+      } else if (PSTEP) {
+#pragma unroll
+        for (int i = 0; i < E; ++i) sm[pb + i * PSTEP] = raw[i];
+      } else {
+#pragma unroll
+        for (int i = 0; i < E; ++i) sm[padix(tl.tile_index(b, base + i * TMIN))] = raw[i];
+      }
+    }
+  }
+}
+
+template <int LOG_S, int P, int IN, int OUT, class Tile>
+__device__ __forceinline__ void fwd_passes_fp(u64* sm, const Tile& tl, u64* gout,
+                                              const DevChain& ch) {
+  constexpr int NP = npass(LOG_S);
+  if constexpr (P < NP) {
+    constexpr bool last = (P == NP - 1);
+    run_pass_fp<LOG_S, pass_r0(LOG_S, P), pass_e(LOG_S, P), true, P == 0, last, IN, OUT>(
+        sm, tl, gout, ch);
+    if constexpr (!last) {
+      __syncthreads();
+      fwd_passes_fp<LOG_S, P + 1, IN, OUT>(sm, tl, gout, ch);
+    }
+  }
+}
+
+template <int LOG_S, int P, int IN, int OUT, class Tile>
+__device__ __forceinline__ void inv_passes_fp(u64* sm, const Tile& tl, u64* gout,
+                                              const DevChain& ch) {
+  if constexpr (P >= 0) {
+    constexpr bool last = (P == 0);
+    run_pass_fp<LOG_S, pass_r0(LOG_S, P), pass_e(LOG_S, P), false, P == npass(LOG_S) - 1, last,
+                IN, OUT>(sm, tl, gout, ch);
+    if constexpr (!last) {
+      __syncthreads();
+      inv_passes_fp<LOG_S, P - 1, IN, OUT>(sm, tl, gout, ch);
     }
   }
 }
@@ -425,6 +602,36 @@ __global__ void __launch_bounds__(kThreads, FHE_NTT_MINB)
   }
 }
 
+// FP64-pipe variant of the persistent tile kernel.
+template <class Tile, bool FWD, int IN, int OUT>
+__global__ void __launch_bounds__(kThreads, FHE_NTT_MINB)
+    ntt_tiles_fp_kernel(const DevChain ch, u64* dst, const u64* src, Tile tl, int ntiles) {
+  extern __shared__ __align__(16) u64 smem_raw[];
+  u64* smem[2] = {smem_raw, smem_raw + kTileSmem};
+  int t = blockIdx.x;
+  if (t >= ntiles) return;
+  Tile cur = tl;
+  cur.setup(t);
+  load_tile(smem[0], cur, src);
+  int buf = 0;
+  for (; t < ntiles; t += gridDim.x) {
+    cp_async_wait_all();
+    __syncthreads();
+    const int tn = t + gridDim.x;
+    if (tn < ntiles) {
+      Tile nxt = tl;
+      nxt.setup(tn);
+      load_tile(smem[buf ^ 1], nxt, src);
+    }
+    if (FWD)
+      fwd_passes_fp<Tile::LOG_S, 0, IN, OUT>(smem[buf], cur, dst, ch);
+    else
+      inv_passes_fp<Tile::LOG_S, npass(Tile::LOG_S) - 1, IN, OUT>(smem[buf], cur, dst, ch);
+    if (tn < ntiles) cur.setup(tn);
+    buf ^= 1;
+  }
+}
+
 int g_sm_count = 0;
 int sm_count() {
   if (!g_sm_count) {
@@ -453,6 +660,24 @@ int launch_tiles(const DevChain& ch, u64* dst, const u64* src, const Tile& tl, i
   return 0;
 }
 
+
+template <class Tile, bool FWD, int IN, int OUT>
+int launch_tiles_fp(const DevChain& ch, u64* dst, const u64* src, const Tile& tl, int ntiles,
+                    cudaStream_t st) {
+  if (ntiles <= 0) return 0;
+  const int grid = std::min(ntiles, FHE_NTT_MINB * sm_count());
+  constexpr int smem = 2 * kTileSmem * sizeof(u64);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(ntt_tiles_fp_kernel<Tile, FWD, IN, OUT>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr = true;
+  }
+  ntt_tiles_fp_kernel<Tile, FWD, IN, OUT><<<grid, kThreads, smem, st>>>(ch, dst, src, tl, ntiles);
+  FHE_LAUNCH_CHECK();
+  return 0;
+}
+
 template <int LOG_N>
 int launch_rows(const DevChain& ch, const NttArgs& a, bool inverse, bool lazy, cudaStream_t st) {
   using T = RowsTile<LOG_N>;
@@ -463,6 +688,9 @@ int launch_rows(const DevChain& ch, const NttArgs& a, bool inverse, bool lazy, c
   tl.dst = RowAddr{a.dst_bstride, a.map.limbs, LOG_N};
   tl.fwd = !inverse;
   const int ntiles = (a.rows + T::NB - 1) / T::NB;
+  if (ch.fp64_ok)
+    return inverse ? launch_tiles_fp<T, false, FPIN_U64, FPOUT_U64>(ch, a.dst, a.src, tl, ntiles, st)
+                   : launch_tiles_fp<T, true, FPIN_U64, FPOUT_U64>(ch, a.dst, a.src, tl, ntiles, st);
   if (inverse) return launch_tiles<T, false, false, OUT_RAW>(ch, a.dst, a.src, tl, ntiles, st);
   if (lazy) return launch_tiles<T, true, true, OUT_REDUCE>(ch, a.dst, a.src, tl, ntiles, st);
   return launch_tiles<T, true, false, OUT_CANON4>(ch, a.dst, a.src, tl, ntiles, st);
@@ -484,6 +712,24 @@ int launch_split(const DevChain& ch, const NttArgs& a, bool inverse, bool lazy,
   const RowAddr s{a.src_bstride, a.map.limbs, LOG_N}, d{a.dst_bstride, a.map.limbs, LOG_N};
   const int nc = a.rows * C::TILES, nk = a.rows * K::TILES;
   int rc;
+  if (ch.fp64_ok) {
+    if (!inverse) {
+      ct.src = s;
+      ct.dst = d;
+      kt.src = d;
+      kt.dst = d;
+      rc = launch_tiles_fp<C, true, FPIN_U64, FPOUT_DOUBLE>(ch, a.dst, a.src, ct, nc, st);
+      if (!rc) rc = launch_tiles_fp<K, true, FPIN_DOUBLE, FPOUT_U64>(ch, a.dst, a.dst, kt, nk, st);
+    } else {
+      kt.src = s;
+      kt.dst = d;
+      ct.src = d;
+      ct.dst = d;
+      rc = launch_tiles_fp<K, false, FPIN_U64, FPOUT_DOUBLE>(ch, a.dst, a.src, kt, nk, st);
+      if (!rc) rc = launch_tiles_fp<C, false, FPIN_DOUBLE, FPOUT_U64>(ch, a.dst, a.dst, ct, nc, st);
+    }
+    return rc;
+  }
   if (!inverse) {
     ct.src = s;
     ct.dst = d;

@@ -59,13 +59,14 @@ def test_reference_gadget_bit_identical_at_config4(ref_gadget):
     assert digest(res.data.view()) == g["rescale"]
 
 
-@pytest.fixture(scope="module")
-def hybrid():
+@pytest.fixture(scope="module", params=[50, 60], ids=["P50_fp64", "P60_int"])
+def hybrid(request):
+    """P = 10 x 50-bit (FP64-pipe NTT path) and 10 x 60-bit (integer path)."""
     from paper_2503_22227_b200.context import Context, PoolConfig, hybrid_params
     from paper_2503_22227_b200.keys import galois_keygen, keygen, pk_gen, relin_keygen
 
-    params = hybrid_params(1 << 16, 30, bits=50, special=10, special_bits=60, dnum=3,
-                           scale=float(2 ** 49))
+    params = hybrid_params(1 << 16, 30, bits=50, special=10, special_bits=request.param,
+                           dnum=3, scale=float(2 ** 49))
     ctx = Context(params, PoolConfig(unit_mb=200, cap_mb=4096))
     sk = keygen(ctx, seeded_rng(4))
     return {"ctx": ctx, "sk": sk, "pk": pk_gen(ctx, sk, seeded_rng(41)),
