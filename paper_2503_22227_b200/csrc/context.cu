@@ -254,10 +254,36 @@ int build_levels(FheContext* ctx) {
       rs_inv[j] = wpair(invmod_h(pr[l - 1] % pr[j], pr[j]), pr[j]);
       rs_qlast[j] = pr[l - 1] % pr[j];
     }
+    // FP64 pairs (value, value / modulus) for the FP64-pipe base conversions
+    const bool fp64 = ctx->chain->dev.fp64_ok;
+    std::vector<double2> up_inv_d, up_w_d, down_inv_d, down_w_d;
+    if (fp64) {
+      for (int s = 0; s < l; ++s)
+        up_inv_d.push_back(make_double2((double)up_inv[s].w, (double)up_inv[s].w / (double)pr[s]));
+      for (int di = 0; di < D; ++di) {
+        const int s0 = lp.dig_s0[di], na = lp.dig_na[di], nt = l + K - na;
+        for (int s = 0; s < na; ++s)
+          for (int t = 0; t < nt; ++t) {
+            const int m = t < s0 ? t : t + na;
+            const u64 w = up_w[lp.dig_w_off[di] + s * nt + t];
+            up_w_d.push_back(make_double2((double)w, (double)w / (double)pr[cp(m)]));
+          }
+      }
+      for (int k = 0; k < K; ++k)
+        down_inv_d.push_back(
+            make_double2((double)down_inv[k].w, (double)down_inv[k].w / (double)pr[L + k]));
+      for (int k = 0; k < K; ++k)
+        for (int j = 0; j < l; ++j) {
+          const u64 w = down_w[(size_t)k * l + j];
+          down_w_d.push_back(make_double2((double)w, (double)w / (double)pr[j]));
+        }
+    }
     Packer pk;
     const size_t o1 = pk.addv(up_inv), o2 = pk.addv(up_w), o3 = pk.addv(ext_prime),
                  o4 = pk.addv(info), o5 = pk.addv(down_inv), o6 = pk.addv(down_w),
                  o7 = pk.addv(p_inv), o8 = pk.addv(rs_inv), o9 = pk.addv(rs_qlast);
+    const size_t o10 = pk.addv(up_inv_d), o11 = pk.addv(up_w_d), o12 = pk.addv(down_inv_d),
+                 o13 = pk.addv(down_w_d);
     void* d = nullptr;
     FHE_CUDA_CHECK(cudaMalloc(&d, pk.buf.size()));
     FHE_CUDA_CHECK(cudaMemcpy(d, pk.buf.data(), pk.buf.size(), cudaMemcpyHostToDevice));
@@ -272,6 +298,12 @@ int build_levels(FheContext* ctx) {
     lp.p_inv = (const WPair*)(b + o7);
     lp.rs_inv = (const WPair*)(b + o8);
     lp.rs_qlast = (const u64*)(b + o9);
+    if (fp64) {
+      lp.up_inv_d = (const double2*)(b + o10);
+      lp.up_w_d = (const double2*)(b + o11);
+      lp.down_inv_d = (const double2*)(b + o12);
+      lp.down_w_d = (const double2*)(b + o13);
+    }
   }
   return 0;
 }

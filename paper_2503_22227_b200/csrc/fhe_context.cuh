@@ -33,6 +33,11 @@ struct LevelPlan {
   const WPair* p_inv = nullptr;      // [l] P^-1 mod q_j
   const WPair* rs_inv = nullptr;     // [l-1] q_{l-1}^-1 mod q_j
   const u64* rs_qlast = nullptr;     // [l-1] q_{l-1} mod q_j
+  // FP64-pipe copies (w, w / modulus) when every chain prime is < 2^50
+  const double2* up_inv_d = nullptr;
+  const double2* up_w_d = nullptr;
+  const double2* down_inv_d = nullptr;
+  const double2* down_w_d = nullptr;
   void* dmem = nullptr;
 };
 

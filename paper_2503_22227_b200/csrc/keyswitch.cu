@@ -15,6 +15,7 @@
 // are the input itself, so the INTT/NTT round trip of the reference
 // (NTT(INTT(d) mod q_i) = d) is skipped without changing a bit.
 #include "fhe_context.cuh"
+#include "fparith.cuh"
 
 namespace {
 
@@ -131,24 +132,59 @@ __global__ void __launch_bounds__(kThreads)
         }
       }
     }
-    for (int b = 0; b < batch; ++b) {
-      u64 rb, ra;
-      if (cached) {
-        u64 bh = 0, bl = 0, ah = 0, al = 0;
+    if (cached) {
+      // four batch items per iteration: all their operand loads are issued
+      // before the first multiply, hiding HBM latency across the batch
+      const u64* src[kCache];
+      long sstr[kCache];
 #pragma unroll
-        for (int di = 0; di < kCache; ++di) {
-          if (di < D) {
-            const int s0 = sinfo[4 * di], na = sinfo[4 * di + 1], ro = sinfo[4 * di + 2];
-            const u64 v = (m >= s0 && m < s0 + na)
-                              ? d[b * d_stride + (long)m * n + i]
-                              : ext[b * ext_stride + (long)(ro + (m < s0 ? m : m - na)) * n + i];
-            mac_wide(bh, bl, v, kbc[di]);
-            mac_wide(ah, al, v, kac[di]);
+      for (int di = 0; di < kCache; ++di) {
+        if (di < D) {
+          const int s0 = sinfo[4 * di], na = sinfo[4 * di + 1], ro = sinfo[4 * di + 2];
+          const bool own = m >= s0 && m < s0 + na;
+          src[di] = own ? d + (long)m * n + i : ext + (long)(ro + (m < s0 ? m : m - na)) * n + i;
+          sstr[di] = own ? d_stride : ext_stride;
+        }
+      }
+      for (int b0 = 0; b0 < batch; b0 += 4) {
+        u64 v[4][kCache];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int di = 0; di < kCache; ++di)
+            if (di < D && b0 + u < batch) v[u][di] = __ldg(src[di] + (b0 + u) * sstr[di]);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (b0 + u >= batch) break;
+          const int b = b0 + u;
+          u64 bh = 0, bl = 0, ah = 0, al = 0;
+#pragma unroll
+          for (int di = 0; di < kCache; ++di) {
+            if (di < D) {
+              mac_wide(bh, bl, v[u][di], kbc[di]);
+              mac_wide(ah, al, v[u][di], kac[di]);
+            }
+          }
+          const u64 rb = reduce_fold(bh, bl, mc), ra = reduce_fold(ah, al, mc);
+          if (K == 0) {
+            const long o = b * out_stride + (long)m * n + i;
+            const long ai = b * add_stride + (long)m * n + i;
+            out0[o] = add0 ? add_mod(add0[ai], rb, mc.q) : rb;
+            out1[o] = add1 ? add_mod(add1[ai], ra, mc.q) : ra;
+          } else if (m < level) {
+            accQ[((long)(b * 2 + 0) * level + m) * n + i] = rb;
+            accQ[((long)(b * 2 + 1) * level + m) * n + i] = ra;
+          } else {
+            accP[((long)(b * 2 + 0) * K + (m - level)) * n + i] = rb;
+            accP[((long)(b * 2 + 1) * K + (m - level)) * n + i] = ra;
           }
         }
-        rb = reduce_fold(bh, bl, mc);
-        ra = reduce_fold(ah, al, mc);
-      } else {
+      }
+      continue;
+    }
+    for (int b = 0; b < batch; ++b) {
+      u64 rb, ra;
+      {
         Acc ab, aa;
         for (int di = 0; di < D; ++di) {
           const int s0 = sinfo[4 * di], na = sinfo[4 * di + 1], ro = sinfo[4 * di + 2];
@@ -255,6 +291,131 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
+// ---------------------------------------------------------------------------
+// FP64-pipe base conversions (every chain prime < 2^50): each term
+// y_s * w_{s,m} mod p is an exact fp_mulmod (fparith.cuh) with w/p
+// precomputed; up to 16 signed terms of |.| <= p/2 + eps sum exactly in a
+// double (< 2^53) and are reduced once.  The same integers as the 128-bit
+// integer accumulation, at half the pipe cost of the quarter-rate
+// IMAD.WIDE products.
+
+// canonical [0, q) representative as a double
+__device__ __forceinline__ double fp_pos(double x, double q) { return x < 0.0 ? __dadd_rn(x, q) : x; }
+
+__global__ void __launch_bounds__(kThreads)
+    modup_fp_kernel(const DevChain ch, const u64* __restrict__ c, long c_stride,
+                    u64* __restrict__ ext, long ext_stride, const int* __restrict__ dig_info,
+                    const double2* __restrict__ up_inv, const double2* __restrict__ up_w, int level,
+                    int K, int L) {
+  const int di = blockIdx.y, b = blockIdx.z;
+  const int s0 = dig_info[4 * di], na = dig_info[4 * di + 1];
+  const int row_off = dig_info[4 * di + 2], w_off = dig_info[4 * di + 3];
+  const int nt = level + K - na;
+  extern __shared__ double2 swd[];
+  for (int i = threadIdx.x; i < na * nt; i += blockDim.x) swd[i] = up_w[w_off + i];
+  __syncthreads();
+  const int log_n = ch.log_n;
+  const long n = 1L << log_n;
+  const u64* cb = c + b * c_stride;
+  u64* eb = ext + b * ext_stride + (long)row_off * n;
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n;
+       i += (long)gridDim.x * blockDim.x) {
+    double y[kMaxAlpha];
+#pragma unroll
+    for (int s = 0; s < kMaxAlpha; ++s) {
+      if (s < na) {
+        const double q = ch.qd[s0 + s].x;
+        // y_s = [c_s (Q_d/q_s)^-1]_{q_s}, canonical: the conversion is an
+        // integer-level formula, so the representative matters
+        y[s] = fp_pos(fp_mulmod((double)cb[(long)(s0 + s) * n + i], up_inv[s0 + s], q), q);
+      }
+    }
+    int t = 0;
+    for (; t + 4 <= nt; t += 4) {
+      double acc[4] = {0.0, 0.0, 0.0, 0.0};
+      double pq[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int m = t + u < s0 ? t + u : t + u + na;
+        pq[u] = ch.qd[m < level ? m : L + (m - level)].x;
+      }
+#pragma unroll
+      for (int s = 0; s < kMaxAlpha; ++s) {
+        if (s < na) {
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            acc[u] = __dadd_rn(acc[u], fp_mulmod(y[s], swd[s * nt + t + u], pq[u]));
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int m = t + u < s0 ? t + u : t + u + na;
+        const double2 qd = ch.qd[m < level ? m : L + (m - level)];
+        eb[(long)(t + u) * n + i] = fp_canon(fp_reduce(acc[u], qd), qd.x);
+      }
+    }
+    for (; t < nt; ++t) {
+      const int m = t < s0 ? t : t + na;
+      const double2 qd = ch.qd[m < level ? m : L + (m - level)];
+      double acc = 0.0;
+#pragma unroll
+      for (int s = 0; s < kMaxAlpha; ++s)
+        if (s < na) acc = __dadd_rn(acc, fp_mulmod(y[s], swd[s * nt + t], qd.x));
+      eb[(long)t * n + i] = fp_canon(fp_reduce(acc, qd), qd.x);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kThreads)
+    moddown_conv_fp_kernel(const DevChain ch, const u64* __restrict__ accP,
+                           u64* __restrict__ conv, const double2* __restrict__ down_inv,
+                           const double2* __restrict__ down_w, int level, int K, int L) {
+  extern __shared__ double2 swd[];
+  for (int i = threadIdx.x; i < K * level; i += blockDim.x) swd[i] = down_w[i];
+  __syncthreads();
+  const int bp = blockIdx.y;
+  const int log_n = ch.log_n;
+  const long n = 1L << log_n;
+  const u64* src = accP + (long)bp * K * n;
+  u64* dst = conv + (long)bp * level * n;
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n;
+       i += (long)gridDim.x * blockDim.x) {
+    double y[kMaxAlpha];
+#pragma unroll
+    for (int k = 0; k < kMaxAlpha; ++k) {
+      if (k < K) {
+        const double p = ch.qd[L + k].x;
+        y[k] = fp_pos(fp_mulmod((double)src[(long)k * n + i], down_inv[k], p), p);
+      }
+    }
+    int j = 0;
+    for (; j + 4 <= level; j += 4) {
+      double acc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+      for (int k = 0; k < kMaxAlpha; ++k) {
+        if (k < K) {
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            acc[u] = __dadd_rn(acc[u], fp_mulmod(y[k], swd[k * level + j + u], ch.qd[j + u].x));
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const double2 qd = ch.qd[j + u];
+        dst[(long)(j + u) * n + i] = fp_canon(fp_reduce(acc[u], qd), qd.x);
+      }
+    }
+    for (; j < level; ++j) {
+      const double2 qd = ch.qd[j];
+      double acc = 0.0;
+#pragma unroll
+      for (int k = 0; k < kMaxAlpha; ++k)
+        if (k < K) acc = __dadd_rn(acc, fp_mulmod(y[k], swd[k * level + j], qd.x));
+      dst[(long)j * n + i] = fp_canon(fp_reduce(acc, qd), qd.x);
+    }
+  }
+}
+
 int mac_chunk(const std::vector<u64>& primes) {
   u64 mx = 0;
   for (u64 p : primes) mx = p > mx ? p : mx;
@@ -311,11 +472,22 @@ int run_keyswitch(const FheContext& ctx, int level, const u64* d, long d_stride,
       max_w = std::max(max_w, lp.dig_na[di] * (level + K - lp.dig_na[di]));
     const size_t smem = (size_t)max_w * sizeof(u64);
     dim3 grid((unsigned)std::max<long>(1, std::min<long>(n / kThreads, 1024)), lp.digits, batch);
-    if (smem > 48 * 1024)
-      cudaFuncSetAttribute(modup_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    modup_kernel<<<grid, kThreads, smem, st>>>(ch, c, (long)level * n, ext,
-                                               (long)lp.ext_rows * n, lp.dig_info, lp.up_inv,
-                                               lp.up_w, level, K, L, chunk);
+    if (ch.fp64_ok && lp.up_w_d) {
+      const size_t smem_d = (size_t)max_w * sizeof(double2);
+      if (smem_d > 48 * 1024)
+        cudaFuncSetAttribute(modup_fp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem_d);
+      modup_fp_kernel<<<grid, kThreads, smem_d, st>>>(ch, c, (long)level * n, ext,
+                                                      (long)lp.ext_rows * n, lp.dig_info,
+                                                      lp.up_inv_d, lp.up_w_d, level, K, L);
+    } else {
+      if (smem > 48 * 1024)
+        cudaFuncSetAttribute(modup_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+      modup_kernel<<<grid, kThreads, smem, st>>>(ch, c, (long)level * n, ext,
+                                                 (long)lp.ext_rows * n, lp.dig_info, lp.up_inv,
+                                                 lp.up_w, level, K, L, chunk);
+    }
     FHE_LAUNCH_CHECK();
     if (lp.ext_rows > 0) {
       rc = launch_ntt(ch, ext, ext, batch * lp.ext_rows,
@@ -338,8 +510,12 @@ int run_keyswitch(const FheContext& ctx, int level, const u64* d, long d_stride,
   {
     const size_t smem = (size_t)K * level * sizeof(u64);
     dim3 grid((unsigned)std::max<long>(1, std::min<long>(n / kThreads, 1024)), batch * 2);
-    moddown_conv_kernel<<<grid, kThreads, smem, st>>>(ch, accP, conv, lp.down_inv, lp.down_w,
-                                                      level, K, L, chunk);
+    if (ch.fp64_ok && lp.down_w_d)
+      moddown_conv_fp_kernel<<<grid, kThreads, 2 * smem, st>>>(ch, accP, conv, lp.down_inv_d,
+                                                               lp.down_w_d, level, K, L);
+    else
+      moddown_conv_kernel<<<grid, kThreads, smem, st>>>(ch, accP, conv, lp.down_inv, lp.down_w,
+                                                        level, K, L, chunk);
     FHE_LAUNCH_CHECK();
   }
   rc = launch_ntt(ch, conv, conv, batch * 2 * level, RowMap{nullptr, level, 0}, false, st);

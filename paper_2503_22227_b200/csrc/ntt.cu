@@ -30,6 +30,7 @@
 //    stages on [N1 x 16]-column tiles (128-byte segments), a chunk kernel
 //    the remaining log N2 stages on contiguous N2-chunks.
 #include "fhe_kernels.cuh"
+#include "fparith.cuh"
 
 namespace {
 
@@ -388,26 +389,6 @@ __device__ __forceinline__ void inv_passes(u64* sm, const Tile& tl, u64* gout,
 //   t = fma(-k, q, h) + l                 (= x w - k q exactly, |t| <= q/2 + eps)
 // so every value is an exact integer and the canonical outputs are the same
 // bits as the integer path.
-constexpr double kMagic = 6755399441055744.0;  // 1.5 * 2^52
-
-__device__ __forceinline__ double fp_rint_mul(double x, double y) {
-  return __dadd_rn(__fma_rn(x, y, kMagic), -kMagic);
-}
-__device__ __forceinline__ double fp_mulmod(double x, double2 w, double q) {
-  const double h = __dmul_rn(x, w.x);
-  const double l = __fma_rn(x, w.x, -h);
-  const double k = fp_rint_mul(x, w.y);
-  return __dadd_rn(__fma_rn(-k, q, h), l);
-}
-__device__ __forceinline__ double fp_reduce(double x, double2 qd) {
-  return __fma_rn(-fp_rint_mul(x, qd.y), qd.x, x);
-}
-__device__ __forceinline__ u64 fp_canon(double x, double q) {
-  x = x < 0.0 ? __dadd_rn(x, q) : x;
-  x = x >= q ? __dadd_rn(x, -q) : x;
-  return (u64)__double2ll_rn(x);
-}
-
 enum FpIn { FPIN_DOUBLE = 0, FPIN_U64 = 1 };
 enum FpOut { FPOUT_DOUBLE = 0, FPOUT_U64 = 1 };
 
