@@ -36,3 +36,9 @@ __device__ __forceinline__ u64 fp_canon(double x, double q) {
   x = x >= q ? __dadd_rn(x, -q) : x;
   return (u64)__double2ll_rn(x);
 }
+
+// representative in [-q/2 - eps, q/2 + eps] (fp_reduce / fp_mulmod output)
+// -> canonical u64 in [0, q)
+__device__ __forceinline__ u64 fp_canon_half(double x, double q) {
+  return (u64)__double2ll_rn(x < 0.0 ? __dadd_rn(x, q) : x);
+}

@@ -104,6 +104,7 @@ struct RowsTile {
   RowAddr src, dst;
   bool fwd;
   int row0, nb;
+  bool valid = true;
   int prime[NB];
   __device__ __forceinline__ void setup(int t) {
     row0 = t * NB;
@@ -141,6 +142,7 @@ struct ColsTile {
   RowAddr src, dst;
   bool fwd;
   int row, j0, p;
+  bool valid = true;
   long so, dof;  // word offsets of the tile's first element in src / dst
   __device__ __forceinline__ void setup(int t) {
     row = t / TILES;
@@ -181,10 +183,19 @@ struct ChunksTile {
   RowAddr src, dst;
   bool fwd;
   int row, c0, p;
+  int rpc = 1;  // rows per residue class (rows sharing a prime: r0 + k * map.limbs)
+  bool valid = true;
   long so, dof;  // word offsets of the tile's first element in src / dst
+  // Tile order: (residue class r0, chunk block, k).  Consecutive tiles of a
+  // CTA share the prime and the chunk range, so their twiddles (distinct per
+  // chunk in these stages) stay in L1 across the rows of the batch.
   __device__ __forceinline__ void setup(int t) {
-    row = t / TILES;
-    c0 = (t % TILES) * NB;
+    const int k = t % rpc;
+    const int u = t / rpc;
+    row = (u / TILES) + k * map.limbs;
+    c0 = (u % TILES) * NB;
+    valid = row < rows;
+    if (!valid) return;
     p = map(row);
     so = src(row) + (long)c0 * S;
     dof = dst(row) + (long)c0 * S;
@@ -475,7 +486,7 @@ __device__ __forceinline__ void run_pass_fp(u64* sm, const Tile& tl, u64* gout,
     }
 #pragma unroll
     for (int i = 0; i < E; ++i)
-      raw[i] = (LAST && OUT == FPOUT_U64) ? fp_canon(FWD ? fp_reduce(x[i], qd) : x[i], qd.x)
+      raw[i] = (LAST && OUT == FPOUT_U64) ? fp_canon_half(FWD ? fp_reduce(x[i], qd) : x[i], qd.x)
                                           : (u64)__double_as_longlong(x[i]);
     if (LAST) {
       u64* o = tl.gdst(gout, b, base);
@@ -559,26 +570,32 @@ __global__ void __launch_bounds__(kThreads, FHE_NTT_MINB)
     ntt_tiles_kernel(const DevChain ch, u64* dst, const u64* src, Tile tl, int ntiles) {
   extern __shared__ __align__(16) u64 smem_raw[];
   u64* smem[2] = {smem_raw, smem_raw + kTileSmem};
-  int t = blockIdx.x;
-  if (t >= ntiles) return;
+  // contiguous tile range per CTA (keeps the tile order's twiddle locality)
+  const int t_end = (int)(((long)(blockIdx.x + 1) * ntiles) / gridDim.x);
+  int t = (int)(((long)blockIdx.x * ntiles) / gridDim.x);
+  if (t >= t_end) return;
   Tile cur = tl;
   cur.setup(t);
-  load_tile(smem[0], cur, src);
+  if (cur.valid) load_tile(smem[0], cur, src);
+  else cp_async_commit();
   int buf = 0;
-  for (; t < ntiles; t += gridDim.x) {
+  for (; t < t_end; ++t) {
     cp_async_wait_all();
     __syncthreads();
-    const int tn = t + gridDim.x;
-    if (tn < ntiles) {
+    const int tn = t + 1;
+    if (tn < t_end) {
       Tile nxt = tl;
       nxt.setup(tn);
-      load_tile(smem[buf ^ 1], nxt, src);
+      if (nxt.valid) load_tile(smem[buf ^ 1], nxt, src);
+      else cp_async_commit();
     }
-    if (FWD)
-      fwd_passes<Tile::LOG_S, 0, LAZY, OUT>(smem[buf], cur, dst, ch);
-    else
-      inv_passes<Tile::LOG_S, npass(Tile::LOG_S) - 1>(smem[buf], cur, dst, ch);
-    if (tn < ntiles) cur.setup(tn);
+    if (cur.valid) {
+      if (FWD)
+        fwd_passes<Tile::LOG_S, 0, LAZY, OUT>(smem[buf], cur, dst, ch);
+      else
+        inv_passes<Tile::LOG_S, npass(Tile::LOG_S) - 1>(smem[buf], cur, dst, ch);
+    }
+    if (tn < t_end) cur.setup(tn);
     buf ^= 1;
   }
 }
@@ -589,26 +606,32 @@ __global__ void __launch_bounds__(kThreads, FHE_NTT_MINB)
     ntt_tiles_fp_kernel(const DevChain ch, u64* dst, const u64* src, Tile tl, int ntiles) {
   extern __shared__ __align__(16) u64 smem_raw[];
   u64* smem[2] = {smem_raw, smem_raw + kTileSmem};
-  int t = blockIdx.x;
-  if (t >= ntiles) return;
+  // contiguous tile range per CTA (keeps the tile order's twiddle locality)
+  const int t_end = (int)(((long)(blockIdx.x + 1) * ntiles) / gridDim.x);
+  int t = (int)(((long)blockIdx.x * ntiles) / gridDim.x);
+  if (t >= t_end) return;
   Tile cur = tl;
   cur.setup(t);
-  load_tile(smem[0], cur, src);
+  if (cur.valid) load_tile(smem[0], cur, src);
+  else cp_async_commit();
   int buf = 0;
-  for (; t < ntiles; t += gridDim.x) {
+  for (; t < t_end; ++t) {
     cp_async_wait_all();
     __syncthreads();
-    const int tn = t + gridDim.x;
-    if (tn < ntiles) {
+    const int tn = t + 1;
+    if (tn < t_end) {
       Tile nxt = tl;
       nxt.setup(tn);
-      load_tile(smem[buf ^ 1], nxt, src);
+      if (nxt.valid) load_tile(smem[buf ^ 1], nxt, src);
+      else cp_async_commit();
     }
-    if (FWD)
-      fwd_passes_fp<Tile::LOG_S, 0, IN, OUT>(smem[buf], cur, dst, ch);
-    else
-      inv_passes_fp<Tile::LOG_S, npass(Tile::LOG_S) - 1, IN, OUT>(smem[buf], cur, dst, ch);
-    if (tn < ntiles) cur.setup(tn);
+    if (cur.valid) {
+      if (FWD)
+        fwd_passes_fp<Tile::LOG_S, 0, IN, OUT>(smem[buf], cur, dst, ch);
+      else
+        inv_passes_fp<Tile::LOG_S, npass(Tile::LOG_S) - 1, IN, OUT>(smem[buf], cur, dst, ch);
+    }
+    if (tn < t_end) cur.setup(tn);
     buf ^= 1;
   }
 }
@@ -691,7 +714,9 @@ int launch_split(const DevChain& ch, const NttArgs& a, bool inverse, bool lazy,
   kt.map = a.map;
   kt.fwd = !inverse;
   const RowAddr s{a.src_bstride, a.map.limbs, LOG_N}, d{a.dst_bstride, a.map.limbs, LOG_N};
-  const int nc = a.rows * C::TILES, nk = a.rows * K::TILES;
+  const int classes = std::min(a.map.limbs, a.rows);
+  kt.rpc = (a.rows + a.map.limbs - 1) / a.map.limbs;
+  const int nc = a.rows * C::TILES, nk = classes * K::TILES * kt.rpc;
   int rc;
   if (ch.fp64_ok) {
     if (!inverse) {
