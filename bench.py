@@ -250,6 +250,54 @@ def e2e_step(w, batch: int, host_in, host_out):
         host_out[b].copy_(r.data.view(), non_blocking=True)
 
 
+def pdq_latency(reps: int = 3):
+    """Config 5: the four standard queries over 1024 rows (pdq profile,
+    N=4096, 13 x 45-bit), keyed like the reference PdqClient.  Returns the
+    median end-to-end engine latency per query in ms (host encode of the
+    query constants and the in-process inverse exchange included)."""
+    import torch
+
+    from paper_2503_22227_b200.context import Context, PoolConfig, Scheme, params_for_profile
+    from paper_2503_22227_b200.coremath.sampling import Rng
+    from paper_2503_22227_b200.keys import galois_keygen, keygen, pk_gen, relin_keygen
+    from paper_2503_22227_b200.pdq.columns import encode_column
+    from paper_2503_22227_b200.pdq.config import PdqConfig
+    from paper_2503_22227_b200.pdq.dataset import make_dataset, oracle_result
+    from paper_2503_22227_b200.pdq.engine import (LocalInverseClient, PdqEngine,
+                                                  interpret_result, standard_query)
+    from paper_2503_22227_b200.pdq.evaluator import CkksEval, rotation_steps
+
+    cfg = PdqConfig()
+    ctx = Context(params_for_profile("pdq", Scheme.CKKS), PoolConfig(unit_mb=64, cap_mb=2048))
+    rng = Rng((1).to_bytes(32, "little"))
+    sk = keygen(ctx, rng)
+    pk = pk_gen(ctx, sk, rng)
+    ev = CkksEval(ctx, relin_keygen(ctx, sk, rng),
+                  galois_keygen(ctx, sk, rotation_steps(ctx.n), rng))
+    data = make_dataset(cfg)
+    engine = PdqEngine(ev, cfg)
+    for name, vals in data.items():
+        engine.add_column(encode_column(ev, cfg, name, vals, pk, rng))
+    inv = LocalInverseClient(ev, cfg, sk, pk, rng=rng)
+    mask_rng = np.random.default_rng(20240118)
+    out = {}
+    for qid in (1, 2, 3, 4):
+        spec = standard_query(qid)
+        times = []
+        for _ in range(reps):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            res = engine.run(spec, channel=inv, rng=mask_rng)
+            torch.cuda.synchronize()
+            times.append((time.perf_counter() - t0) * 1e3)
+        got = interpret_result(ev, sk, res, cfg.rows)
+        want = oracle_result(spec, data)
+        if spec.agg == "index" and not (np.asarray(got) == want).all():
+            raise AssertionError("PDQ-1 mask differs from the plaintext oracle")
+        out[f"q{qid}_ms"] = statistics.median(times)
+    return out
+
+
 def cpu_baseline_hmult(seconds_budget: float = 20.0):
     """The oracle port of the reference algorithm (per-prime gadget key switch,
     keys.py:186-237, alpha=1, K=0) at N=2^16, L=30 on all host threads."""
@@ -307,6 +355,7 @@ def main():
     ap.add_argument("--batch", type=int, default=8)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-pdq", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
@@ -344,9 +393,17 @@ def main():
     # roofline: batched NTT (dominant kernel family of the key-switch step)
     ntt_ms, algo, rows = ntt_roofline(max(3, args.steps // 4), 3)
     fwd_gbs = algo / (ntt_ms["forward"] / 1000.0) / 1e9
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "r1_ntt_traffic.json")) as f:
+            tr = json.load(f)
+        traffic = (tr["cols_kernel_dram_bytes"] + tr["chunks_kernel_dram_bytes"]) * rows / tr["rows"]
+    except Exception:
+        pass
     inv_gbs = algo / (ntt_ms["inverse"] / 1000.0) / 1e9
     decrypt_err = w["err"]
     del w
+    pdq = pdq_latency() if not args.no_pdq else None
     line = {
         "metric": METRIC, "value": ops, "unit": "ops/s", "n_gpus": world, "steps": args.steps,
         "warmup": max(args.warmup, 3), "ms_per_step": ms, "higher_is_better": True,
@@ -361,13 +418,15 @@ def main():
         "roofline": {"bound": "hbm", "kernel": "batched NTT forward (cols+chunks passes), "
                      f"N=2^16, {rows} rows", "achieved": fwd_gbs, "peak": peak,
                      "peak_kind": peak_kind, "unit": "GB/s", "frac": fwd_gbs / peak,
-                     "traffic": None, "inverse_achieved": inv_gbs,
+                     "traffic": traffic, "traffic_source": "profiles/r1_ntt_traffic.json (ncu, "
+                     "scaled per row)", "inverse_achieved": inv_gbs,
                      "algorithmic_bytes_per_launch": algo},
         "ntt": {"forward_ms": ntt_ms["forward"], "inverse_ms": ntt_ms["inverse"],
                 "forward_gbs": fwd_gbs, "inverse_gbs": inv_gbs, "rows": rows, "N": n},
         "gpu_launches": launches_per_step(LEVELS) * args.steps,
         "clocks": clk.summary(),
         "decrypt_err_hmult_relin_rescale": decrypt_err,
+        "pdq_1024_rows": pdq,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline_hmult()
