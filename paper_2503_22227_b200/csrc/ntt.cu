@@ -45,6 +45,9 @@ constexpr int kCols = 16;    // columns per column tile (one 128-byte segment)
 #ifndef FHE_NTT_MINB
 #define FHE_NTT_MINB 2
 #endif
+#ifndef FHE_NTT_FP_MINB
+#define FHE_NTT_FP_MINB 2
+#endif
 constexpr int npass(int log_s) { return (log_s + FHE_NTT_MAXE - 1) / FHE_NTT_MAXE; }
 constexpr int pass_e(int log_s, int p) {
   return log_s / npass(log_s) + (p < log_s % npass(log_s) ? 1 : 0);
@@ -456,7 +459,9 @@ __device__ __forceinline__ void run_pass_fp(u64* sm, const Tile& tl, u64* gout,
 #pragma unroll
           for (int i = 0; i < half; ++i) {
             const int a = blk * 2 * half + i, c = a + half;
-            const double u = fp_reduce(x[a], qd);
+            // reduce u on odd local stages only: |values| stay <= 2q (< 2^51,
+            // the magic-rounding bound) and every odd stage returns them to <= q
+            const double u = ((R0 + rr) & 1) ? fp_reduce(x[a], qd) : x[a];
             const double t = fp_mulmod(x[c], w, qd.x);
             x[a] = __dadd_rn(u, t);
             x[c] = __dadd_rn(u, -t);
@@ -602,7 +607,7 @@ __global__ void __launch_bounds__(kThreads, FHE_NTT_MINB)
 
 // FP64-pipe variant of the persistent tile kernel.
 template <class Tile, bool FWD, int IN, int OUT>
-__global__ void __launch_bounds__(kThreads, FHE_NTT_MINB)
+__global__ void __launch_bounds__(kThreads, FHE_NTT_FP_MINB)
     ntt_tiles_fp_kernel(const DevChain ch, u64* dst, const u64* src, Tile tl, int ntiles) {
   extern __shared__ __align__(16) u64 smem_raw[];
   u64* smem[2] = {smem_raw, smem_raw + kTileSmem};
@@ -669,7 +674,7 @@ template <class Tile, bool FWD, int IN, int OUT>
 int launch_tiles_fp(const DevChain& ch, u64* dst, const u64* src, const Tile& tl, int ntiles,
                     cudaStream_t st) {
   if (ntiles <= 0) return 0;
-  const int grid = std::min(ntiles, FHE_NTT_MINB * sm_count());
+  const int grid = std::min(ntiles, FHE_NTT_FP_MINB * sm_count());
   constexpr int smem = 2 * kTileSmem * sizeof(u64);
   static bool attr = false;
   if (!attr) {
