@@ -416,6 +416,86 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
+// FP64-pipe key inner product (every chain prime < 2^50, at most 4 digits):
+// the key words are variable operands, so their quotient estimates key/p
+// are formed on the fly (one DMUL); each term is an exact fp_mulmod, the
+// digit sum (|.| <= 4 * 0.75 p) is reduced once.
+__global__ void __launch_bounds__(kThreads)
+    ks_inner_fp_kernel(const DevChain ch, const u64* __restrict__ d, long d_stride,
+                       const u64* __restrict__ ext, long ext_stride, const u64* __restrict__ key,
+                       int keyL, const int* __restrict__ dig_info, int D, int level, int K, int L,
+                       u64* __restrict__ accQ, u64* __restrict__ accP, const u64* add0,
+                       const u64* add1, long add_stride, u64* out0, u64* out1, long out_stride,
+                       int batch) {
+  constexpr int kD = 4;
+  extern __shared__ int sinfo[];
+  for (int i = threadIdx.x; i < 4 * D; i += blockDim.x) sinfo[i] = dig_info[i];
+  __syncthreads();
+  const int log_n = ch.log_n;
+  const long n = 1L << log_n;
+  const long total = (long)(level + K) << log_n;
+  for (long t = blockIdx.x * (long)blockDim.x + threadIdx.x; t < total;
+       t += (long)gridDim.x * blockDim.x) {
+    const int m = (int)(t >> log_n);
+    const long i = t & (n - 1);
+    const int p = m < level ? m : L + (m - level);
+    const double2 qd = ch.qd[p];
+    const u64 q = ch.mc[p].q;
+    double2 kb[kD], ka[kD];
+    const u64* src[kD];
+    long sstr[kD];
+#pragma unroll
+    for (int di = 0; di < kD; ++di) {
+      if (di < D) {
+        const double b = (double)__ldg(key + ((long)(2 * di) * keyL + p) * n + i);
+        const double a = (double)__ldg(key + ((long)(2 * di + 1) * keyL + p) * n + i);
+        kb[di] = make_double2(b, __dmul_rn(b, qd.y));
+        ka[di] = make_double2(a, __dmul_rn(a, qd.y));
+        const int s0 = sinfo[4 * di], na = sinfo[4 * di + 1], ro = sinfo[4 * di + 2];
+        const bool own = m >= s0 && m < s0 + na;
+        src[di] = own ? d + (long)m * n + i : ext + (long)(ro + (m < s0 ? m : m - na)) * n + i;
+        sstr[di] = own ? d_stride : ext_stride;
+      }
+    }
+    for (int b0 = 0; b0 < batch; b0 += 4) {
+      u64 v[4][kD];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int di = 0; di < kD; ++di)
+          if (di < D && b0 + u < batch) v[u][di] = __ldg(src[di] + (b0 + u) * sstr[di]);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (b0 + u >= batch) break;
+        const int b = b0 + u;
+        double sb = 0.0, sa = 0.0;
+#pragma unroll
+        for (int di = 0; di < kD; ++di) {
+          if (di < D) {
+            const double x = (double)v[u][di];
+            sb = __dadd_rn(sb, fp_mulmod(x, kb[di], qd.x));
+            sa = __dadd_rn(sa, fp_mulmod(x, ka[di], qd.x));
+          }
+        }
+        const u64 rb = fp_canon_half(fp_reduce(sb, qd), qd.x);
+        const u64 ra = fp_canon_half(fp_reduce(sa, qd), qd.x);
+        if (K == 0) {
+          const long o = b * out_stride + (long)m * n + i;
+          const long ai = b * add_stride + (long)m * n + i;
+          out0[o] = add0 ? add_mod(add0[ai], rb, q) : rb;
+          out1[o] = add1 ? add_mod(add1[ai], ra, q) : ra;
+        } else if (m < level) {
+          accQ[((long)(b * 2 + 0) * level + m) * n + i] = rb;
+          accQ[((long)(b * 2 + 1) * level + m) * n + i] = ra;
+        } else {
+          accP[((long)(b * 2 + 0) * K + (m - level)) * n + i] = rb;
+          accP[((long)(b * 2 + 1) * K + (m - level)) * n + i] = ra;
+        }
+      }
+    }
+  }
+}
+
 int mac_chunk(const std::vector<u64>& primes) {
   u64 mx = 0;
   for (u64 p : primes) mx = p > mx ? p : mx;
@@ -498,9 +578,14 @@ int run_keyswitch(const FheContext& ctx, int level, const u64* d, long d_stride,
   // 3. inner product with the key digits (K == 0 writes the result directly)
   {
     const long work = (long)(level + K) << log_n;
-    ks_inner_kernel<<<grid_for(work), kThreads, 4 * lp.digits * sizeof(int), st>>>(
-        ch, d, d_stride, ext, (long)lp.ext_rows * n, key, L + K, lp.dig_info, lp.digits, level,
-        K, L, accQ, accP, add0, add1, add_stride, out0, out1, out_stride, batch, chunk);
+    if (ch.fp64_ok && lp.digits <= 4)
+      ks_inner_fp_kernel<<<grid_for(work), kThreads, 4 * lp.digits * sizeof(int), st>>>(
+          ch, d, d_stride, ext, (long)lp.ext_rows * n, key, L + K, lp.dig_info, lp.digits, level,
+          K, L, accQ, accP, add0, add1, add_stride, out0, out1, out_stride, batch);
+    else
+      ks_inner_kernel<<<grid_for(work), kThreads, 4 * lp.digits * sizeof(int), st>>>(
+          ch, d, d_stride, ext, (long)lp.ext_rows * n, key, L + K, lp.dig_info, lp.digits, level,
+          K, L, accQ, accP, add0, add1, add_stride, out0, out1, out_stride, batch, chunk);
     FHE_LAUNCH_CHECK();
   }
   if (K == 0) return 0;
