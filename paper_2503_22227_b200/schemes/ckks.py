@@ -268,8 +268,46 @@ def ckks_multiply_plain(ctx: Context, a: CkksCiphertext, pt: CkksPlaintext) -> C
     return CkksCiphertext(out, a.scale * pt.scale, a.level)
 
 
+class PlaintextCache:
+    """Small LRU of encoded constant plaintexts (identical bits, no re-encode).
+
+    Query circuits encode the same constants (1.0 boosts, EQ/LT coefficients,
+    validity masks) hundreds of times; each host encode is an FFT, a residue
+    lift, an upload and an NTT.  Plaintexts are never mutated by the ops."""
+
+    def __init__(self, capacity: int = 512):
+        from collections import OrderedDict
+
+        self.capacity = capacity
+        self._d = OrderedDict()
+
+    def get(self, key, make):
+        hit = self._d.get(key)
+        if hit is not None:
+            self._d.move_to_end(key)
+            return hit
+        val = make()
+        self._d[key] = val
+        if len(self._d) > self.capacity:
+            self._d.popitem(last=False)
+        return val
+
+
+def plaintext_cache(ctx: Context) -> PlaintextCache:
+    c = getattr(ctx, "_pt_cache", None)
+    if c is None:
+        c = PlaintextCache()
+        ctx._pt_cache = c
+    return c
+
+
 def scalar_plaintext(ctx: Context, z: complex, scale: float, level: int) -> CkksPlaintext:
-    """The two-term plaintext Re(z) + Im(z) X^(n/2) of ckks.py:290-305."""
+    """The two-term plaintext Re(z) + Im(z) X^(n/2) of ckks.py:290-305 (cached)."""
+    return plaintext_cache(ctx).get(("scalar", complex(z), float(scale), level),
+                                    lambda: _scalar_plaintext(ctx, z, scale, level))
+
+
+def _scalar_plaintext(ctx: Context, z: complex, scale: float, level: int) -> CkksPlaintext:
     n = ctx.n
     coeffs = np.zeros(n)
     coeffs[0] = z.real * scale
