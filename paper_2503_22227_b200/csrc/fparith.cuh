@@ -39,6 +39,18 @@ __device__ __forceinline__ u64 fp_canon(double x, double q) {
 
 // representative in [-q/2 - eps, q/2 + eps] (fp_reduce / fp_mulmod output)
 // -> canonical u64 in [0, q)
+__device__ __forceinline__ u64 fp_canon_half(double x, double q);
+
+// exact u64 -> double for x < 2^52 (one LOP + one DADD instead of I2F.F64)
+__device__ __forceinline__ double fp_from_u52(u64 x) {
+  return __dadd_rn(__longlong_as_double((long long)(x | 0x4330000000000000ull)),
+                   -4503599627370496.0);
+}
+// exact double -> u64 for an integer-valued x in [0, 2^52) (DADD + LOP, no F2I)
+__device__ __forceinline__ u64 fp_to_u52(double x) {
+  return (u64)__double_as_longlong(__dadd_rn(x, 4503599627370496.0)) & 0x000FFFFFFFFFFFFFull;
+}
+
 __device__ __forceinline__ u64 fp_canon_half(double x, double q) {
-  return (u64)__double2ll_rn(x < 0.0 ? __dadd_rn(x, q) : x);
+  return fp_to_u52(x < 0.0 ? __dadd_rn(x, q) : x);
 }

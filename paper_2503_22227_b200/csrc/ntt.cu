@@ -35,7 +35,8 @@
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kTile = 4096;  // elements per tile (32 KB)
+constexpr int kLogTile = 12;
+constexpr int kTile = 1 << kLogTile;  // elements per tile (32 KB)
 constexpr int kCols = 16;    // columns per column tile (one 128-byte segment)
 
 
@@ -89,6 +90,21 @@ struct RowAddr {
   }
 };
 
+// n / d for 0 <= n < 2^31 without a hardware divide (Granlund-Montgomery):
+// n / d = (umulhi(n, m) + n) >> s.  Built on the host.
+struct FastDiv {
+  u32 d = 1, m = 1, s = 0;
+  void init(u32 d_) {
+    d = d_;
+    s = 0;
+    while ((1u << s) < d) ++s;
+    m = (u32)((((1ull << 32) * ((1ull << s) - d)) / d) + 1);
+  }
+  __device__ __forceinline__ int div(int n) const {
+    return (int)((__umulhi((u32)n, m) + (u32)n) >> s);
+  }
+};
+
 // ---------------------------------------------------------------------------
 // Tile policies.  A tile holds arrays() local arrays of S = 2^LOG_S elements.
 // tile_index(b, k) is an element's slot in the tile before swizzling;
@@ -130,6 +146,12 @@ struct RowsTile {
     return ArrCtx{(fwd ? ch.tw : ch.itw) + ((size_t)p << LOG_N), ch.mc[p].q, 1, p, !fwd};
   }
   __device__ __forceinline__ int arrays() const { return nb; }
+  // rows of a tile may use different primes: twiddles are read through L1
+  static constexpr int TWMAX = 0;
+  __device__ __forceinline__ int tw_blocks() const { return 0; }
+  __device__ __forceinline__ void tw_block(int, int& n, int& o, long& g) const { n = o = 0; g = 0; }
+  __device__ __forceinline__ int tw_off(int) const { return 0; }
+  __device__ __forceinline__ int tw_prime() const { return 0; }
 };
 
 // First log N1 stages on a [N1][16] column tile of one row.
@@ -147,13 +169,27 @@ struct ColsTile {
   int row, j0, p;
   bool valid = true;
   long so, dof;  // word offsets of the tile's first element in src / dst
+  FastDiv limbs_div;  // row -> (row / limbs, row % limbs) without IMAD-heavy division
   __device__ __forceinline__ void setup(int t) {
     row = t / TILES;
     j0 = (t % TILES) * kCols;
-    p = map(row);
-    so = src(row) + j0;
-    dof = dst(row) + j0;
+    const int rq = limbs_div.div(row);
+    const int cls = row - rq * map.limbs;
+    p = (map.idx ? map.idx[cls] : cls) + map.offset;
+    so = (src.bstride ? rq * src.bstride + ((long)cls << LOG_N) : ((long)row << LOG_N)) + j0;
+    dof = (dst.bstride ? rq * dst.bstride + ((long)cls << LOG_N) : ((long)row << LOG_N)) + j0;
   }
+  // twiddles staged in shared memory per tile: psi_br[0 .. N1) of the row's
+  // prime (every column stage indexes below N1)
+  static constexpr int TWMAX = 1 << LOG_N1;
+  __device__ __forceinline__ int tw_blocks() const { return 1; }
+  __device__ __forceinline__ void tw_block(int, int& n, int& smem_off, long& gofs) const {
+    n = 1 << LOG_N1;
+    smem_off = 0;
+    gofs = 0;
+  }
+  __device__ __forceinline__ int tw_off(int) const { return 0; }
+  __device__ __forceinline__ int tw_prime() const { return p; }
   __device__ __forceinline__ int tile_index(int b, int k) const { return k * kCols + b; }
   __device__ __forceinline__ void split(int G, int, int& b, int& g) const {
     b = G % kCols;
@@ -171,7 +207,11 @@ struct ColsTile {
   __device__ __forceinline__ int arrays() const { return kCols; }
 };
 
-// Remaining stages on NB contiguous N2-chunks of one row.
+// Remaining stages on contiguous N2-chunks: a tile holds R rows of one
+// residue class (rows r0 + i * limbs share a prime) x C consecutive chunks,
+// R * C = NB.  Array b = (i, c) with i = b >> log_c, c = b & (C - 1).  The
+// R rows of a tile share every twiddle (the chunk stages' twiddles depend only
+// on the chunk index), so one L1 line serves R arrays.
 template <int LOG_N, int LOG_N1>
 struct ChunksTile {
   static constexpr int LOG_S = LOG_N - LOG_N1;
@@ -180,45 +220,88 @@ struct ChunksTile {
   static constexpr bool COLS = false;
   static constexpr long GSTEP_PER_K = 1;
   static constexpr int N1 = 1 << LOG_N1;
-  static constexpr int TILES = N1 / NB;
   int rows;
   RowMap map;
   RowAddr src, dst;
   bool fwd;
-  int row, c0, p;
-  int rpc = 1;  // rows per residue class (rows sharing a prime: r0 + k * map.limbs)
+  int log_r = 0;    // rows per tile = 1 << log_r (<= NB)
+  int rblocks = 1;  // row blocks per residue class
+  int cblocks = 1;  // chunk blocks per row = N1 / C
   bool valid = true;
-  long so, dof;  // word offsets of the tile's first element in src / dst
-  // Tile order: (residue class r0, chunk block, k).  Consecutive tiles of a
-  // CTA share the prime and the chunk range, so their twiddles (distinct per
-  // chunk in these stages) stay in L1 across the rows of the batch.
+  int log_c, c0, p, nb;
+  long so, dof, sstep, dstep;  // word offsets of array (0, 0) and the per-row steps
+  // Tile order: (residue class, row block, chunk block): consecutive tiles of
+  // a CTA share the prime and walk the chunks of the same rows.
+  int log_cb = 0;       // log2(cblocks)
+  int rows_q = 0, rows_r = 0;  // rows / limbs, rows % limbs
+  FastDiv rb_div;       // division by rblocks
   __device__ __forceinline__ void setup(int t) {
-    const int k = t % rpc;
-    const int u = t / rpc;
-    row = (u / TILES) + k * map.limbs;
-    c0 = (u % TILES) * NB;
-    valid = row < rows;
+    const int cb = t & (cblocks - 1);
+    const int u = t >> log_cb;
+    const int cls = rb_div.div(u);
+    const int rb = u - cls * rblocks;
+    log_c = kLogTile - LOG_S - log_r;
+    c0 = cb << log_c;
+    const int i0 = rb << log_r;
+    const int row0 = cls + i0 * map.limbs;
+    valid = row0 < rows;
     if (!valid) return;
-    p = map(row);
-    so = src(row) + (long)c0 * S;
-    dof = dst(row) + (long)c0 * S;
+    const int in_class = rows_q + (cls < rows_r ? 1 : 0);
+    nb = min(1 << log_r, in_class - i0) << log_c;
+    p = (map.idx ? map.idx[cls] : cls) + map.offset;
+    so = (src.bstride ? i0 * src.bstride + ((long)cls << LOG_N) : ((long)row0 << LOG_N)) +
+         ((long)c0 << LOG_S);
+    dof = (dst.bstride ? i0 * dst.bstride + ((long)cls << LOG_N) : ((long)row0 << LOG_N)) +
+          ((long)c0 << LOG_S);
+    sstep = src.bstride ? src.bstride : ((long)map.limbs << LOG_N);
+    dstep = dst.bstride ? dst.bstride : ((long)map.limbs << LOG_N);
   }
+  // twiddles staged in shared memory per tile (tiles of <= 2 chunks): local
+  // stage s of chunk c reads psi_br[((N1 + c) << s) + j], so the C chunks of a
+  // tile need, per stage, the contiguous run of C << s pairs from
+  // (N1 + c0) << s, stored at C * (2^s - 1).
+  static constexpr int TWMAX = 2 * ((1 << LOG_S) - 1);
+  __device__ __forceinline__ int tw_blocks() const { return LOG_S; }
+  __device__ __forceinline__ void tw_block(int s, int& n, int& smem_off, long& gofs) const {
+    n = 1 << (s + log_c);
+    smem_off = ((1 << s) - 1) << log_c;
+    gofs = (long)(N1 + c0) << s;
+  }
+  __device__ __forceinline__ int tw_off(int s) const {
+    return (((1 << s) - 1) << log_c) - ((N1 + c0) << s);
+  }
+  __device__ __forceinline__ int tw_prime() const { return p; }
   __device__ __forceinline__ int tile_index(int b, int k) const { return (b << LOG_S) + k; }
   __device__ __forceinline__ void split(int G, int gpa_log, int& b, int& g) const {
     b = G >> gpa_log;
     g = G & ((1 << gpa_log) - 1);
   }
   __device__ __forceinline__ const u64* gsrc(const u64* base, int b, int k) const {
-    return base + so + (b << LOG_S) + k;
+    return base + so + (b >> log_c) * sstep + ((b & ((1 << log_c) - 1)) << LOG_S) + k;
   }
   __device__ __forceinline__ u64* gdst(u64* base, int b, int k) const {
-    return base + dof + (b << LOG_S) + k;
+    return base + dof + (b >> log_c) * dstep + ((b & ((1 << log_c) - 1)) << LOG_S) + k;
   }
   __device__ __forceinline__ ArrCtx ctx(int b, const DevChain& ch) const {
-    return ArrCtx{(fwd ? ch.tw : ch.itw) + ((size_t)p << LOG_N), ch.mc[p].q, N1 + c0 + b, p,
-                  false};
+    return ArrCtx{(fwd ? ch.tw : ch.itw) + ((size_t)p << LOG_N), ch.mc[p].q,
+                  N1 + c0 + (b & ((1 << log_c) - 1)), p, false};
   }
-  __device__ __forceinline__ int arrays() const { return NB; }
+  __device__ __forceinline__ int arrays() const { return nb; }
+  // host: tiles for `rows` rows with residue classes of `limbs`
+  int plan(int rows_, int limbs) {
+    const int rpc = (rows_ + limbs - 1) / limbs;
+    log_r = 0;
+    while ((2 << log_r) <= NB && (2 << log_r) <= rpc) ++log_r;
+    rblocks = (rpc + (1 << log_r) - 1) >> log_r;
+    const int C = NB >> log_r;
+    cblocks = N1 / C;
+    log_cb = 0;
+    while ((1 << log_cb) < cblocks) ++log_cb;
+    rb_div.init(rblocks);
+    rows_q = rows_ / limbs;
+    rows_r = rows_ % limbs;
+    return std::min(limbs, rows_) * rblocks * cblocks;
+  }
 };
 
 // Output handling of the final pass of a kernel.
@@ -407,9 +490,9 @@ enum FpIn { FPIN_DOUBLE = 0, FPIN_U64 = 1 };
 enum FpOut { FPOUT_DOUBLE = 0, FPOUT_U64 = 1 };
 
 template <int LOG_S, int R0, int E_LOG, bool FWD, bool FIRST, bool LAST, int IN, int OUT,
-          class Tile>
-__device__ __forceinline__ void run_pass_fp(u64* sm, const Tile& tl, u64* gout,
-                                            const DevChain& ch) {
+          bool STW, class Tile>
+__device__ __forceinline__ void run_pass_fp(u64* sm, const double2* tws, const Tile& tl,
+                                            u64* gout, const DevChain& ch) {
   constexpr int E = 1 << E_LOG;
   constexpr int T0 = (1 << LOG_S) >> (R0 + 1);
   constexpr int TMIN_LOG = LOG_S - R0 - E_LOG;
@@ -418,6 +501,9 @@ __device__ __forceinline__ void run_pass_fp(u64* sm, const Tile& tl, u64* gout,
   constexpr bool VEC = (TMIN_LOG == 0) && !Tile::COLS && E >= 2;
   constexpr int PSTEP = Tile::COLS ? 18 * TMIN
                                    : (TMIN_LOG == 0 ? 1 : (TMIN_LOG >= 4 ? TMIN + TMIN / 8 : 0));
+  // twiddles of the whole pass are loaded up front (E - 1 pairs) when they
+  // fit the register budget, so their L1/L2 latency overlaps the tile reads
+  constexpr bool PRELOAD = !STW && E <= 16;
   const int total = tl.arrays() << GPA_LOG;
   for (int G = threadIdx.x; G < total; G += blockDim.x) {
     int b, g;
@@ -427,8 +513,17 @@ __device__ __forceinline__ void run_pass_fp(u64* sm, const Tile& tl, u64* gout,
     const int base = hi * 2 * T0 + lo;
     const int pb = padix(tl.tile_index(b, base));
     const ArrCtx cx = tl.ctx(b, ch);
-    const double2 qd = ch.qd[cx.prime];
+    const double2 qd = __ldg(&ch.qd[cx.prime]);
     const double2* tw = (FWD ? ch.twd : ch.itwd) + ((size_t)cx.prime << ch.log_n);
+    double2 wt[PRELOAD ? E - 1 : 1];
+    if (PRELOAD) {
+#pragma unroll
+      for (int rr = 0; rr < E_LOG; ++rr) {
+        const double2* twr = tw + (cx.m0 << (R0 + rr)) + (hi << rr);
+#pragma unroll
+        for (int blk = 0; blk < (1 << rr); ++blk) wt[(1 << rr) - 1 + blk] = __ldg(twr + blk);
+      }
+    }
     u64 raw[E];
     if (VEC) {
 #pragma unroll
@@ -447,15 +542,16 @@ __device__ __forceinline__ void run_pass_fp(u64* sm, const Tile& tl, u64* gout,
     double x[E];
 #pragma unroll
     for (int i = 0; i < E; ++i)
-      x[i] = (FIRST && IN == FPIN_U64) ? (double)raw[i] : __longlong_as_double((long long)raw[i]);
+      x[i] = (FIRST && IN == FPIN_U64) ? fp_from_u52(raw[i]) : __longlong_as_double((long long)raw[i]);
     if (FWD) {
 #pragma unroll
       for (int rr = 0; rr < E_LOG; ++rr) {
         const int half = E >> (rr + 1);
-        const double2* twr = tw + (cx.m0 << (R0 + rr)) + (hi << rr);
+        const double2* twr = STW ? tws + tl.tw_off(R0 + rr) + (cx.m0 << (R0 + rr)) + (hi << rr)
+                                 : tw + (cx.m0 << (R0 + rr)) + (hi << rr);
 #pragma unroll
         for (int blk = 0; blk < (1 << rr); ++blk) {
-          const double2 w = __ldg(twr + blk);
+          const double2 w = PRELOAD ? wt[(1 << rr) - 1 + blk] : (STW ? twr[blk] : __ldg(twr + blk));
 #pragma unroll
           for (int i = 0; i < half; ++i) {
             const int a = blk * 2 * half + i, c = a + half;
@@ -473,11 +569,14 @@ __device__ __forceinline__ void run_pass_fp(u64* sm, const Tile& tl, u64* gout,
       for (int rr = E_LOG - 1; rr >= 0; --rr) {
         const int half = E >> (rr + 1);
         const bool fold = (R0 == 0) && (rr == 0) && cx.fold;
-        const double2* twr = tw + (cx.m0 << (R0 + rr)) + (hi << rr);
+        const double2* twr = STW ? tws + tl.tw_off(R0 + rr) + (cx.m0 << (R0 + rr)) + (hi << rr)
+                                 : tw + (cx.m0 << (R0 + rr)) + (hi << rr);
 #pragma unroll
         for (int blk = 0; blk < (1 << rr); ++blk) {
-          const double2 w = fold ? ch.ninv_w1_d[cx.prime] : __ldg(twr + blk);
-          const double2 sn = fold ? ch.ninv_d[cx.prime] : w;
+          const double2 w = fold ? __ldg(&ch.ninv_w1_d[cx.prime])
+                                 : (PRELOAD ? wt[(1 << rr) - 1 + blk]
+                                            : (STW ? twr[blk] : __ldg(twr + blk)));
+          const double2 sn = fold ? __ldg(&ch.ninv_d[cx.prime]) : w;
 #pragma unroll
           for (int i = 0; i < half; ++i) {
             const int a = blk * 2 * half + i, c = a + half;
@@ -520,32 +619,44 @@ __device__ __forceinline__ void run_pass_fp(u64* sm, const Tile& tl, u64* gout,
   }
 }
 
-template <int LOG_S, int P, int IN, int OUT, class Tile>
-__device__ __forceinline__ void fwd_passes_fp(u64* sm, const Tile& tl, u64* gout,
-                                              const DevChain& ch) {
+template <int LOG_S, int P, int IN, int OUT, bool STW, class Tile>
+__device__ __forceinline__ void fwd_passes_fp(u64* sm, const double2* tws, const Tile& tl,
+                                              u64* gout, const DevChain& ch) {
   constexpr int NP = npass(LOG_S);
   if constexpr (P < NP) {
     constexpr bool last = (P == NP - 1);
-    run_pass_fp<LOG_S, pass_r0(LOG_S, P), pass_e(LOG_S, P), true, P == 0, last, IN, OUT>(
-        sm, tl, gout, ch);
+    run_pass_fp<LOG_S, pass_r0(LOG_S, P), pass_e(LOG_S, P), true, P == 0, last, IN, OUT, STW>(
+        sm, tws, tl, gout, ch);
     if constexpr (!last) {
       __syncthreads();
-      fwd_passes_fp<LOG_S, P + 1, IN, OUT>(sm, tl, gout, ch);
+      fwd_passes_fp<LOG_S, P + 1, IN, OUT, STW>(sm, tws, tl, gout, ch);
     }
   }
 }
 
-template <int LOG_S, int P, int IN, int OUT, class Tile>
-__device__ __forceinline__ void inv_passes_fp(u64* sm, const Tile& tl, u64* gout,
-                                              const DevChain& ch) {
+template <int LOG_S, int P, int IN, int OUT, bool STW, class Tile>
+__device__ __forceinline__ void inv_passes_fp(u64* sm, const double2* tws, const Tile& tl,
+                                              u64* gout, const DevChain& ch) {
   if constexpr (P >= 0) {
     constexpr bool last = (P == 0);
     run_pass_fp<LOG_S, pass_r0(LOG_S, P), pass_e(LOG_S, P), false, P == npass(LOG_S) - 1, last,
-                IN, OUT>(sm, tl, gout, ch);
+                IN, OUT, STW>(sm, tws, tl, gout, ch);
     if constexpr (!last) {
       __syncthreads();
-      inv_passes_fp<LOG_S, P - 1, IN, OUT>(sm, tl, gout, ch);
+      inv_passes_fp<LOG_S, P - 1, IN, OUT, STW>(sm, tws, tl, gout, ch);
     }
+  }
+}
+
+// Stage the tile's twiddle pairs in shared memory (cp.async, committed with
+// the tile's data group).
+template <class Tile>
+__device__ __forceinline__ void load_tw(double2* tws, const Tile& tl, const double2* table) {
+  for (int s = 0; s < tl.tw_blocks(); ++s) {
+    int n, off;
+    long g;
+    tl.tw_block(s, n, off, g);
+    for (int j = threadIdx.x; j < n; j += blockDim.x) cp_async16(&tws[off + j], &table[g + j]);
   }
 }
 
@@ -574,14 +685,13 @@ template <class Tile, bool FWD, bool LAZY, int OUT>
 __global__ void __launch_bounds__(kThreads, FHE_NTT_MINB)
     ntt_tiles_kernel(const DevChain ch, u64* dst, const u64* src, Tile tl, int ntiles) {
   extern __shared__ __align__(16) u64 smem_raw[];
-  u64* smem[2] = {smem_raw, smem_raw + kTileSmem};
   // contiguous tile range per CTA (keeps the tile order's twiddle locality)
   const int t_end = (int)(((long)(blockIdx.x + 1) * ntiles) / gridDim.x);
   int t = (int)(((long)blockIdx.x * ntiles) / gridDim.x);
   if (t >= t_end) return;
   Tile cur = tl;
   cur.setup(t);
-  if (cur.valid) load_tile(smem[0], cur, src);
+  if (cur.valid) load_tile(smem_raw, cur, src);
   else cp_async_commit();
   int buf = 0;
   for (; t < t_end; ++t) {
@@ -591,34 +701,42 @@ __global__ void __launch_bounds__(kThreads, FHE_NTT_MINB)
     if (tn < t_end) {
       Tile nxt = tl;
       nxt.setup(tn);
-      if (nxt.valid) load_tile(smem[buf ^ 1], nxt, src);
+      if (nxt.valid) load_tile(smem_raw + (buf ? 0 : kTileSmem), nxt, src);
       else cp_async_commit();
     }
     if (cur.valid) {
       if (FWD)
-        fwd_passes<Tile::LOG_S, 0, LAZY, OUT>(smem[buf], cur, dst, ch);
+        fwd_passes<Tile::LOG_S, 0, LAZY, OUT>(smem_raw + (buf ? kTileSmem : 0), cur, dst, ch);
       else
-        inv_passes<Tile::LOG_S, npass(Tile::LOG_S) - 1>(smem[buf], cur, dst, ch);
+        inv_passes<Tile::LOG_S, npass(Tile::LOG_S) - 1>(smem_raw + (buf ? kTileSmem : 0), cur, dst, ch);
     }
     if (tn < t_end) cur.setup(tn);
     buf ^= 1;
   }
 }
 
-// FP64-pipe variant of the persistent tile kernel.
-template <class Tile, bool FWD, int IN, int OUT>
+// FP64-pipe variant of the persistent tile kernel.  STW: the tile's twiddles
+// are staged in shared memory with its data (double-buffered), so every
+// butterfly reads its twiddle with an LDS instead of an L1/L2 round trip.
+template <class Tile, bool FWD, int IN, int OUT, bool STW>
 __global__ void __launch_bounds__(kThreads, FHE_NTT_FP_MINB)
     ntt_tiles_fp_kernel(const DevChain ch, u64* dst, const u64* src, Tile tl, int ntiles) {
   extern __shared__ __align__(16) u64 smem_raw[];
-  u64* smem[2] = {smem_raw, smem_raw + kTileSmem};
+  constexpr int TWM = STW ? Tile::TWMAX : 0;
+  double2* tw_raw = reinterpret_cast<double2*>(smem_raw + 2 * kTileSmem);
+  const double2* table = FWD ? ch.twd : ch.itwd;
   // contiguous tile range per CTA (keeps the tile order's twiddle locality)
   const int t_end = (int)(((long)(blockIdx.x + 1) * ntiles) / gridDim.x);
   int t = (int)(((long)blockIdx.x * ntiles) / gridDim.x);
   if (t >= t_end) return;
   Tile cur = tl;
   cur.setup(t);
-  if (cur.valid) load_tile(smem[0], cur, src);
-  else cp_async_commit();
+  if (cur.valid) {
+    if (STW) load_tw(tw_raw, cur, table + ((size_t)cur.tw_prime() << ch.log_n));
+    load_tile(smem_raw, cur, src);
+  } else {
+    cp_async_commit();
+  }
   int buf = 0;
   for (; t < t_end; ++t) {
     cp_async_wait_all();
@@ -627,14 +745,21 @@ __global__ void __launch_bounds__(kThreads, FHE_NTT_FP_MINB)
     if (tn < t_end) {
       Tile nxt = tl;
       nxt.setup(tn);
-      if (nxt.valid) load_tile(smem[buf ^ 1], nxt, src);
-      else cp_async_commit();
+      if (nxt.valid) {
+        if (STW)
+          load_tw(tw_raw + (buf ? 0 : TWM), nxt, table + ((size_t)nxt.tw_prime() << ch.log_n));
+        load_tile(smem_raw + (buf ? 0 : kTileSmem), nxt, src);
+      } else {
+        cp_async_commit();
+      }
     }
     if (cur.valid) {
+      u64* sm = smem_raw + (buf ? kTileSmem : 0);
+      const double2* tws = tw_raw + (buf ? TWM : 0);
       if (FWD)
-        fwd_passes_fp<Tile::LOG_S, 0, IN, OUT>(smem[buf], cur, dst, ch);
+        fwd_passes_fp<Tile::LOG_S, 0, IN, OUT, STW>(sm, tws, cur, dst, ch);
       else
-        inv_passes_fp<Tile::LOG_S, npass(Tile::LOG_S) - 1, IN, OUT>(smem[buf], cur, dst, ch);
+        inv_passes_fp<Tile::LOG_S, npass(Tile::LOG_S) - 1, IN, OUT, STW>(sm, tws, cur, dst, ch);
     }
     if (tn < t_end) cur.setup(tn);
     buf ^= 1;
@@ -670,19 +795,20 @@ int launch_tiles(const DevChain& ch, u64* dst, const u64* src, const Tile& tl, i
 }
 
 
-template <class Tile, bool FWD, int IN, int OUT>
+template <class Tile, bool FWD, int IN, int OUT, bool STW = false>
 int launch_tiles_fp(const DevChain& ch, u64* dst, const u64* src, const Tile& tl, int ntiles,
                     cudaStream_t st) {
   if (ntiles <= 0) return 0;
   const int grid = std::min(ntiles, FHE_NTT_FP_MINB * sm_count());
-  constexpr int smem = 2 * kTileSmem * sizeof(u64);
+  constexpr int smem = 2 * kTileSmem * sizeof(u64) + (STW ? 2 * Tile::TWMAX * sizeof(double2) : 0);
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(ntt_tiles_fp_kernel<Tile, FWD, IN, OUT>,
+    cudaFuncSetAttribute(ntt_tiles_fp_kernel<Tile, FWD, IN, OUT, STW>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     attr = true;
   }
-  ntt_tiles_fp_kernel<Tile, FWD, IN, OUT><<<grid, kThreads, smem, st>>>(ch, dst, src, tl, ntiles);
+  ntt_tiles_fp_kernel<Tile, FWD, IN, OUT, STW><<<grid, kThreads, smem, st>>>(ch, dst, src, tl,
+                                                                            ntiles);
   FHE_LAUNCH_CHECK();
   return 0;
 }
@@ -719,9 +845,10 @@ int launch_split(const DevChain& ch, const NttArgs& a, bool inverse, bool lazy,
   kt.map = a.map;
   kt.fwd = !inverse;
   const RowAddr s{a.src_bstride, a.map.limbs, LOG_N}, d{a.dst_bstride, a.map.limbs, LOG_N};
-  const int classes = std::min(a.map.limbs, a.rows);
-  kt.rpc = (a.rows + a.map.limbs - 1) / a.map.limbs;
-  const int nc = a.rows * C::TILES, nk = classes * K::TILES * kt.rpc;
+  const int nc = a.rows * C::TILES, nk = kt.plan(a.rows, a.map.limbs);
+  ct.limbs_div.init(a.map.limbs);
+  // chunk tiles of <= 2 chunks stage their twiddles in shared memory
+  const bool kstage = (K::NB >> kt.log_r) <= 2;
   int rc;
   if (ch.fp64_ok) {
     if (!inverse) {
@@ -729,15 +856,19 @@ int launch_split(const DevChain& ch, const NttArgs& a, bool inverse, bool lazy,
       ct.dst = d;
       kt.src = d;
       kt.dst = d;
-      rc = launch_tiles_fp<C, true, FPIN_U64, FPOUT_DOUBLE>(ch, a.dst, a.src, ct, nc, st);
-      if (!rc) rc = launch_tiles_fp<K, true, FPIN_DOUBLE, FPOUT_U64>(ch, a.dst, a.dst, kt, nk, st);
+      rc = launch_tiles_fp<C, true, FPIN_U64, FPOUT_DOUBLE, true>(ch, a.dst, a.src, ct, nc, st);
+      if (!rc)
+        rc = kstage ? launch_tiles_fp<K, true, FPIN_DOUBLE, FPOUT_U64, true>(ch, a.dst, a.dst, kt, nk, st)
+                    : launch_tiles_fp<K, true, FPIN_DOUBLE, FPOUT_U64>(ch, a.dst, a.dst, kt, nk, st);
     } else {
       kt.src = s;
       kt.dst = d;
       ct.src = d;
       ct.dst = d;
-      rc = launch_tiles_fp<K, false, FPIN_U64, FPOUT_DOUBLE>(ch, a.dst, a.src, kt, nk, st);
-      if (!rc) rc = launch_tiles_fp<C, false, FPIN_DOUBLE, FPOUT_U64>(ch, a.dst, a.dst, ct, nc, st);
+      rc = kstage ? launch_tiles_fp<K, false, FPIN_U64, FPOUT_DOUBLE, true>(ch, a.dst, a.src, kt, nk, st)
+                  : launch_tiles_fp<K, false, FPIN_U64, FPOUT_DOUBLE>(ch, a.dst, a.src, kt, nk, st);
+      if (!rc)
+        rc = launch_tiles_fp<C, false, FPIN_DOUBLE, FPOUT_U64, true>(ch, a.dst, a.dst, ct, nc, st);
     }
     return rc;
   }
