@@ -117,6 +117,7 @@ struct RowsTile {
   static constexpr int S = 1 << LOG_N;
   static constexpr int NB = S >= kTile ? 1 : (kTile / S > 32 ? 32 : kTile / S);
   static constexpr bool COLS = false;
+  static constexpr bool EPI = true;
   static constexpr long GSTEP_PER_K = 1;
   int rows;
   RowMap map;
@@ -152,6 +153,9 @@ struct RowsTile {
   __device__ __forceinline__ void tw_block(int, int& n, int& o, long& g) const { n = o = 0; g = 0; }
   __device__ __forceinline__ int tw_off(int) const { return 0; }
   __device__ __forceinline__ int tw_prime() const { return 0; }
+  static constexpr bool TW_T = false;
+  static constexpr int TW_P = 0;
+  __device__ __forceinline__ int tw_perm(int, int j) const { return j; }
 };
 
 // First log N1 stages on a [N1][16] column tile of one row.
@@ -159,6 +163,7 @@ template <int LOG_N, int LOG_N1>
 struct ColsTile {
   static constexpr int LOG_S = LOG_N1;
   static constexpr bool COLS = true;
+  static constexpr bool EPI = true;
   static constexpr int N2 = 1 << (LOG_N - LOG_N1);
   static constexpr long GSTEP_PER_K = N2;
   static constexpr int TILES = N2 / kCols;
@@ -190,10 +195,32 @@ struct ColsTile {
   }
   __device__ __forceinline__ int tw_off(int) const { return 0; }
   __device__ __forceinline__ int tw_prime() const { return p; }
+  // last-pass stages stored transposed, as in ChunksTile: pair 2^s + j with
+  // j = (g << rr) | blk goes to 2^s + ((blk << TW_P) | g)
+  static constexpr int TW_P = pass_r0(LOG_S, npass(LOG_S) - 1);
+  static constexpr bool TW_T = true;
+  __device__ __forceinline__ int tw_perm(int, int j) const {
+    if (j < (1 << TW_P)) return j;
+    const int s = 31 - __clz(j);
+    const int rr = s - TW_P;
+    const int jl = j - (1 << s);
+    return (1 << s) | ((jl & ((1 << rr) - 1)) << TW_P) | (jl >> rr);
+  }
   __device__ __forceinline__ int tile_index(int b, int k) const { return k * kCols + b; }
-  __device__ __forceinline__ void split(int G, int, int& b, int& g) const {
-    b = G % kCols;
-    g = G / kCols;
+  // array-major: the groups of one column sit on consecutive lanes, so a
+  // pass's exchange stays inside the warp when every pass has 2^g_log groups
+  // With 16 groups per column a warp owns two columns; each half-warp holds
+  // 8 groups of both columns so its 8-byte shared accesses (serviced per
+  // half-warp) hit 16 distinct bank pairs in both passes.
+  __device__ __forceinline__ void split(int G, int gpa_log, int& b, int& g) const {
+    if (gpa_log == 4) {
+      const int lane = G & 31;
+      b = ((G >> 5) << 1) + ((lane >> 3) & 1);
+      g = ((lane >> 4) << 3) | (lane & 7);
+    } else {
+      b = G >> gpa_log;
+      g = G & ((1 << gpa_log) - 1);
+    }
   }
   __device__ __forceinline__ const u64* gsrc(const u64* base, int b, int k) const {
     return base + so + k * N2 + b;
@@ -218,6 +245,7 @@ struct ChunksTile {
   static constexpr int S = 1 << LOG_S;
   static constexpr int NB = kTile / S;
   static constexpr bool COLS = false;
+  static constexpr bool EPI = true;
   static constexpr long GSTEP_PER_K = 1;
   static constexpr int N1 = 1 << LOG_N1;
   int rows;
@@ -271,6 +299,18 @@ struct ChunksTile {
     return (((1 << s) - 1) << log_c) - ((N1 + c0) << s);
   }
   __device__ __forceinline__ int tw_prime() const { return p; }
+  // Stages s >= TW_P (the last register pass, one group per thread) store a
+  // chunk's pairs transposed: j = (g << rr) | blk (rr = s - TW_P) goes to
+  // (blk << TW_P) | g, so the 16 groups of a warp read 16 consecutive pairs
+  // (conflict-free) instead of pairs 2^rr apart.
+  static constexpr int TW_P = pass_r0(LOG_S, npass(LOG_S) - 1);
+  static constexpr bool TW_T = true;
+  __device__ __forceinline__ int tw_perm(int s, int j) const {
+    if (s < TW_P) return j;
+    const int rr = s - TW_P;
+    const int jl = j & ((1 << s) - 1);
+    return (j - jl) | ((jl & ((1 << rr) - 1)) << TW_P) | (jl >> rr);
+  }
   __device__ __forceinline__ int tile_index(int b, int k) const { return (b << LOG_S) + k; }
   __device__ __forceinline__ void split(int G, int gpa_log, int& b, int& g) const {
     b = G >> gpa_log;
@@ -316,8 +356,67 @@ enum OutMode {
 // strided passes (8-byte accesses, lanes on consecutive words) are both
 // bank-conflict free, and the padded index stays affine in the element
 // counter, so every shared-memory access of a pass uses an immediate offset.
-__device__ __forceinline__ int padix(int t) { return t + ((t >> 4) << 1); }
-constexpr int kTileSmem = kTile + kTile / 8;  // padded words per buffer
+// Padded shared-memory index: 16 bytes of pad per 16-element (128-byte) row
+// and another 16 per 256 elements.  With array-major thread mapping (the
+// 2^g groups of one array on consecutive lanes) every pass is conflict-free:
+// stride-16 groups vary the row's low nibble (first term), contiguous groups
+// of the column tile vary the high nibble (second term).
+__device__ __forceinline__ int padix(int t) { return t + ((t >> 4) << 1) + ((t >> 8) << 1); }
+constexpr int kTileSmem = kTile + kTile / 8 + kTile / 128;  // padded words per buffer
+// padded distance between element i and i+1 of a thread's group (stride TMIN
+// in tile rows of 16 (COLS) or elements), 0 when it is not affine
+constexpr int pad_step(bool cols, int tmin, int e) {
+  return cols ? (tmin >= 16 ? 18 * tmin + 2 * (tmin / 16) : (tmin * e <= 16 ? 18 * tmin : 0))
+              : (tmin == 1 ? 1
+                           : (tmin >= 256 ? tmin + tmin / 8 + tmin / 128
+                                          : (tmin >= 16 && tmin * e <= 256 ? tmin + tmin / 8 : 0)));
+}
+
+// Every register pass of a LOG_S-stage local transform has the same radix and
+// at most 32 groups per array: with array-major thread mapping each array is
+// owned by one warp in every pass, so passes exchange data under __syncwarp.
+constexpr bool warp_local(int log_s) {
+  for (int p = 1; p < npass(log_s); ++p)
+    if (pass_e(log_s, p) != pass_e(log_s, 0)) return false;
+  return log_s - pass_e(log_s, 0) <= 5;
+}
+
+// Copy a finished tile from shared memory to global memory in 16-byte pairs.
+//  * column tiles: CTA-wide (a k-row of 16 columns = 128 contiguous bytes);
+//  * array tiles, warp-local passes: each warp stores the arrays it computed;
+//  * array tiles otherwise: CTA-wide over all arrays.
+template <class Tile, int GPA_LOG, bool WL>
+__device__ __forceinline__ void epilogue_store(const u64* sm, const Tile& tl, u64* gout) {
+  constexpr int S = 1 << Tile::LOG_S;
+  if constexpr (Tile::COLS) {
+    __syncthreads();
+    for (int q = threadIdx.x; q < S * kCols / 2; q += blockDim.x) {
+      const int k = q >> 3, c = (q & 7) << 1;
+      const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(&sm[padix(tl.tile_index(c, k))]);
+      *reinterpret_cast<ulonglong2*>(tl.gdst(gout, c, k)) = v;
+    }
+  } else if constexpr (WL) {
+    __syncwarp();
+    const int lane = threadIdx.x & 31;
+    const int total = tl.arrays() << GPA_LOG;
+    for (int G0 = threadIdx.x - lane; G0 < total; G0 += blockDim.x) {
+      const int b0 = G0 >> GPA_LOG;
+      const int b1 = min((G0 + 32) >> GPA_LOG, tl.arrays());
+      for (int q = lane; q < ((b1 - b0) * S) >> 1; q += 32) {
+        const int bb = b0 + q / (S >> 1), k = (q % (S >> 1)) << 1;
+        const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(&sm[padix(tl.tile_index(bb, k))]);
+        *reinterpret_cast<ulonglong2*>(tl.gdst(gout, bb, k)) = v;
+      }
+    }
+  } else {
+    __syncthreads();
+    for (int q = threadIdx.x; q < (tl.arrays() * S) >> 1; q += blockDim.x) {
+      const int bb = q / (S >> 1), k = (q % (S >> 1)) << 1;
+      const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(&sm[padix(tl.tile_index(bb, k))]);
+      *reinterpret_cast<ulonglong2*>(tl.gdst(gout, bb, k)) = v;
+    }
+  }
+}
 
 // One register pass covering local stages R0 .. R0+E_LOG-1.
 // LAST: values go straight to global memory instead of back to the tile.
@@ -331,8 +430,7 @@ __device__ __forceinline__ void run_pass(u64* sm, const Tile& tl, u64* gout,
   constexpr int GPA_LOG = LOG_S - E_LOG;
   constexpr bool VEC = (TMIN_LOG == 0) && !Tile::COLS && E >= 2;
   // padded stride between consecutive elements of the thread (0: not affine)
-  constexpr int PSTEP = Tile::COLS ? 18 * TMIN
-                                   : (TMIN_LOG == 0 ? 1 : (TMIN_LOG >= 4 ? TMIN + TMIN / 8 : 0));
+  constexpr int PSTEP = pad_step(Tile::COLS, TMIN, E);
   const int total = tl.arrays() << GPA_LOG;
   for (int G = threadIdx.x; G < total; G += blockDim.x) {
     int b, g;
@@ -499,11 +597,16 @@ __device__ __forceinline__ void run_pass_fp(u64* sm, const double2* tws, const T
   constexpr int TMIN = 1 << TMIN_LOG;
   constexpr int GPA_LOG = LOG_S - E_LOG;
   constexpr bool VEC = (TMIN_LOG == 0) && !Tile::COLS && E >= 2;
-  constexpr int PSTEP = Tile::COLS ? 18 * TMIN
-                                   : (TMIN_LOG == 0 ? 1 : (TMIN_LOG >= 4 ? TMIN + TMIN / 8 : 0));
+  constexpr int PSTEP = pad_step(Tile::COLS, TMIN, E);
   // twiddles of the whole pass are loaded up front (E - 1 pairs) when they
   // fit the register budget, so their L1/L2 latency overlaps the tile reads
   constexpr bool PRELOAD = !STW && E <= 16;
+  // results of the last pass go back to shared memory and leave in 16-byte
+  // coalesced stores (no strided 8-byte STGs from the butterfly registers)
+  constexpr bool EPI = Tile::EPI;
+  constexpr bool WL = warp_local(LOG_S);
+  // staged twiddles of this pass are stored transposed (Tile::tw_perm)
+  constexpr bool TT = STW && Tile::TW_T && R0 == Tile::TW_P && TMIN_LOG == 0;
   const int total = tl.arrays() << GPA_LOG;
   for (int G = threadIdx.x; G < total; G += blockDim.x) {
     int b, g;
@@ -547,11 +650,12 @@ __device__ __forceinline__ void run_pass_fp(u64* sm, const double2* tws, const T
 #pragma unroll
       for (int rr = 0; rr < E_LOG; ++rr) {
         const int half = E >> (rr + 1);
-        const double2* twr = STW ? tws + tl.tw_off(R0 + rr) + (cx.m0 << (R0 + rr)) + (hi << rr)
-                                 : tw + (cx.m0 << (R0 + rr)) + (hi << rr);
+        const double2* twr = TT ? tws + tl.tw_off(R0 + rr) + (cx.m0 << (R0 + rr)) + hi
+                             : STW ? tws + tl.tw_off(R0 + rr) + (cx.m0 << (R0 + rr)) + (hi << rr)
+                                   : tw + (cx.m0 << (R0 + rr)) + (hi << rr);
 #pragma unroll
         for (int blk = 0; blk < (1 << rr); ++blk) {
-          const double2 w = PRELOAD ? wt[(1 << rr) - 1 + blk] : (STW ? twr[blk] : __ldg(twr + blk));
+          const double2 w = PRELOAD ? wt[(1 << rr) - 1 + blk] : (STW ? twr[TT ? (blk << R0) : blk] : __ldg(twr + blk));
 #pragma unroll
           for (int i = 0; i < half; ++i) {
             const int a = blk * 2 * half + i, c = a + half;
@@ -569,13 +673,14 @@ __device__ __forceinline__ void run_pass_fp(u64* sm, const double2* tws, const T
       for (int rr = E_LOG - 1; rr >= 0; --rr) {
         const int half = E >> (rr + 1);
         const bool fold = (R0 == 0) && (rr == 0) && cx.fold;
-        const double2* twr = STW ? tws + tl.tw_off(R0 + rr) + (cx.m0 << (R0 + rr)) + (hi << rr)
-                                 : tw + (cx.m0 << (R0 + rr)) + (hi << rr);
+        const double2* twr = TT ? tws + tl.tw_off(R0 + rr) + (cx.m0 << (R0 + rr)) + hi
+                             : STW ? tws + tl.tw_off(R0 + rr) + (cx.m0 << (R0 + rr)) + (hi << rr)
+                                   : tw + (cx.m0 << (R0 + rr)) + (hi << rr);
 #pragma unroll
         for (int blk = 0; blk < (1 << rr); ++blk) {
           const double2 w = fold ? __ldg(&ch.ninv_w1_d[cx.prime])
                                  : (PRELOAD ? wt[(1 << rr) - 1 + blk]
-                                            : (STW ? twr[blk] : __ldg(twr + blk)));
+                                            : (STW ? twr[TT ? (blk << R0) : blk] : __ldg(twr + blk)));
           const double2 sn = fold ? __ldg(&ch.ninv_d[cx.prime]) : w;
 #pragma unroll
           for (int i = 0; i < half; ++i) {
@@ -592,7 +697,7 @@ __device__ __forceinline__ void run_pass_fp(u64* sm, const double2* tws, const T
     for (int i = 0; i < E; ++i)
       raw[i] = (LAST && OUT == FPOUT_U64) ? fp_canon_half(FWD ? fp_reduce(x[i], qd) : x[i], qd.x)
                                           : (u64)__double_as_longlong(x[i]);
-    if (LAST) {
+    if (LAST && !EPI) {
       u64* o = tl.gdst(gout, b, base);
       if (VEC) {
 #pragma unroll
@@ -617,6 +722,7 @@ __device__ __forceinline__ void run_pass_fp(u64* sm, const double2* tws, const T
       }
     }
   }
+  if (LAST && EPI) epilogue_store<Tile, GPA_LOG, WL>(sm, tl, gout);
 }
 
 template <int LOG_S, int P, int IN, int OUT, bool STW, class Tile>
@@ -628,7 +734,7 @@ __device__ __forceinline__ void fwd_passes_fp(u64* sm, const double2* tws, const
     run_pass_fp<LOG_S, pass_r0(LOG_S, P), pass_e(LOG_S, P), true, P == 0, last, IN, OUT, STW>(
         sm, tws, tl, gout, ch);
     if constexpr (!last) {
-      __syncthreads();
+      if constexpr (warp_local(LOG_S)) __syncwarp(); else __syncthreads();
       fwd_passes_fp<LOG_S, P + 1, IN, OUT, STW>(sm, tws, tl, gout, ch);
     }
   }
@@ -642,7 +748,7 @@ __device__ __forceinline__ void inv_passes_fp(u64* sm, const double2* tws, const
     run_pass_fp<LOG_S, pass_r0(LOG_S, P), pass_e(LOG_S, P), false, P == npass(LOG_S) - 1, last,
                 IN, OUT, STW>(sm, tws, tl, gout, ch);
     if constexpr (!last) {
-      __syncthreads();
+      if constexpr (warp_local(LOG_S)) __syncwarp(); else __syncthreads();
       inv_passes_fp<LOG_S, P - 1, IN, OUT, STW>(sm, tws, tl, gout, ch);
     }
   }
@@ -656,7 +762,8 @@ __device__ __forceinline__ void load_tw(double2* tws, const Tile& tl, const doub
     int n, off;
     long g;
     tl.tw_block(s, n, off, g);
-    for (int j = threadIdx.x; j < n; j += blockDim.x) cp_async16(&tws[off + j], &table[g + j]);
+    for (int j = threadIdx.x; j < n; j += blockDim.x)
+      cp_async16(&tws[off + tl.tw_perm(s, j)], &table[g + j]);
   }
 }
 
