@@ -15,6 +15,7 @@
 #include <stdexcept>
 
 #include "fhe_context.cuh"
+#include "ntt_plan.cuh"
 
 namespace {
 
@@ -141,10 +142,13 @@ int build_chain(const u64* primes, int count, int log_n, FheChain* ch) {
   }
   bool fp64 = true;
   for (int p = 0; p < count; ++p) fp64 &= primes[p] < ((u64)1 << 50);
-  std::vector<double2> twd, itwd, qd(count), nid(count), nwd(count);
+  std::vector<double2> twd, itwd, tws, qd(count), nid(count), nwd(count);
+  // staged tables: per prime and direction N1 column pairs + N chunk pairs
+  const size_t tws_dir = log_n >= 13 ? n + ((size_t)1 << split_log_n1(log_n)) : 0;
   if (fp64) {
     twd.resize(count * n);
     itwd.resize(count * n);
+    if (log_n >= 13) tws.assign(count * 2 * tws_dir, make_double2(0.0, 0.0));
     for (int p = 0; p < count; ++p) {
       const double q = (double)primes[p];
       for (size_t i = 0; i < n; ++i) {
@@ -152,6 +156,24 @@ int build_chain(const u64* primes, int count, int log_n, FheChain* ch) {
         itwd[p * n + i] = make_double2((double)itw[p * n + i].w, (double)itw[p * n + i].w / q);
       }
       qd[p] = make_double2(q, 1.0 / q);
+      if (log_n >= 13) {
+        // staged-order tables of the four-step kernels: column part (N1
+        // pairs) then one S-pair block per chunk; see ntt_plan.cuh
+        const int l1 = split_log_n1(log_n), ls = log_n - l1;
+        const size_t n1 = (size_t)1 << l1, s_ = (size_t)1 << ls;
+        double2* f = &tws[p * 2 * tws_dir];
+        double2* iv = &tws[p * 2 * tws_dir + tws_dir];
+        auto put = [&](size_t dst, size_t src_idx) {
+          f[dst] = twd[p * n + src_idx];
+          iv[dst] = itwd[p * n + src_idx];
+        };
+        for (int s = 0; s < l1; ++s)
+          for (int j = 0; j < (1 << s); ++j) put((1u << s) + staged_perm(l1, s, j), (1u << s) + j);
+        for (size_t ck = 0; ck < n1; ++ck)
+          for (int s = 0; s < ls; ++s)
+            for (int j = 0; j < (1 << s); ++j)
+              put(n1 + ck * s_ + (1u << s) + staged_perm(ls, s, j), ((n1 + ck) << s) + j);
+      }
       nid[p] = make_double2((double)ninv[p].w, (double)ninv[p].w / q);
       nwd[p] = make_double2((double)ninv_w1[p].w, (double)ninv_w1[p].w / q);
     }
@@ -160,7 +182,7 @@ int build_chain(const u64* primes, int count, int log_n, FheChain* ch) {
   const size_t o_mc = pk.addv(mc), o_tw = pk.addv(tw), o_itw = pk.addv(itw),
                o_ni = pk.addv(ninv), o_nw = pk.addv(ninv_w1);
   const size_t o_twd = pk.addv(twd), o_itwd = pk.addv(itwd), o_qd = pk.addv(qd),
-               o_nid = pk.addv(nid), o_nwd = pk.addv(nwd);
+               o_nid = pk.addv(nid), o_nwd = pk.addv(nwd), o_tws = pk.addv(tws);
   void* d = nullptr;
   FHE_CUDA_CHECK(cudaMalloc(&d, pk.buf.size()));
   FHE_CUDA_CHECK(cudaMemcpy(d, pk.buf.data(), pk.buf.size(), cudaMemcpyHostToDevice));
@@ -182,6 +204,8 @@ int build_chain(const u64* primes, int count, int log_n, FheChain* ch) {
   ch->dev.qd = fp64 ? (const double2*)(b + o_qd) : nullptr;
   ch->dev.ninv_d = fp64 ? (const double2*)(b + o_nid) : nullptr;
   ch->dev.ninv_w1_d = fp64 ? (const double2*)(b + o_nwd) : nullptr;
+  ch->dev.tws = (fp64 && log_n >= 13) ? (const double2*)(b + o_tws) : nullptr;
+  ch->dev.tws_dir = (long)tws_dir;
   return 0;
 }
 

@@ -34,6 +34,11 @@ struct DevChain {
   const double2* qd;       // [count]    (q, 1 / q)
   const double2* ninv_d;   // [count]    (n^-1, n^-1 / q)
   const double2* ninv_w1_d;// [count]    (ipsi_br[1] n^-1, ... / q)
+  // staged-order (w, w/q) tables of the four-step kernels (log_n >= 13):
+  // [count][2][tws_dir]: forward then inverse; per direction N1 column pairs,
+  // then N1 chunk blocks of N2 pairs (ntt_plan.cuh); tws_dir = N1 + N
+  const double2* tws;
+  long tws_dir;
 };
 
 // Row -> chain position mapping used by every batched kernel.  The

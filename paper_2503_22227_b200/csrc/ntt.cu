@@ -31,33 +31,21 @@
 //    the remaining log N2 stages on contiguous N2-chunks.
 #include "fhe_kernels.cuh"
 #include "fparith.cuh"
+#include "ntt_plan.cuh"
 
 namespace {
 
-constexpr int kThreads = 256;
-constexpr int kLogTile = 12;
-constexpr int kTile = 1 << kLogTile;  // elements per tile (32 KB)
-constexpr int kCols = 16;    // columns per column tile (one 128-byte segment)
+// Tile geometry.  Whole-row tiles: 4096 elements, 256 threads, 2 CTAs/SM.
+// Split (four-step) tiles: 2048 elements, 128 threads, 4 CTAs/SM -- small
+// CTAs keep the SM's FP64 pipe fed while other CTAs sit in their load /
+// barrier / store phases.
+constexpr int kRowThreads = 256;
+constexpr int kLogRowTile = 12;
+constexpr int kSplitThreads = 128;
+constexpr int kLogSplitTile = 11;
+constexpr int kSplitMinB = 4;
 
 
-#ifndef FHE_NTT_MAXE
-#define FHE_NTT_MAXE 5
-#endif
-#ifndef FHE_NTT_MINB
-#define FHE_NTT_MINB 2
-#endif
-#ifndef FHE_NTT_FP_MINB
-#define FHE_NTT_FP_MINB 2
-#endif
-constexpr int npass(int log_s) { return (log_s + FHE_NTT_MAXE - 1) / FHE_NTT_MAXE; }
-constexpr int pass_e(int log_s, int p) {
-  return log_s / npass(log_s) + (p < log_s % npass(log_s) ? 1 : 0);
-}
-constexpr int pass_r0(int log_s, int p) {
-  int r = 0;
-  for (int i = 0; i < p; ++i) r += pass_e(log_s, i);
-  return r;
-}
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
@@ -66,6 +54,23 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n"); }
 __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+}
+
+// Padded shared-memory index of array tiles (whole rows, chunks): 16 bytes of
+// pad per 16-element (128-byte) row and another 16 per 256 elements.  With
+// array-major thread mapping (an array's groups on consecutive lanes) both
+// stride-16 and contiguous groups are bank-conflict free.
+__device__ __forceinline__ int padix(int t) { return t + ((t >> 4) << 1) + ((t >> 8) << 1); }
+
+constexpr int padded_words(int tile) { return tile + tile / 8 + tile / 128; }
+// padded distance between element i and i+1 of a thread's group (stride TMIN
+// in k-rows of CN columns (column tiles) or in elements), 0 when not affine
+constexpr int pad_step(int cn, int tmin, int e) {
+  return cn ? (tmin >= 16 ? (cn + 2) * tmin + 2 * (tmin / 16)
+                          : (tmin * e <= 16 ? (cn + 2) * tmin : 0))
+              : (tmin == 1 ? 1
+                           : (tmin >= 256 ? tmin + tmin / 8 + tmin / 128
+                                          : (tmin >= 16 && tmin * e <= 256 ? tmin + tmin / 8 : 0)));
 }
 
 // Per-array context of one local transform.
@@ -115,10 +120,17 @@ template <int LOG_N>
 struct RowsTile {
   static constexpr int LOG_S = LOG_N;
   static constexpr int S = 1 << LOG_N;
-  static constexpr int NB = S >= kTile ? 1 : (kTile / S > 32 ? 32 : kTile / S);
+  static constexpr int TILE = 1 << kLogRowTile;
+  static constexpr int NB = S >= TILE ? 1 : (TILE / S > 32 ? 32 : TILE / S);
+  static constexpr int THREADS = kRowThreads;
+  static constexpr int MINB = 2;
+  static constexpr int SMEM_WORDS = padded_words(NB * S);
+  static constexpr int LOG_CN_OR0 = 0;
+  static constexpr long N2 = 1;  // (column tiles only)
   static constexpr bool COLS = false;
   static constexpr bool EPI = true;
   static constexpr long GSTEP_PER_K = 1;
+  __device__ static __forceinline__ int pad(int t) { return padix(t); }
   int rows;
   RowMap map;
   RowAddr src, dst;
@@ -149,16 +161,14 @@ struct RowsTile {
   __device__ __forceinline__ int arrays() const { return nb; }
   // rows of a tile may use different primes: twiddles are read through L1
   static constexpr int TWMAX = 0;
-  __device__ __forceinline__ int tw_blocks() const { return 0; }
-  __device__ __forceinline__ void tw_block(int, int& n, int& o, long& g) const { n = o = 0; g = 0; }
-  __device__ __forceinline__ int tw_off(int) const { return 0; }
+  __device__ __forceinline__ int tw_pairs() const { return 0; }
+  __device__ __forceinline__ long tw_src_off() const { return 0; }
+  __device__ __forceinline__ int tw_base(int, int) const { return 0; }
   __device__ __forceinline__ int tw_prime() const { return 0; }
-  static constexpr bool TW_T = false;
-  static constexpr int TW_P = 0;
-  __device__ __forceinline__ int tw_perm(int, int j) const { return j; }
 };
 
-// First log N1 stages on a [N1][16] column tile of one row.
+// First log N1 stages on a [N1][CN] column tile of one row (CN = 2048 / N1
+// columns, one 8*CN-byte segment per k).
 template <int LOG_N, int LOG_N1>
 struct ColsTile {
   static constexpr int LOG_S = LOG_N1;
@@ -166,7 +176,20 @@ struct ColsTile {
   static constexpr bool EPI = true;
   static constexpr int N2 = 1 << (LOG_N - LOG_N1);
   static constexpr long GSTEP_PER_K = N2;
-  static constexpr int TILES = N2 / kCols;
+  static constexpr int LOG_CN = kLogSplitTile - LOG_N1;
+  static constexpr int CN = 1 << LOG_CN;
+  static constexpr int LOG_CN_OR0 = LOG_CN;
+  static constexpr int TILES = N2 / CN;
+  static constexpr int THREADS = kSplitThreads;
+  static constexpr int MINB = kSplitMinB;
+  static constexpr int TILE = 1 << kLogSplitTile;
+  // padded index: k-rows of CN words + 2, and 2 more per 16 k-rows, so both
+  // stride-16 and contiguous-16 groups along k are bank-conflict free
+  __device__ static __forceinline__ int pad(int t) {
+    const int k = t >> LOG_CN;
+    return t + (k << 1) + ((k >> 4) << 1);
+  }
+  static constexpr int SMEM_WORDS = TILE + 2 * (1 << LOG_N1) + 2 * ((1 << LOG_N1) >> 4);
   int rows;
   RowMap map;
   RowAddr src, dst;
@@ -177,36 +200,21 @@ struct ColsTile {
   FastDiv limbs_div;  // row -> (row / limbs, row % limbs) without IMAD-heavy division
   __device__ __forceinline__ void setup(int t) {
     row = t / TILES;
-    j0 = (t % TILES) * kCols;
+    j0 = (t % TILES) * CN;
     const int rq = limbs_div.div(row);
     const int cls = row - rq * map.limbs;
     p = (map.idx ? map.idx[cls] : cls) + map.offset;
     so = (src.bstride ? rq * src.bstride + ((long)cls << LOG_N) : ((long)row << LOG_N)) + j0;
     dof = (dst.bstride ? rq * dst.bstride + ((long)cls << LOG_N) : ((long)row << LOG_N)) + j0;
   }
-  // twiddles staged in shared memory per tile: psi_br[0 .. N1) of the row's
-  // prime (every column stage indexes below N1)
+  // twiddles staged in shared memory per tile: the N1-pair column block of
+  // the prime's staged table (ntt_plan.cuh)
   static constexpr int TWMAX = 1 << LOG_N1;
-  __device__ __forceinline__ int tw_blocks() const { return 1; }
-  __device__ __forceinline__ void tw_block(int, int& n, int& smem_off, long& gofs) const {
-    n = 1 << LOG_N1;
-    smem_off = 0;
-    gofs = 0;
-  }
-  __device__ __forceinline__ int tw_off(int) const { return 0; }
+  __device__ __forceinline__ int tw_pairs() const { return 1 << LOG_N1; }
+  __device__ __forceinline__ long tw_src_off() const { return 0; }
+  __device__ __forceinline__ int tw_base(int s, int) const { return 1 << s; }
   __device__ __forceinline__ int tw_prime() const { return p; }
-  // last-pass stages stored transposed, as in ChunksTile: pair 2^s + j with
-  // j = (g << rr) | blk goes to 2^s + ((blk << TW_P) | g)
-  static constexpr int TW_P = pass_r0(LOG_S, npass(LOG_S) - 1);
-  static constexpr bool TW_T = true;
-  __device__ __forceinline__ int tw_perm(int, int j) const {
-    if (j < (1 << TW_P)) return j;
-    const int s = 31 - __clz(j);
-    const int rr = s - TW_P;
-    const int jl = j - (1 << s);
-    return (1 << s) | ((jl & ((1 << rr) - 1)) << TW_P) | (jl >> rr);
-  }
-  __device__ __forceinline__ int tile_index(int b, int k) const { return k * kCols + b; }
+  __device__ __forceinline__ int tile_index(int b, int k) const { return (k << LOG_CN) + b; }
   // array-major: the groups of one column sit on consecutive lanes, so a
   // pass's exchange stays inside the warp when every pass has 2^g_log groups
   // With 16 groups per column a warp owns two columns; each half-warp holds
@@ -231,7 +239,7 @@ struct ColsTile {
   __device__ __forceinline__ ArrCtx ctx(int, const DevChain& ch) const {
     return ArrCtx{(fwd ? ch.tw : ch.itw) + ((size_t)p << LOG_N), ch.mc[p].q, 1, p, !fwd};
   }
-  __device__ __forceinline__ int arrays() const { return kCols; }
+  __device__ __forceinline__ int arrays() const { return CN; }
 };
 
 // Remaining stages on contiguous N2-chunks: a tile holds R rows of one
@@ -243,10 +251,17 @@ template <int LOG_N, int LOG_N1>
 struct ChunksTile {
   static constexpr int LOG_S = LOG_N - LOG_N1;
   static constexpr int S = 1 << LOG_S;
-  static constexpr int NB = kTile / S;
+  static constexpr int TILE = 1 << kLogSplitTile;
+  static constexpr int NB = TILE / S;
+  static constexpr int THREADS = kSplitThreads;
+  static constexpr int MINB = kSplitMinB;
+  static constexpr int SMEM_WORDS = padded_words(TILE);
+  static constexpr int LOG_CN_OR0 = 0;
+  static constexpr long N2 = 1;  // (column tiles only)
   static constexpr bool COLS = false;
   static constexpr bool EPI = true;
   static constexpr long GSTEP_PER_K = 1;
+  __device__ static __forceinline__ int pad(int t) { return padix(t); }
   static constexpr int N1 = 1 << LOG_N1;
   int rows;
   RowMap map;
@@ -268,7 +283,7 @@ struct ChunksTile {
     const int u = t >> log_cb;
     const int cls = rb_div.div(u);
     const int rb = u - cls * rblocks;
-    log_c = kLogTile - LOG_S - log_r;
+    log_c = kLogSplitTile - LOG_S - log_r;
     c0 = cb << log_c;
     const int i0 = rb << log_r;
     const int row0 = cls + i0 * map.limbs;
@@ -284,33 +299,15 @@ struct ChunksTile {
     sstep = src.bstride ? src.bstride : ((long)map.limbs << LOG_N);
     dstep = dst.bstride ? dst.bstride : ((long)map.limbs << LOG_N);
   }
-  // twiddles staged in shared memory per tile (tiles of <= 2 chunks): local
-  // stage s of chunk c reads psi_br[((N1 + c) << s) + j], so the C chunks of a
-  // tile need, per stage, the contiguous run of C << s pairs from
-  // (N1 + c0) << s, stored at C * (2^s - 1).
-  static constexpr int TWMAX = 2 * ((1 << LOG_S) - 1);
-  __device__ __forceinline__ int tw_blocks() const { return LOG_S; }
-  __device__ __forceinline__ void tw_block(int s, int& n, int& smem_off, long& gofs) const {
-    n = 1 << (s + log_c);
-    smem_off = ((1 << s) - 1) << log_c;
-    gofs = (long)(N1 + c0) << s;
-  }
-  __device__ __forceinline__ int tw_off(int s) const {
-    return (((1 << s) - 1) << log_c) - ((N1 + c0) << s);
+  // twiddles staged in shared memory per tile (tiles of <= 2 chunks): the
+  // C consecutive S-pair chunk blocks of the prime's staged table
+  static constexpr int TWMAX = 2 << LOG_S;
+  __device__ __forceinline__ int tw_pairs() const { return S << log_c; }
+  __device__ __forceinline__ long tw_src_off() const { return N1 + ((long)c0 << LOG_S); }
+  __device__ __forceinline__ int tw_base(int s, int m0) const {
+    return ((m0 - N1 - c0) << LOG_S) + (1 << s);
   }
   __device__ __forceinline__ int tw_prime() const { return p; }
-  // Stages s >= TW_P (the last register pass, one group per thread) store a
-  // chunk's pairs transposed: j = (g << rr) | blk (rr = s - TW_P) goes to
-  // (blk << TW_P) | g, so the 16 groups of a warp read 16 consecutive pairs
-  // (conflict-free) instead of pairs 2^rr apart.
-  static constexpr int TW_P = pass_r0(LOG_S, npass(LOG_S) - 1);
-  static constexpr bool TW_T = true;
-  __device__ __forceinline__ int tw_perm(int s, int j) const {
-    if (s < TW_P) return j;
-    const int rr = s - TW_P;
-    const int jl = j & ((1 << s) - 1);
-    return (j - jl) | ((jl & ((1 << rr) - 1)) << TW_P) | (jl >> rr);
-  }
   __device__ __forceinline__ int tile_index(int b, int k) const { return (b << LOG_S) + k; }
   __device__ __forceinline__ void split(int G, int gpa_log, int& b, int& g) const {
     b = G >> gpa_log;
@@ -351,27 +348,6 @@ enum OutMode {
   OUT_REDUCE = 2   // forward lazy: [0, 33q) -> [0, q) by Barrett
 };
 
-// Padded shared-memory index: one 16-byte pad per 16-element (128-byte)
-// row.  Contiguous passes (16-byte accesses, lanes on different rows) and
-// strided passes (8-byte accesses, lanes on consecutive words) are both
-// bank-conflict free, and the padded index stays affine in the element
-// counter, so every shared-memory access of a pass uses an immediate offset.
-// Padded shared-memory index: 16 bytes of pad per 16-element (128-byte) row
-// and another 16 per 256 elements.  With array-major thread mapping (the
-// 2^g groups of one array on consecutive lanes) every pass is conflict-free:
-// stride-16 groups vary the row's low nibble (first term), contiguous groups
-// of the column tile vary the high nibble (second term).
-__device__ __forceinline__ int padix(int t) { return t + ((t >> 4) << 1) + ((t >> 8) << 1); }
-constexpr int kTileSmem = kTile + kTile / 8 + kTile / 128;  // padded words per buffer
-// padded distance between element i and i+1 of a thread's group (stride TMIN
-// in tile rows of 16 (COLS) or elements), 0 when it is not affine
-constexpr int pad_step(bool cols, int tmin, int e) {
-  return cols ? (tmin >= 16 ? 18 * tmin + 2 * (tmin / 16) : (tmin * e <= 16 ? 18 * tmin : 0))
-              : (tmin == 1 ? 1
-                           : (tmin >= 256 ? tmin + tmin / 8 + tmin / 128
-                                          : (tmin >= 16 && tmin * e <= 256 ? tmin + tmin / 8 : 0)));
-}
-
 // Every register pass of a LOG_S-stage local transform has the same radix and
 // at most 32 groups per array: with array-major thread mapping each array is
 // owned by one warp in every pass, so passes exchange data under __syncwarp.
@@ -387,32 +363,50 @@ constexpr bool warp_local(int log_s) {
 //  * array tiles otherwise: CTA-wide over all arrays.
 template <class Tile, int GPA_LOG, bool WL>
 __device__ __forceinline__ void epilogue_store(const u64* sm, const Tile& tl, u64* gout) {
-  constexpr int S = 1 << Tile::LOG_S;
+  constexpr int LOG_S = Tile::LOG_S;
+  constexpr int S = 1 << LOG_S;
+  constexpr int T = Tile::THREADS;
   if constexpr (Tile::COLS) {
+    constexpr int CN = 1 << Tile::LOG_CN_OR0;
+    constexpr int PPR = CN / 2;
+    constexpr int KSTEP = T / PPR;
     __syncthreads();
-    for (int q = threadIdx.x; q < S * kCols / 2; q += blockDim.x) {
-      const int k = q >> 3, c = (q & 7) << 1;
-      const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(&sm[padix(tl.tile_index(c, k))]);
-      *reinterpret_cast<ulonglong2*>(tl.gdst(gout, c, k)) = v;
+    const int k0 = threadIdx.x / PPR, c = (threadIdx.x % PPR) * 2;
+    u64* g = tl.gdst(gout, c, k0);
+#pragma unroll
+    for (int j = 0; j < S / KSTEP; ++j) {
+      const int so = (KSTEP % 16 == 0)
+                         ? Tile::pad(k0 * CN + c) + j * (KSTEP * (CN + 2) + 2 * (KSTEP / 16))
+                         : Tile::pad((k0 + j * KSTEP) * CN + c);
+      const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(sm + so);
+      *reinterpret_cast<ulonglong2*>(g + (long)j * KSTEP * Tile::N2) = v;
     }
   } else if constexpr (WL) {
+    // the warp's arrays (all passes kept them on this warp)
     __syncwarp();
     const int lane = threadIdx.x & 31;
+    constexpr int APW = 32 >> GPA_LOG;  // arrays per warp and G-sweep
     const int total = tl.arrays() << GPA_LOG;
-    for (int G0 = threadIdx.x - lane; G0 < total; G0 += blockDim.x) {
-      const int b0 = G0 >> GPA_LOG;
-      const int b1 = min((G0 + 32) >> GPA_LOG, tl.arrays());
-      for (int q = lane; q < ((b1 - b0) * S) >> 1; q += 32) {
-        const int bb = b0 + q / (S >> 1), k = (q % (S >> 1)) << 1;
-        const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(&sm[padix(tl.tile_index(bb, k))]);
-        *reinterpret_cast<ulonglong2*>(tl.gdst(gout, bb, k)) = v;
+    for (int G0 = threadIdx.x - lane; G0 < total; G0 += T) {
+#pragma unroll
+      for (int a = 0; a < APW; ++a) {
+        const int b = (G0 >> GPA_LOG) + a;
+        if (b >= tl.arrays()) break;
+        u64* g = tl.gdst(gout, b, 0);
+#pragma unroll
+        for (int k = 2 * lane; k < S; k += 64) {
+          const ulonglong2 v =
+              *reinterpret_cast<const ulonglong2*>(&sm[Tile::pad((b << LOG_S) + k)]);
+          *reinterpret_cast<ulonglong2*>(g + k) = v;
+        }
       }
     }
   } else {
     __syncthreads();
-    for (int q = threadIdx.x; q < (tl.arrays() * S) >> 1; q += blockDim.x) {
-      const int bb = q / (S >> 1), k = (q % (S >> 1)) << 1;
-      const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(&sm[padix(tl.tile_index(bb, k))]);
+    for (int q = threadIdx.x; q < (tl.arrays() << LOG_S) >> 1; q += T) {
+      const int bb = q >> (LOG_S - 1), k = (q & ((S >> 1) - 1)) << 1;
+      const ulonglong2 v =
+          *reinterpret_cast<const ulonglong2*>(&sm[Tile::pad((bb << LOG_S) + k)]);
       *reinterpret_cast<ulonglong2*>(tl.gdst(gout, bb, k)) = v;
     }
   }
@@ -430,7 +424,7 @@ __device__ __forceinline__ void run_pass(u64* sm, const Tile& tl, u64* gout,
   constexpr int GPA_LOG = LOG_S - E_LOG;
   constexpr bool VEC = (TMIN_LOG == 0) && !Tile::COLS && E >= 2;
   // padded stride between consecutive elements of the thread (0: not affine)
-  constexpr int PSTEP = pad_step(Tile::COLS, TMIN, E);
+  constexpr int PSTEP = pad_step(Tile::COLS ? (1 << Tile::LOG_CN_OR0) : 0, TMIN, E);
   const int total = tl.arrays() << GPA_LOG;
   for (int G = threadIdx.x; G < total; G += blockDim.x) {
     int b, g;
@@ -438,7 +432,7 @@ __device__ __forceinline__ void run_pass(u64* sm, const Tile& tl, u64* gout,
     const int hi = g >> TMIN_LOG;
     const int lo = g & (TMIN - 1);
     const int base = hi * 2 * T0 + lo;
-    const int pb = padix(tl.tile_index(b, base));
+    const int pb = Tile::pad(tl.tile_index(b, base));
     const ArrCtx cx = tl.ctx(b, ch);
     const u64 q = cx.q;
     const u64 q2 = 2 * q;
@@ -455,7 +449,7 @@ __device__ __forceinline__ void run_pass(u64* sm, const Tile& tl, u64* gout,
       for (int i = 0; i < E; ++i) x[i] = sm[pb + i * PSTEP];
     } else {
 #pragma unroll
-      for (int i = 0; i < E; ++i) x[i] = sm[padix(tl.tile_index(b, base + i * TMIN))];
+      for (int i = 0; i < E; ++i) x[i] = sm[Tile::pad(tl.tile_index(b, base + i * TMIN))];
     }
     if (FWD) {
 #pragma unroll
@@ -534,7 +528,7 @@ __device__ __forceinline__ void run_pass(u64* sm, const Tile& tl, u64* gout,
         for (int i = 0; i < E; ++i) sm[pb + i * PSTEP] = x[i];
       } else {
 #pragma unroll
-        for (int i = 0; i < E; ++i) sm[padix(tl.tile_index(b, base + i * TMIN))] = x[i];
+        for (int i = 0; i < E; ++i) sm[Tile::pad(tl.tile_index(b, base + i * TMIN))] = x[i];
       }
     }
   }
@@ -597,7 +591,7 @@ __device__ __forceinline__ void run_pass_fp(u64* sm, const double2* tws, const T
   constexpr int TMIN = 1 << TMIN_LOG;
   constexpr int GPA_LOG = LOG_S - E_LOG;
   constexpr bool VEC = (TMIN_LOG == 0) && !Tile::COLS && E >= 2;
-  constexpr int PSTEP = pad_step(Tile::COLS, TMIN, E);
+  constexpr int PSTEP = pad_step(Tile::COLS ? (1 << Tile::LOG_CN_OR0) : 0, TMIN, E);
   // twiddles of the whole pass are loaded up front (E - 1 pairs) when they
   // fit the register budget, so their L1/L2 latency overlaps the tile reads
   constexpr bool PRELOAD = !STW && E <= 16;
@@ -605,8 +599,8 @@ __device__ __forceinline__ void run_pass_fp(u64* sm, const double2* tws, const T
   // coalesced stores (no strided 8-byte STGs from the butterfly registers)
   constexpr bool EPI = Tile::EPI;
   constexpr bool WL = warp_local(LOG_S);
-  // staged twiddles of this pass are stored transposed (Tile::tw_perm)
-  constexpr bool TT = STW && Tile::TW_T && R0 == Tile::TW_P && TMIN_LOG == 0;
+  // staged twiddles of the last pass are stored transposed (staged_perm)
+  constexpr bool TT = STW && R0 == pass_r0(LOG_S, npass(LOG_S) - 1) && TMIN_LOG == 0;
   const int total = tl.arrays() << GPA_LOG;
   for (int G = threadIdx.x; G < total; G += blockDim.x) {
     int b, g;
@@ -614,7 +608,7 @@ __device__ __forceinline__ void run_pass_fp(u64* sm, const double2* tws, const T
     const int hi = g >> TMIN_LOG;
     const int lo = g & (TMIN - 1);
     const int base = hi * 2 * T0 + lo;
-    const int pb = padix(tl.tile_index(b, base));
+    const int pb = Tile::pad(tl.tile_index(b, base));
     const ArrCtx cx = tl.ctx(b, ch);
     const double2 qd = __ldg(&ch.qd[cx.prime]);
     const double2* tw = (FWD ? ch.twd : ch.itwd) + ((size_t)cx.prime << ch.log_n);
@@ -640,7 +634,7 @@ __device__ __forceinline__ void run_pass_fp(u64* sm, const double2* tws, const T
       for (int i = 0; i < E; ++i) raw[i] = sm[pb + i * PSTEP];
     } else {
 #pragma unroll
-      for (int i = 0; i < E; ++i) raw[i] = sm[padix(tl.tile_index(b, base + i * TMIN))];
+      for (int i = 0; i < E; ++i) raw[i] = sm[Tile::pad(tl.tile_index(b, base + i * TMIN))];
     }
     double x[E];
 #pragma unroll
@@ -650,8 +644,8 @@ __device__ __forceinline__ void run_pass_fp(u64* sm, const double2* tws, const T
 #pragma unroll
       for (int rr = 0; rr < E_LOG; ++rr) {
         const int half = E >> (rr + 1);
-        const double2* twr = TT ? tws + tl.tw_off(R0 + rr) + (cx.m0 << (R0 + rr)) + hi
-                             : STW ? tws + tl.tw_off(R0 + rr) + (cx.m0 << (R0 + rr)) + (hi << rr)
+        const double2* twr = TT ? tws + tl.tw_base(R0 + rr, cx.m0) + hi
+                             : STW ? tws + tl.tw_base(R0 + rr, cx.m0) + (hi << rr)
                                    : tw + (cx.m0 << (R0 + rr)) + (hi << rr);
 #pragma unroll
         for (int blk = 0; blk < (1 << rr); ++blk) {
@@ -673,8 +667,8 @@ __device__ __forceinline__ void run_pass_fp(u64* sm, const double2* tws, const T
       for (int rr = E_LOG - 1; rr >= 0; --rr) {
         const int half = E >> (rr + 1);
         const bool fold = (R0 == 0) && (rr == 0) && cx.fold;
-        const double2* twr = TT ? tws + tl.tw_off(R0 + rr) + (cx.m0 << (R0 + rr)) + hi
-                             : STW ? tws + tl.tw_off(R0 + rr) + (cx.m0 << (R0 + rr)) + (hi << rr)
+        const double2* twr = TT ? tws + tl.tw_base(R0 + rr, cx.m0) + hi
+                             : STW ? tws + tl.tw_base(R0 + rr, cx.m0) + (hi << rr)
                                    : tw + (cx.m0 << (R0 + rr)) + (hi << rr);
 #pragma unroll
         for (int blk = 0; blk < (1 << rr); ++blk) {
@@ -718,7 +712,7 @@ __device__ __forceinline__ void run_pass_fp(u64* sm, const double2* tws, const T
         for (int i = 0; i < E; ++i) sm[pb + i * PSTEP] = raw[i];
       } else {
 #pragma unroll
-        for (int i = 0; i < E; ++i) sm[padix(tl.tile_index(b, base + i * TMIN))] = raw[i];
+        for (int i = 0; i < E; ++i) sm[Tile::pad(tl.tile_index(b, base + i * TMIN))] = raw[i];
       }
     }
   }
@@ -754,42 +748,58 @@ __device__ __forceinline__ void inv_passes_fp(u64* sm, const double2* tws, const
   }
 }
 
-// Stage the tile's twiddle pairs in shared memory (cp.async, committed with
-// the tile's data group).
+// Stage the tile's twiddle pairs in shared memory (one contiguous block of
+// the staged table; cp.async, committed with the tile's data group).
 template <class Tile>
 __device__ __forceinline__ void load_tw(double2* tws, const Tile& tl, const double2* table) {
-  for (int s = 0; s < tl.tw_blocks(); ++s) {
-    int n, off;
-    long g;
-    tl.tw_block(s, n, off, g);
-    for (int j = threadIdx.x; j < n; j += blockDim.x)
-      cp_async16(&tws[off + tl.tw_perm(s, j)], &table[g + j]);
-  }
+  const double2* g = table + tl.tw_src_off();
+  for (int j = threadIdx.x; j < tl.tw_pairs(); j += Tile::THREADS) cp_async16(&tws[j], &g[j]);
 }
 
-// Issue the cp.async copies of one tile (16 bytes per copy).
+// Issue the cp.async copies of one tile (16 bytes per copy).  Each thread
+// copies fixed (column pair | array offset) positions, so the per-copy
+// address arithmetic reduces to constant strides.
 template <class Tile>
 __device__ __forceinline__ void load_tile(u64* sm, const Tile& tl, const u64* src) {
   constexpr int LOG_S = Tile::LOG_S;
-  const int nel = tl.arrays() << LOG_S;
-#pragma unroll 4
-  for (int e = 2 * threadIdx.x; e < nel; e += 2 * blockDim.x) {
-    int b, k;
-    if (Tile::COLS) {
-      k = e / kCols;
-      b = e % kCols;
+  constexpr int S = 1 << LOG_S;
+  constexpr int T = Tile::THREADS;
+  if constexpr (Tile::COLS) {
+    constexpr int CN = 1 << Tile::LOG_CN_OR0;
+    constexpr int PPR = CN / 2;       // pairs per k-row
+    constexpr int KSTEP = T / PPR;    // k-rows per sweep of the CTA
+    const int k0 = threadIdx.x / PPR, c = (threadIdx.x % PPR) * 2;
+    const u64* g = tl.gsrc(src, c, k0);
+    if constexpr (KSTEP % 16 == 0) {
+      u64* s = sm + Tile::pad(k0 * CN + c);
+#pragma unroll
+      for (int j = 0; j < S / KSTEP; ++j)
+        cp_async16(s + j * (KSTEP * (CN + 2) + 2 * (KSTEP / 16)), g + (long)j * KSTEP * Tile::N2);
     } else {
-      b = e >> LOG_S;
-      k = e & ((1 << LOG_S) - 1);
+#pragma unroll
+      for (int j = 0; j < S / KSTEP; ++j)
+        cp_async16(&sm[Tile::pad((k0 + j * KSTEP) * CN + c)], g + (long)j * KSTEP * Tile::N2);
     }
-    cp_async16(&sm[padix(e)], tl.gsrc(src, b, k));
+  } else {
+    constexpr int PPA = S / 2;  // pairs per array
+    if constexpr (PPA <= T) {
+      constexpr int APJ = T / PPA;
+      const int k = (threadIdx.x % PPA) * 2;
+      for (int b = threadIdx.x / PPA; b < tl.arrays(); b += APJ)
+        cp_async16(&sm[Tile::pad((b << LOG_S) + k)], tl.gsrc(src, b, k));
+    } else {
+      for (int b = 0; b < tl.arrays(); ++b)
+#pragma unroll 4
+        for (int k = 2 * threadIdx.x; k < S; k += 2 * T)
+          cp_async16(&sm[Tile::pad((b << LOG_S) + k)], tl.gsrc(src, b, k));
+    }
   }
   cp_async_commit();
 }
 
 // Persistent, double-buffered transform kernel over the tiles of one policy.
 template <class Tile, bool FWD, bool LAZY, int OUT>
-__global__ void __launch_bounds__(kThreads, FHE_NTT_MINB)
+__global__ void __launch_bounds__(Tile::THREADS, Tile::MINB)
     ntt_tiles_kernel(const DevChain ch, u64* dst, const u64* src, Tile tl, int ntiles) {
   extern __shared__ __align__(16) u64 smem_raw[];
   // contiguous tile range per CTA (keeps the tile order's twiddle locality)
@@ -808,14 +818,15 @@ __global__ void __launch_bounds__(kThreads, FHE_NTT_MINB)
     if (tn < t_end) {
       Tile nxt = tl;
       nxt.setup(tn);
-      if (nxt.valid) load_tile(smem_raw + (buf ? 0 : kTileSmem), nxt, src);
+      if (nxt.valid) load_tile(smem_raw + (buf ? 0 : Tile::SMEM_WORDS), nxt, src);
       else cp_async_commit();
     }
     if (cur.valid) {
       if (FWD)
-        fwd_passes<Tile::LOG_S, 0, LAZY, OUT>(smem_raw + (buf ? kTileSmem : 0), cur, dst, ch);
+        fwd_passes<Tile::LOG_S, 0, LAZY, OUT>(smem_raw + (buf ? Tile::SMEM_WORDS : 0), cur, dst, ch);
       else
-        inv_passes<Tile::LOG_S, npass(Tile::LOG_S) - 1>(smem_raw + (buf ? kTileSmem : 0), cur, dst, ch);
+        inv_passes<Tile::LOG_S, npass(Tile::LOG_S) - 1>(smem_raw + (buf ? Tile::SMEM_WORDS : 0), cur,
+                                                         dst, ch);
     }
     if (tn < t_end) cur.setup(tn);
     buf ^= 1;
@@ -826,12 +837,13 @@ __global__ void __launch_bounds__(kThreads, FHE_NTT_MINB)
 // are staged in shared memory with its data (double-buffered), so every
 // butterfly reads its twiddle with an LDS instead of an L1/L2 round trip.
 template <class Tile, bool FWD, int IN, int OUT, bool STW>
-__global__ void __launch_bounds__(kThreads, FHE_NTT_FP_MINB)
+__global__ void __launch_bounds__(Tile::THREADS, Tile::MINB)
     ntt_tiles_fp_kernel(const DevChain ch, u64* dst, const u64* src, Tile tl, int ntiles) {
   extern __shared__ __align__(16) u64 smem_raw[];
   constexpr int TWM = STW ? Tile::TWMAX : 0;
-  double2* tw_raw = reinterpret_cast<double2*>(smem_raw + 2 * kTileSmem);
-  const double2* table = FWD ? ch.twd : ch.itwd;
+  double2* tw_raw = reinterpret_cast<double2*>(smem_raw + 2 * Tile::SMEM_WORDS);
+  // staged tables: [prime][fwd | inv][N]
+  const double2* table = STW ? ch.tws + (FWD ? 0 : ch.tws_dir) : nullptr;
   // contiguous tile range per CTA (keeps the tile order's twiddle locality)
   const int t_end = (int)(((long)(blockIdx.x + 1) * ntiles) / gridDim.x);
   int t = (int)(((long)blockIdx.x * ntiles) / gridDim.x);
@@ -839,7 +851,7 @@ __global__ void __launch_bounds__(kThreads, FHE_NTT_FP_MINB)
   Tile cur = tl;
   cur.setup(t);
   if (cur.valid) {
-    if (STW) load_tw(tw_raw, cur, table + ((size_t)cur.tw_prime() << ch.log_n));
+    if (STW) load_tw(tw_raw, cur, table + 2 * ch.tws_dir * cur.tw_prime());
     load_tile(smem_raw, cur, src);
   } else {
     cp_async_commit();
@@ -854,14 +866,14 @@ __global__ void __launch_bounds__(kThreads, FHE_NTT_FP_MINB)
       nxt.setup(tn);
       if (nxt.valid) {
         if (STW)
-          load_tw(tw_raw + (buf ? 0 : TWM), nxt, table + ((size_t)nxt.tw_prime() << ch.log_n));
-        load_tile(smem_raw + (buf ? 0 : kTileSmem), nxt, src);
+          load_tw(tw_raw + (buf ? 0 : TWM), nxt, table + 2 * ch.tws_dir * nxt.tw_prime());
+        load_tile(smem_raw + (buf ? 0 : Tile::SMEM_WORDS), nxt, src);
       } else {
         cp_async_commit();
       }
     }
     if (cur.valid) {
-      u64* sm = smem_raw + (buf ? kTileSmem : 0);
+      u64* sm = smem_raw + (buf ? Tile::SMEM_WORDS : 0);
       const double2* tws = tw_raw + (buf ? TWM : 0);
       if (FWD)
         fwd_passes_fp<Tile::LOG_S, 0, IN, OUT, STW>(sm, tws, cur, dst, ch);
@@ -888,15 +900,16 @@ template <class Tile, bool FWD, bool LAZY, int OUT>
 int launch_tiles(const DevChain& ch, u64* dst, const u64* src, const Tile& tl, int ntiles,
                  cudaStream_t st) {
   if (ntiles <= 0) return 0;
-  const int grid = std::min(ntiles, FHE_NTT_MINB * sm_count());
-  constexpr int smem = 2 * kTileSmem * sizeof(u64);
+  const int grid = std::min(ntiles, Tile::MINB * sm_count());
+  constexpr int smem = 2 * Tile::SMEM_WORDS * sizeof(u64);
   static bool attr = false;  // once per instantiation
   if (!attr) {
     cudaFuncSetAttribute(ntt_tiles_kernel<Tile, FWD, LAZY, OUT>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     attr = true;
   }
-  ntt_tiles_kernel<Tile, FWD, LAZY, OUT><<<grid, kThreads, smem, st>>>(ch, dst, src, tl, ntiles);
+  ntt_tiles_kernel<Tile, FWD, LAZY, OUT><<<grid, Tile::THREADS, smem, st>>>(ch, dst, src, tl,
+                                                                           ntiles);
   FHE_LAUNCH_CHECK();
   return 0;
 }
@@ -906,15 +919,16 @@ template <class Tile, bool FWD, int IN, int OUT, bool STW = false>
 int launch_tiles_fp(const DevChain& ch, u64* dst, const u64* src, const Tile& tl, int ntiles,
                     cudaStream_t st) {
   if (ntiles <= 0) return 0;
-  const int grid = std::min(ntiles, FHE_NTT_FP_MINB * sm_count());
-  constexpr int smem = 2 * kTileSmem * sizeof(u64) + (STW ? 2 * Tile::TWMAX * sizeof(double2) : 0);
+  const int grid = std::min(ntiles, Tile::MINB * sm_count());
+  constexpr int smem =
+      2 * Tile::SMEM_WORDS * sizeof(u64) + (STW ? 2 * Tile::TWMAX * sizeof(double2) : 0);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(ntt_tiles_fp_kernel<Tile, FWD, IN, OUT, STW>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     attr = true;
   }
-  ntt_tiles_fp_kernel<Tile, FWD, IN, OUT, STW><<<grid, kThreads, smem, st>>>(ch, dst, src, tl,
+  ntt_tiles_fp_kernel<Tile, FWD, IN, OUT, STW><<<grid, Tile::THREADS, smem, st>>>(ch, dst, src, tl,
                                                                             ntiles);
   FHE_LAUNCH_CHECK();
   return 0;

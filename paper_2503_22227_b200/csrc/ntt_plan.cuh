@@ -1,0 +1,34 @@
+// Register-pass plan of the tiled NTT, shared by the kernels (ntt.cu) and the
+// host-side table builder (context.cu).
+#pragma once
+
+#ifndef FHE_NTT_MAXE
+#define FHE_NTT_MAXE 5
+#endif
+
+// A local transform of 2^log_s points runs npass register passes of radix
+// 2^pass_e; pass p starts at local stage pass_r0.
+constexpr int npass(int log_s) { return (log_s + FHE_NTT_MAXE - 1) / FHE_NTT_MAXE; }
+constexpr int pass_e(int log_s, int p) {
+  return log_s / npass(log_s) + (p < log_s % npass(log_s) ? 1 : 0);
+}
+constexpr int pass_r0(int log_s, int p) {
+  int r = 0;
+  for (int i = 0; i < p; ++i) r += pass_e(log_s, i);
+  return r;
+}
+
+// Four-step split N = N1 * N2 used for log N >= 13 (column stages first).
+constexpr int split_log_n1(int log_n) { return log_n >= 16 ? 8 : (log_n >= 14 ? 7 : 6); }
+
+// Staged twiddle order.  Stage s of a local transform reads 2^s twiddles
+// (per chunk); they are kept at (1 << s) + perm(s, j).  Stages of the last
+// register pass (s >= p_last) hold pair j = (g << rr) | blk (rr = s - p_last,
+// g the thread's group) at (blk << p_last) | g, so the groups of a warp read
+// consecutive pairs.
+constexpr int staged_perm(int log_s, int s, int j) {
+  const int pl = pass_r0(log_s, npass(log_s) - 1);
+  if (s < pl) return j;
+  const int rr = s - pl;
+  return ((j & ((1 << rr) - 1)) << pl) | (j >> rr);
+}
