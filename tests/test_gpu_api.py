@@ -154,3 +154,28 @@ def test_exact_integer_ops(scheme):
         assert bgv.bgv_noise_budget(ctx, ca, sk) > 10
     else:
         assert bfv.noise_budget(ctx, ca, sk) > 10
+
+
+def test_host_batch_pipeline_matches_operators(ck):
+    """host_io.hmult_relin_host_batch (H2D / compute / D2H on three streams)
+    returns the same residues as the operators run one by one."""
+    import torch
+
+    from paper_2503_22227_b200.host_io import CopyStreams, hmult_relin_host_batch
+    from paper_2503_22227_b200.schemes import ckks
+
+    ctx, pk, rlk = ck["ctx"], ck["pk"], ck["rlk"]
+    rng = np.random.default_rng(11)
+    cts = [ckks.ckks_encrypt(ctx, ckks.ckks_encode(ctx, slots(rng)), pk, seeded_rng(20 + i))
+           for i in range(6)]
+    level = cts[0].level
+    hx = torch.stack([c.data.view().cpu() for c in cts[0::2]]).pin_memory()
+    hy = torch.stack([c.data.view().cpu() for c in cts[1::2]]).pin_memory()
+    out = torch.empty_like(hx).pin_memory()
+    streams = CopyStreams.create()
+    for _ in range(2):  # second round reuses pool blocks across streams
+        hmult_relin_host_batch(ctx, hx, hy, cts[0].scale, cts[1].scale, level, rlk, out, streams)
+    torch.cuda.synchronize()
+    for b in range(3):
+        want = ckks.ckks_relinearize(ctx, ckks.ckks_multiply(ctx, cts[2 * b], cts[2 * b + 1]), rlk)
+        assert torch.equal(out[b], want.data.view().cpu())
