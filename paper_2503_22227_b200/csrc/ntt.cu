@@ -43,7 +43,14 @@ constexpr int kRowThreads = 256;
 constexpr int kLogRowTile = 12;
 constexpr int kSplitThreads = 128;
 constexpr int kLogSplitTile = 11;
-constexpr int kSplitMinB = 4;
+#ifndef FHE_SPLIT_MINB
+#define FHE_SPLIT_MINB 6
+#endif
+#ifndef FHE_SPLIT_NBUF
+#define FHE_SPLIT_NBUF 1
+#endif
+constexpr int kSplitMinB = FHE_SPLIT_MINB;
+constexpr int kSplitNBuf = FHE_SPLIT_NBUF;  // tile buffers per CTA (1: occupancy hides loads)
 
 
 
@@ -124,6 +131,7 @@ struct RowsTile {
   static constexpr int NB = S >= TILE ? 1 : (TILE / S > 32 ? 32 : TILE / S);
   static constexpr int THREADS = kRowThreads;
   static constexpr int MINB = 2;
+  static constexpr int NBUF = 2;
   static constexpr int SMEM_WORDS = padded_words(NB * S);
   static constexpr int LOG_CN_OR0 = 0;
   static constexpr long N2 = 1;  // (column tiles only)
@@ -182,6 +190,7 @@ struct ColsTile {
   static constexpr int TILES = N2 / CN;
   static constexpr int THREADS = kSplitThreads;
   static constexpr int MINB = kSplitMinB;
+  static constexpr int NBUF = kSplitNBuf;
   static constexpr int TILE = 1 << kLogSplitTile;
   // padded index: k-rows of CN words + 2, and 2 more per 16 k-rows, so both
   // stride-16 and contiguous-16 groups along k are bank-conflict free
@@ -255,6 +264,7 @@ struct ChunksTile {
   static constexpr int NB = TILE / S;
   static constexpr int THREADS = kSplitThreads;
   static constexpr int MINB = kSplitMinB;
+  static constexpr int NBUF = kSplitNBuf;
   static constexpr int SMEM_WORDS = padded_words(TILE);
   static constexpr int LOG_CN_OR0 = 0;
   static constexpr long N2 = 1;  // (column tiles only)
@@ -841,7 +851,7 @@ __global__ void __launch_bounds__(Tile::THREADS, Tile::MINB)
     ntt_tiles_fp_kernel(const DevChain ch, u64* dst, const u64* src, Tile tl, int ntiles) {
   extern __shared__ __align__(16) u64 smem_raw[];
   constexpr int TWM = STW ? Tile::TWMAX : 0;
-  double2* tw_raw = reinterpret_cast<double2*>(smem_raw + 2 * Tile::SMEM_WORDS);
+  double2* tw_raw = reinterpret_cast<double2*>(smem_raw + Tile::NBUF * Tile::SMEM_WORDS);
   // staged tables: [prime][fwd | inv][N]
   const double2* table = STW ? ch.tws + (FWD ? 0 : ch.tws_dir) : nullptr;
   // contiguous tile range per CTA (keeps the tile order's twiddle locality)
@@ -849,6 +859,24 @@ __global__ void __launch_bounds__(Tile::THREADS, Tile::MINB)
   int t = (int)(((long)blockIdx.x * ntiles) / gridDim.x);
   if (t >= t_end) return;
   Tile cur = tl;
+  if constexpr (Tile::NBUF == 1) {
+    // single buffer: the other resident CTAs overlap this one's loads
+    for (; t < t_end; ++t) {
+      cur.setup(t);
+      if (!cur.valid) continue;
+      if (STW) load_tw(tw_raw, cur, table + 2 * ch.tws_dir * cur.tw_prime());
+      load_tile(smem_raw, cur, src);
+      cp_async_wait_all();
+      __syncthreads();
+      if (FWD)
+        fwd_passes_fp<Tile::LOG_S, 0, IN, OUT, STW>(smem_raw, tw_raw, cur, dst, ch);
+      else
+        inv_passes_fp<Tile::LOG_S, npass(Tile::LOG_S) - 1, IN, OUT, STW>(smem_raw, tw_raw, cur,
+                                                                          dst, ch);
+      __syncthreads();
+    }
+    return;
+  }
   cur.setup(t);
   if (cur.valid) {
     if (STW) load_tw(tw_raw, cur, table + 2 * ch.tws_dir * cur.tw_prime());
@@ -920,8 +948,8 @@ int launch_tiles_fp(const DevChain& ch, u64* dst, const u64* src, const Tile& tl
                     cudaStream_t st) {
   if (ntiles <= 0) return 0;
   const int grid = std::min(ntiles, Tile::MINB * sm_count());
-  constexpr int smem =
-      2 * Tile::SMEM_WORDS * sizeof(u64) + (STW ? 2 * Tile::TWMAX * sizeof(double2) : 0);
+  constexpr int smem = Tile::NBUF * (Tile::SMEM_WORDS * sizeof(u64) +
+                                     (STW ? Tile::TWMAX * sizeof(double2) : 0));
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(ntt_tiles_fp_kernel<Tile, FWD, IN, OUT, STW>,
