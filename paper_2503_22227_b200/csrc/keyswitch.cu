@@ -302,7 +302,7 @@ __global__ void __launch_bounds__(kThreads)
 // canonical [0, q) representative as a double
 __device__ __forceinline__ double fp_pos(double x, double q) { return x < 0.0 ? __dadd_rn(x, q) : x; }
 
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, 3)
     modup_fp_kernel(const DevChain ch, const u64* __restrict__ c, long c_stride,
                     u64* __restrict__ ext, long ext_stride, const int* __restrict__ dig_info,
                     const double2* __restrict__ up_inv, const double2* __restrict__ up_w, int level,
@@ -327,7 +327,7 @@ __global__ void __launch_bounds__(kThreads)
         const double q = ch.qd[s0 + s].x;
         // y_s = [c_s (Q_d/q_s)^-1]_{q_s}, canonical: the conversion is an
         // integer-level formula, so the representative matters
-        y[s] = fp_pos(fp_mulmod((double)cb[(long)(s0 + s) * n + i], up_inv[s0 + s], q), q);
+        y[s] = fp_pos(fp_mulmod(fp_from_u52(cb[(long)(s0 + s) * n + i]), up_inv[s0 + s], q), q);
       }
     }
     int t = 0;
@@ -385,7 +385,7 @@ __global__ void __launch_bounds__(kThreads)
     for (int k = 0; k < kMaxAlpha; ++k) {
       if (k < K) {
         const double p = ch.qd[L + k].x;
-        y[k] = fp_pos(fp_mulmod((double)src[(long)k * n + i], down_inv[k], p), p);
+        y[k] = fp_pos(fp_mulmod(fp_from_u52(src[(long)k * n + i]), down_inv[k], p), p);
       }
     }
     int j = 0;
@@ -447,8 +447,8 @@ __global__ void __launch_bounds__(kThreads)
 #pragma unroll
     for (int di = 0; di < kD; ++di) {
       if (di < D) {
-        const double b = (double)__ldg(key + ((long)(2 * di) * keyL + p) * n + i);
-        const double a = (double)__ldg(key + ((long)(2 * di + 1) * keyL + p) * n + i);
+        const double b = fp_from_u52(__ldg(key + ((long)(2 * di) * keyL + p) * n + i));
+        const double a = fp_from_u52(__ldg(key + ((long)(2 * di + 1) * keyL + p) * n + i));
         kb[di] = make_double2(b, __dmul_rn(b, qd.y));
         ka[di] = make_double2(a, __dmul_rn(a, qd.y));
         const int s0 = sinfo[4 * di], na = sinfo[4 * di + 1], ro = sinfo[4 * di + 2];
@@ -472,7 +472,7 @@ __global__ void __launch_bounds__(kThreads)
 #pragma unroll
         for (int di = 0; di < kD; ++di) {
           if (di < D) {
-            const double x = (double)v[u][di];
+            const double x = fp_from_u52(v[u][di]);
             sb = __dadd_rn(sb, fp_mulmod(x, kb[di], qd.x));
             sa = __dadd_rn(sa, fp_mulmod(x, ka[di], qd.x));
           }
