@@ -21,6 +21,12 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kMaxAlpha = 16;
+#ifndef FHE_INNER_MINB
+#define FHE_INNER_MINB 2
+#endif
+#ifndef FHE_MODUP_U
+#define FHE_MODUP_U 6
+#endif
 
 // Reduce a chain of multiply-accumulates every `chunk` terms so the 128-bit
 // accumulator stays below 2^126 (reduce_fold's domain).
@@ -302,6 +308,9 @@ __global__ void __launch_bounds__(kThreads)
 // canonical [0, q) representative as a double
 __device__ __forceinline__ double fp_pos(double x, double q) { return x < 0.0 ? __dadd_rn(x, q) : x; }
 
+// Per-target constants staged in shared memory; NSM bounds the digit size
+// (registers), U targets are accumulated at once (independent FP64 chains).
+template <int NSM, int U>
 __global__ void __launch_bounds__(kThreads, 3)
     modup_fp_kernel(const DevChain ch, const u64* __restrict__ c, long c_stride,
                     u64* __restrict__ ext, long ext_stride, const int* __restrict__ dig_info,
@@ -312,7 +321,12 @@ __global__ void __launch_bounds__(kThreads, 3)
   const int row_off = dig_info[4 * di + 2], w_off = dig_info[4 * di + 3];
   const int nt = level + K - na;
   extern __shared__ double2 swd[];
+  double2* tq = swd + na * nt;  // (p, 1/p) of each target
   for (int i = threadIdx.x; i < na * nt; i += blockDim.x) swd[i] = up_w[w_off + i];
+  for (int t = threadIdx.x; t < nt; t += blockDim.x) {
+    const int m = t < s0 ? t : t + na;
+    tq[t] = ch.qd[m < level ? m : L + (m - level)];
+  }
   __syncthreads();
   const int log_n = ch.log_n;
   const long n = 1L << log_n;
@@ -320,9 +334,9 @@ __global__ void __launch_bounds__(kThreads, 3)
   u64* eb = ext + b * ext_stride + (long)row_off * n;
   for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n;
        i += (long)gridDim.x * blockDim.x) {
-    double y[kMaxAlpha];
+    double y[NSM];
 #pragma unroll
-    for (int s = 0; s < kMaxAlpha; ++s) {
+    for (int s = 0; s < NSM; ++s) {
       if (s < na) {
         const double q = ch.qd[s0 + s].x;
         // y_s = [c_s (Q_d/q_s)^-1]_{q_s}, canonical: the conversion is an
@@ -331,47 +345,44 @@ __global__ void __launch_bounds__(kThreads, 3)
       }
     }
     int t = 0;
-    for (; t + 4 <= nt; t += 4) {
-      double acc[4] = {0.0, 0.0, 0.0, 0.0};
-      double pq[4];
+    for (; t + U <= nt; t += U) {
+      double acc[U];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int m = t + u < s0 ? t + u : t + u + na;
-        pq[u] = ch.qd[m < level ? m : L + (m - level)].x;
-      }
+      for (int u = 0; u < U; ++u) acc[u] = 0.0;
 #pragma unroll
-      for (int s = 0; s < kMaxAlpha; ++s) {
+      for (int s = 0; s < NSM; ++s) {
         if (s < na) {
 #pragma unroll
-          for (int u = 0; u < 4; ++u)
-            acc[u] = __dadd_rn(acc[u], fp_mulmod(y[s], swd[s * nt + t + u], pq[u]));
+          for (int u = 0; u < U; ++u)
+            acc[u] = __dadd_rn(acc[u], fp_mulmod(y[s], swd[s * nt + t + u], tq[t + u].x));
         }
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int m = t + u < s0 ? t + u : t + u + na;
-        const double2 qd = ch.qd[m < level ? m : L + (m - level)];
+      for (int u = 0; u < U; ++u) {
+        const double2 qd = tq[t + u];
         eb[(long)(t + u) * n + i] = fp_canon(fp_reduce(acc[u], qd), qd.x);
       }
     }
     for (; t < nt; ++t) {
-      const int m = t < s0 ? t : t + na;
-      const double2 qd = ch.qd[m < level ? m : L + (m - level)];
+      const double2 qd = tq[t];
       double acc = 0.0;
 #pragma unroll
-      for (int s = 0; s < kMaxAlpha; ++s)
+      for (int s = 0; s < NSM; ++s)
         if (s < na) acc = __dadd_rn(acc, fp_mulmod(y[s], swd[s * nt + t], qd.x));
       eb[(long)t * n + i] = fp_canon(fp_reduce(acc, qd), qd.x);
     }
   }
 }
 
-__global__ void __launch_bounds__(kThreads)
+template <int NSM, int U>
+__global__ void __launch_bounds__(kThreads, 3)
     moddown_conv_fp_kernel(const DevChain ch, const u64* __restrict__ accP,
                            u64* __restrict__ conv, const double2* __restrict__ down_inv,
                            const double2* __restrict__ down_w, int level, int K, int L) {
   extern __shared__ double2 swd[];
+  double2* tq = swd + K * level;  // (q, 1/q) of each target
   for (int i = threadIdx.x; i < K * level; i += blockDim.x) swd[i] = down_w[i];
+  for (int j = threadIdx.x; j < level; j += blockDim.x) tq[j] = ch.qd[j];
   __syncthreads();
   const int bp = blockIdx.y;
   const int log_n = ch.log_n;
@@ -380,36 +391,38 @@ __global__ void __launch_bounds__(kThreads)
   u64* dst = conv + (long)bp * level * n;
   for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n;
        i += (long)gridDim.x * blockDim.x) {
-    double y[kMaxAlpha];
+    double y[NSM];
 #pragma unroll
-    for (int k = 0; k < kMaxAlpha; ++k) {
+    for (int k = 0; k < NSM; ++k) {
       if (k < K) {
         const double p = ch.qd[L + k].x;
         y[k] = fp_pos(fp_mulmod(fp_from_u52(src[(long)k * n + i]), down_inv[k], p), p);
       }
     }
     int j = 0;
-    for (; j + 4 <= level; j += 4) {
-      double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    for (; j + U <= level; j += U) {
+      double acc[U];
 #pragma unroll
-      for (int k = 0; k < kMaxAlpha; ++k) {
+      for (int u = 0; u < U; ++u) acc[u] = 0.0;
+#pragma unroll
+      for (int k = 0; k < NSM; ++k) {
         if (k < K) {
 #pragma unroll
-          for (int u = 0; u < 4; ++u)
-            acc[u] = __dadd_rn(acc[u], fp_mulmod(y[k], swd[k * level + j + u], ch.qd[j + u].x));
+          for (int u = 0; u < U; ++u)
+            acc[u] = __dadd_rn(acc[u], fp_mulmod(y[k], swd[k * level + j + u], tq[j + u].x));
         }
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const double2 qd = ch.qd[j + u];
+      for (int u = 0; u < U; ++u) {
+        const double2 qd = tq[j + u];
         dst[(long)(j + u) * n + i] = fp_canon(fp_reduce(acc[u], qd), qd.x);
       }
     }
     for (; j < level; ++j) {
-      const double2 qd = ch.qd[j];
+      const double2 qd = tq[j];
       double acc = 0.0;
 #pragma unroll
-      for (int k = 0; k < kMaxAlpha; ++k)
+      for (int k = 0; k < NSM; ++k)
         if (k < K) acc = __dadd_rn(acc, fp_mulmod(y[k], swd[k * level + j], qd.x));
       dst[(long)j * n + i] = fp_canon(fp_reduce(acc, qd), qd.x);
     }
@@ -420,7 +433,7 @@ __global__ void __launch_bounds__(kThreads)
 // the key words are variable operands, so their quotient estimates key/p
 // are formed on the fly (one DMUL); each term is an exact fp_mulmod, the
 // digit sum (|.| <= 4 * 0.75 p) is reduced once.
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, FHE_INNER_MINB)
     ks_inner_fp_kernel(const DevChain ch, const u64* __restrict__ d, long d_stride,
                        const u64* __restrict__ ext, long ext_stride, const u64* __restrict__ key,
                        int keyL, const int* __restrict__ dig_info, int D, int level, int K, int L,
@@ -553,13 +566,18 @@ int run_keyswitch(const FheContext& ctx, int level, const u64* d, long d_stride,
     const size_t smem = (size_t)max_w * sizeof(u64);
     dim3 grid((unsigned)std::max<long>(1, std::min<long>(n / kThreads, 1024)), lp.digits, batch);
     if (ch.fp64_ok && lp.up_w_d) {
-      const size_t smem_d = (size_t)max_w * sizeof(double2);
-      if (smem_d > 48 * 1024)
-        cudaFuncSetAttribute(modup_fp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem_d);
-      modup_fp_kernel<<<grid, kThreads, smem_d, st>>>(ch, c, (long)level * n, ext,
-                                                      (long)lp.ext_rows * n, lp.dig_info,
-                                                      lp.up_inv_d, lp.up_w_d, level, K, L);
+      int max_na = 0;
+      for (int di = 0; di < lp.digits; ++di) max_na = std::max(max_na, lp.dig_na[di]);
+      const size_t smem_d = ((size_t)max_w + level + K) * sizeof(double2);
+      auto go = [&](auto kern) {
+        if (smem_d > 48 * 1024)
+          cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_d);
+        kern<<<grid, kThreads, smem_d, st>>>(ch, c, (long)level * n, ext, (long)lp.ext_rows * n,
+                                             lp.dig_info, lp.up_inv_d, lp.up_w_d, level, K, L);
+      };
+      if (max_na <= 4) go(modup_fp_kernel<4, FHE_MODUP_U>);
+      else if (max_na <= 12) go(modup_fp_kernel<12, FHE_MODUP_U>);
+      else go(modup_fp_kernel<16, FHE_MODUP_U>);
     } else {
       if (smem > 48 * 1024)
         cudaFuncSetAttribute(modup_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -595,10 +613,18 @@ int run_keyswitch(const FheContext& ctx, int level, const u64* d, long d_stride,
   {
     const size_t smem = (size_t)K * level * sizeof(u64);
     dim3 grid((unsigned)std::max<long>(1, std::min<long>(n / kThreads, 1024)), batch * 2);
-    if (ch.fp64_ok && lp.down_w_d)
-      moddown_conv_fp_kernel<<<grid, kThreads, 2 * smem, st>>>(ch, accP, conv, lp.down_inv_d,
-                                                               lp.down_w_d, level, K, L);
-    else
+    if (ch.fp64_ok && lp.down_w_d) {
+      const size_t smem_d = ((size_t)K * level + level) * sizeof(double2);
+      auto go = [&](auto kern) {
+        if (smem_d > 48 * 1024)
+          cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_d);
+        kern<<<grid, kThreads, smem_d, st>>>(ch, accP, conv, lp.down_inv_d, lp.down_w_d, level,
+                                             K, L);
+      };
+      if (K <= 4) go(moddown_conv_fp_kernel<4, FHE_MODUP_U>);
+      else if (K <= 12) go(moddown_conv_fp_kernel<12, FHE_MODUP_U>);
+      else go(moddown_conv_fp_kernel<16, FHE_MODUP_U>);
+    } else
       moddown_conv_kernel<<<grid, kThreads, smem, st>>>(ch, accP, conv, lp.down_inv, lp.down_w,
                                                         level, K, L, chunk);
     FHE_LAUNCH_CHECK();
