@@ -151,9 +151,16 @@ int build_chain(const u64* primes, int count, int log_n, FheChain* ch) {
     if (log_n >= 13) tws.assign(count * 2 * tws_dir, make_double2(0.0, 0.0));
     for (int p = 0; p < count; ++p) {
       const double q = (double)primes[p];
+      // signed representatives |w| <= q/2: |x w / q| <= |x| / 2, so the FP64
+      // butterflies accept inputs up to 2^52 (lazier reductions, ntt.cu)
+      const u64 qi = primes[p];
+      auto sd = [&](u64 w) {
+        const double v = w > qi / 2 ? -(double)(qi - w) : (double)w;
+        return make_double2(v, v / q);
+      };
       for (size_t i = 0; i < n; ++i) {
-        twd[p * n + i] = make_double2((double)tw[p * n + i].w, (double)tw[p * n + i].w / q);
-        itwd[p * n + i] = make_double2((double)itw[p * n + i].w, (double)itw[p * n + i].w / q);
+        twd[p * n + i] = sd(tw[p * n + i].w);
+        itwd[p * n + i] = sd(itw[p * n + i].w);
       }
       qd[p] = make_double2(q, 1.0 / q);
       if (log_n >= 13) {
@@ -174,8 +181,8 @@ int build_chain(const u64* primes, int count, int log_n, FheChain* ch) {
             for (int j = 0; j < (1 << s); ++j)
               put(n1 + ck * s_ + (1u << s) + staged_perm(ls, s, j), ((n1 + ck) << s) + j);
       }
-      nid[p] = make_double2((double)ninv[p].w, (double)ninv[p].w / q);
-      nwd[p] = make_double2((double)ninv_w1[p].w, (double)ninv_w1[p].w / q);
+      nid[p] = sd(ninv[p].w);
+      nwd[p] = sd(ninv_w1[p].w);
     }
   }
   Packer pk;

@@ -129,6 +129,7 @@ struct RowsTile {
   static constexpr int S = 1 << LOG_N;
   static constexpr int TILE = 1 << kLogRowTile;
   static constexpr int NB = S >= TILE ? 1 : (TILE / S > 32 ? 32 : TILE / S);
+  static constexpr int GS0 = 0;  // global stage of local stage 0
   static constexpr int THREADS = kRowThreads;
   static constexpr int MINB = 2;
   static constexpr int NBUF = 2;
@@ -180,6 +181,7 @@ struct RowsTile {
 template <int LOG_N, int LOG_N1>
 struct ColsTile {
   static constexpr int LOG_S = LOG_N1;
+  static constexpr int GS0 = 0;
   static constexpr bool COLS = true;
   static constexpr bool EPI = true;
   static constexpr int N2 = 1 << (LOG_N - LOG_N1);
@@ -259,6 +261,7 @@ struct ColsTile {
 template <int LOG_N, int LOG_N1>
 struct ChunksTile {
   static constexpr int LOG_S = LOG_N - LOG_N1;
+  static constexpr int GS0 = LOG_N1;
   static constexpr int S = 1 << LOG_S;
   static constexpr int TILE = 1 << kLogSplitTile;
   static constexpr int NB = TILE / S;
@@ -663,9 +666,9 @@ __device__ __forceinline__ void run_pass_fp(u64* sm, const double2* tws, const T
 #pragma unroll
           for (int i = 0; i < half; ++i) {
             const int a = blk * 2 * half + i, c = a + half;
-            // reduce u on odd local stages only: |values| stay <= 2q (< 2^51,
-            // the magic-rounding bound) and every odd stage returns them to <= q
-            const double u = ((R0 + rr) & 1) ? fp_reduce(x[a], qd) : x[a];
+            // signed twiddles take |x| < 2^52 = 4q; bounds grow by 0.75q per
+            // stage from <= 1.25q, so u is reduced on every 4th global stage
+            const double u = ((Tile::GS0 + R0 + rr) & 3) == 3 ? fp_reduce(x[a], qd) : x[a];
             const double t = fp_mulmod(x[c], w, qd.x);
             x[a] = __dadd_rn(u, t);
             x[c] = __dadd_rn(u, -t);
@@ -691,7 +694,10 @@ __device__ __forceinline__ void run_pass_fp(u64* sm, const double2* tws, const T
             const int a = blk * 2 * half + i, c = a + half;
             const double s = __dadd_rn(x[a], x[c]);
             const double d = __dadd_rn(x[a], -x[c]);
-            x[a] = fold ? fp_mulmod(s, sn, qd.x) : fp_reduce(s, qd);
+            // sums double per stage: reduced on even global stages, so the
+            // difference fed to the mulmod stays below 4 * 0.75q < 2^52
+            x[a] = fold ? fp_mulmod(s, sn, qd.x)
+                        : (((Tile::GS0 + R0 + rr) & 1) == 0 ? fp_reduce(s, qd) : s);
             x[c] = fp_mulmod(d, w, qd.x);
           }
         }
