@@ -68,3 +68,35 @@ def test_roundtrip_and_explicit_mod_idx(log_n):
     for r in (0, 5):
         one = NttChain([primes[midx[r]]], n).forward(a[r:r + 1], [0])
         assert one[0].tolist() == f[r].tolist()
+
+
+@pytest.mark.parametrize("log_n", [12, 13, 16])
+def test_extreme_inputs_match_oracle(log_n):
+    """Worst cases for the lazy FP64 butterflies (values grow by up to
+    0.75q per stage between reductions): rows of all q-1, alternating 0/q-1,
+    all 1 and (q-1)/2, at 50-bit primes next to 2^50, forward and inverse
+    against the C oracle."""
+    import torch
+
+    from oracle import fast
+    from paper_2503_22227_b200.coremath.ntt import DeviceChain
+    from paper_2503_22227_b200.coremath.primes import gen_ntt_prime_chain
+
+    n = 1 << log_n
+    primes = [m.value for m in gen_ntt_prime_chain(50, n, 2)]
+    assert all(p > (1 << 49) for p in primes)
+    rows = []
+    for q in primes:
+        rows += [np.full(n, q - 1, np.uint64), np.tile(np.array([0, q - 1], np.uint64), n // 2),
+                 np.ones(n, np.uint64), np.full(n, (q - 1) // 2, np.uint64)]
+    a = np.stack(rows)
+    midx = np.repeat(np.arange(2), 4)
+    ch = DeviceChain(primes, log_n)
+    dev = torch.from_numpy(a.view(np.int64)).cuda()
+    f = dev.clone()
+    ch.transform(f, len(rows), False, mod_idx=midx)
+    i = dev.clone()
+    ch.transform(i, len(rows), True, mod_idx=midx)
+    torch.cuda.synchronize()
+    assert (to_u64(f) == fast.ntt_forward(a, primes, midx)).all()
+    assert (to_u64(i) == fast.ntt_inverse(a, primes, midx)).all()
