@@ -49,8 +49,20 @@ constexpr int kLogSplitTile = 11;
 #ifndef FHE_SPLIT_NBUF
 #define FHE_SPLIT_NBUF 1
 #endif
+#ifndef FHE_CHUNK_MINB
+#define FHE_CHUNK_MINB FHE_SPLIT_MINB
+#endif
+#ifndef FHE_CHUNK_NBUF
+#define FHE_CHUNK_NBUF FHE_SPLIT_NBUF
+#endif
+#ifndef FHE_CHUNK_TWC
+#define FHE_CHUNK_TWC 2
+#endif
 constexpr int kSplitMinB = FHE_SPLIT_MINB;
 constexpr int kSplitNBuf = FHE_SPLIT_NBUF;  // tile buffers per CTA (1: occupancy hides loads)
+constexpr int kChunkMinB = FHE_CHUNK_MINB;
+constexpr int kChunkNBuf = FHE_CHUNK_NBUF;
+constexpr int kChunkTwC = FHE_CHUNK_TWC;    // chunks per tile whose twiddles can be staged
 
 
 
@@ -266,8 +278,8 @@ struct ChunksTile {
   static constexpr int TILE = 1 << kLogSplitTile;
   static constexpr int NB = TILE / S;
   static constexpr int THREADS = kSplitThreads;
-  static constexpr int MINB = kSplitMinB;
-  static constexpr int NBUF = kSplitNBuf;
+  static constexpr int MINB = kChunkMinB;
+  static constexpr int NBUF = kChunkNBuf;
   static constexpr int SMEM_WORDS = padded_words(TILE);
   static constexpr int LOG_CN_OR0 = 0;
   static constexpr long N2 = 1;  // (column tiles only)
@@ -314,7 +326,7 @@ struct ChunksTile {
   }
   // twiddles staged in shared memory per tile (tiles of <= 2 chunks): the
   // C consecutive S-pair chunk blocks of the prime's staged table
-  static constexpr int TWMAX = 2 << LOG_S;
+  static constexpr int TWMAX = kChunkTwC << LOG_S;
   __device__ __forceinline__ int tw_pairs() const { return S << log_c; }
   __device__ __forceinline__ long tw_src_off() const { return N1 + ((long)c0 << LOG_S); }
   __device__ __forceinline__ int tw_base(int s, int m0) const {
@@ -1003,7 +1015,7 @@ int launch_split(const DevChain& ch, const NttArgs& a, bool inverse, bool lazy,
   const int nc = a.rows * C::TILES, nk = kt.plan(a.rows, a.map.limbs);
   ct.limbs_div.init(a.map.limbs);
   // chunk tiles of <= 2 chunks stage their twiddles in shared memory
-  const bool kstage = (K::NB >> kt.log_r) <= 2;
+  const bool kstage = (K::NB >> kt.log_r) <= kChunkTwC;
   int rc;
   if (ch.fp64_ok) {
     if (!inverse) {
