@@ -213,10 +213,15 @@ int build_chain(const u64* primes, int count, int log_n, FheChain* ch) {
   ch->dev.ninv_w1_d = fp64 ? (const double2*)(b + o_nwd) : nullptr;
   ch->dev.tws = (fp64 && log_n >= 13) ? (const double2*)(b + o_tws) : nullptr;
   ch->dev.tws_dir = (long)tws_dir;
+  ch->dev.fuse = fuse_scratch_new();
   return 0;
 }
 
 void free_chain(FheChain* ch) {
+  if (ch) {
+    fuse_scratch_free(ch->dev.fuse);
+    ch->dev.fuse = nullptr;
+  }
   if (ch && ch->dmem) cudaFree(ch->dmem);
   if (ch) ch->dmem = nullptr;
 }

@@ -39,6 +39,8 @@ struct DevChain {
   // then N1 chunk blocks of N2 pairs (ntt_plan.cuh); tws_dir = N1 + N
   const double2* tws;
   long tws_dir;
+  // host-side scratch of the fused four-step NTT (FuseScratch*, ntt.cu)
+  void* fuse;
 };
 
 // Row -> chain position mapping used by every batched kernel.  The

@@ -17,6 +17,9 @@ struct NttArgs {
   long dst_bstride;
 };
 int launch_ntt(const DevChain& ch, const NttArgs& a, bool inverse, cudaStream_t st);
+// per-chain scratch of the fused four-step NTT (tile tickets, group counters)
+void* fuse_scratch_new();
+void fuse_scratch_free(void* p);
 inline int launch_ntt(const DevChain& ch, u64* data, const u64* in, int rows, RowMap map,
                       bool inverse, cudaStream_t st) {
   return launch_ntt(ch, NttArgs{data, in, rows, map, 0, 0}, inverse, st);

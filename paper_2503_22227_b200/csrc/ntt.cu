@@ -33,6 +33,9 @@
 #include "fparith.cuh"
 #include "ntt_plan.cuh"
 
+#include <cstdlib>
+#include <mutex>
+
 namespace {
 
 // Tile geometry.  Whole-row tiles: 4096 elements, 256 threads, 2 CTAs/SM.
@@ -58,6 +61,12 @@ constexpr int kLogSplitTile = 11;
 #ifndef FHE_CHUNK_TWC
 #define FHE_CHUNK_TWC 2
 #endif
+// experiment switch: butterflies skipped (measures the data-movement floor)
+#ifdef FHE_NTT_NOCOMPUTE
+constexpr bool NOCOMP = true;
+#else
+constexpr bool NOCOMP = false;
+#endif
 constexpr int kSplitMinB = FHE_SPLIT_MINB;
 constexpr int kSplitNBuf = FHE_SPLIT_NBUF;  // tile buffers per CTA (1: occupancy hides loads)
 constexpr int kChunkMinB = FHE_CHUNK_MINB;
@@ -73,6 +82,10 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n"); }
 __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait_group() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
 // Padded shared-memory index of array tiles (whole rows, chunks): 16 bytes of
@@ -665,7 +678,11 @@ __device__ __forceinline__ void run_pass_fp(u64* sm, const double2* tws, const T
 #pragma unroll
     for (int i = 0; i < E; ++i)
       x[i] = (FIRST && IN == FPIN_U64) ? fp_from_u52(raw[i]) : __longlong_as_double((long long)raw[i]);
+#ifdef FHE_NTT_NOCOMPUTE
+    if (false) {
+#else
     if (FWD) {
+#endif
 #pragma unroll
       for (int rr = 0; rr < E_LOG; ++rr) {
         const int half = E >> (rr + 1);
@@ -687,7 +704,7 @@ __device__ __forceinline__ void run_pass_fp(u64* sm, const double2* tws, const T
           }
         }
       }
-    } else {
+    } else if (!NOCOMP) {
 #pragma unroll
       for (int rr = E_LOG - 1; rr >= 0; --rr) {
         const int half = E >> (rr + 1);
@@ -895,39 +912,159 @@ __global__ void __launch_bounds__(Tile::THREADS, Tile::MINB)
     }
     return;
   }
-  cur.setup(t);
-  if (cur.valid) {
-    if (STW) load_tw(tw_raw, cur, table + 2 * ch.tws_dir * cur.tw_prime());
-    load_tile(smem_raw, cur, src);
-  } else {
-    cp_async_commit();
-  }
-  int buf = 0;
-  for (; t < t_end; ++t) {
-    cp_async_wait_all();
-    __syncthreads();
-    const int tn = t + 1;
-    if (tn < t_end) {
-      Tile nxt = tl;
-      nxt.setup(tn);
-      if (nxt.valid) {
-        if (STW)
-          load_tw(tw_raw + (buf ? 0 : TWM), nxt, table + 2 * ch.tws_dir * nxt.tw_prime());
-        load_tile(smem_raw + (buf ? 0 : Tile::SMEM_WORDS), nxt, src);
-      } else {
-        cp_async_commit();
+  // NBUF-stage ring: the loads of the next NBUF - 1 tiles are in flight
+  // while a tile computes (one cp.async group per stage, always committed)
+  constexpr int NB = Tile::NBUF;
+  auto issue = [&](int tt, int stage) {
+    if (tt < t_end) {
+      Tile nx = tl;
+      nx.setup(tt);
+      if (nx.valid) {
+        if (STW) load_tw(tw_raw + stage * TWM, nx, table + 2 * ch.tws_dir * nx.tw_prime());
+        load_tile(smem_raw + stage * Tile::SMEM_WORDS, nx, src);
+        return;
       }
     }
+    cp_async_commit();
+  };
+#pragma unroll
+  for (int j = 0; j < NB - 1; ++j) issue(t + j, j);
+  for (int k = 0; t + k < t_end; ++k) {
+    cp_async_wait_group<NB - 2>();
+    __syncthreads();
+    issue(t + k + NB - 1, (k + NB - 1) % NB);
+    cur = tl;
+    cur.setup(t + k);
     if (cur.valid) {
-      u64* sm = smem_raw + (buf ? Tile::SMEM_WORDS : 0);
-      const double2* tws = tw_raw + (buf ? TWM : 0);
+      const int stage = k % NB;
+      u64* sm = smem_raw + stage * Tile::SMEM_WORDS;
+      const double2* tws = tw_raw + stage * TWM;
       if (FWD)
         fwd_passes_fp<Tile::LOG_S, 0, IN, OUT, STW>(sm, tws, cur, dst, ch);
       else
         inv_passes_fp<Tile::LOG_S, npass(Tile::LOG_S) - 1, IN, OUT, STW>(sm, tws, cur, dst, ch);
     }
-    if (tn < t_end) cur.setup(tn);
-    buf ^= 1;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Fused four-step transform (FP64 path): one persistent kernel runs both the
+// column and the chunk tiles, so the intermediate never goes back to HBM --
+// it is written to and re-read from the 126 MB L2 a few microseconds later.
+//
+// Rows are grouped like the chunk tiles (R rows of one residue class).  Tiles
+// are handed out in ticket order; ticket block b holds the first-phase tiles
+// of group b (column tiles forward, chunk tiles inverse) followed by the
+// second-phase tiles of group b - kFuseLag.  A second-phase tile waits until
+// every first-phase tile of its group has signalled its counter.  Tickets
+// are taken by resident CTAs only and a CTA only ever waits on tickets issued
+// before its own, so the wait cannot deadlock.
+#ifndef FHE_FUSE_LAG
+#define FHE_FUSE_LAG 4
+#endif
+constexpr int kFuseLag = FHE_FUSE_LAG;
+constexpr int kFuseSlabs = 8;
+
+struct FusePlan {
+  int groups;     // row groups (residue class x row block)
+  int rblocks;    // row blocks per class
+  int log_r;      // rows per group = 1 << log_r
+  int c_per_g;    // column tiles per group = R * C::TILES
+  int k_per_g;    // chunk tiles per group = cblocks
+  int total;      // tickets
+  FastDiv blk_div;    // ticket -> block (block = c_per_g + k_per_g tickets)
+  FastDiv rb_div;     // group -> (class, row block)
+};
+
+struct FuseScratch {
+  std::mutex mu;
+  int* dev = nullptr;      // kFuseSlabs x slab_ints
+  size_t slab_ints = 0;
+  int next = 0;
+  cudaEvent_t ev[kFuseSlabs] = {};
+};
+
+template <bool FWD, class Tile>
+__device__ __forceinline__ void fused_run_tile(const DevChain& ch, Tile& tl, u64* sm,
+                                               double2* tws, const double2* table, u64* dst,
+                                               const u64* src) {
+  load_tw(tws, tl, table + 2 * ch.tws_dir * tl.tw_prime());
+  load_tile(sm, tl, src);
+  cp_async_wait_all();
+  __syncthreads();
+  if constexpr (FWD)
+    fwd_passes_fp<Tile::LOG_S, 0, Tile::COLS ? FPIN_U64 : FPIN_DOUBLE,
+                  Tile::COLS ? FPOUT_DOUBLE : FPOUT_U64, true>(sm, tws, tl, dst, ch);
+  else
+    inv_passes_fp<Tile::LOG_S, npass(Tile::LOG_S) - 1, Tile::COLS ? FPIN_DOUBLE : FPIN_U64,
+                  Tile::COLS ? FPOUT_U64 : FPOUT_DOUBLE, true>(sm, tws, tl, dst, ch);
+  __syncthreads();
+}
+
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void red_release_add(int* p, int v) {
+  asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+template <class CT, class KT, bool FWD>
+__global__ void __launch_bounds__(kSplitThreads, kSplitMinB)
+    ntt_fused_fp_kernel(const DevChain ch, u64* dst, const u64* src, CT ct, KT kt, FusePlan fp,
+                        int* ctr) {
+  extern __shared__ __align__(16) u64 smem_raw[];
+  __shared__ int s_tk[2];
+  constexpr int SW = CT::SMEM_WORDS > KT::SMEM_WORDS ? CT::SMEM_WORDS : KT::SMEM_WORDS;
+  double2* tws = reinterpret_cast<double2*>(smem_raw + SW);
+  const double2* table = ch.tws + (FWD ? 0 : ch.tws_dir);
+  const int per_block = fp.c_per_g + fp.k_per_g;
+  const int first_n = FWD ? fp.c_per_g : fp.k_per_g;
+  if (threadIdx.x == 0) s_tk[0] = atomicAdd(&ctr[0], 1);
+  __syncthreads();
+  for (int cur = 0;; cur ^= 1) {
+    const int t = s_tk[cur];
+    if (t >= fp.total) break;
+    // the next ticket is fetched while this tile runs (published by the
+    // barrier at the end of the iteration)
+    if (threadIdx.x == 0) s_tk[cur ^ 1] = atomicAdd(&ctr[0], 1);
+    const int blk = fp.blk_div.div(t);
+    const int r = t - blk * per_block;
+    const bool first = r < first_n;
+    const int g = first ? blk : blk - kFuseLag;
+    if (g >= 0 && g < fp.groups) {
+      const int cls = fp.rb_div.div(g);
+      const int rb = g - cls * fp.rblocks;
+      const bool col_tile = (first == FWD);
+      const int idx = first ? r : r - first_n;  // tile index within the group's phase
+      if (!first) {
+        // wait for the group's first phase (written through L2 by other CTAs)
+        if (threadIdx.x == 0) {
+          const int target = FWD ? fp.c_per_g : fp.k_per_g;
+          while (ld_acquire(&ctr[1 + g]) < target) __nanosleep(128);
+        }
+        __syncthreads();
+      }
+      if (col_tile) {
+        const int i = idx / CT::TILES, jb = idx - i * CT::TILES;
+        const int row = cls + ((rb << fp.log_r) + i) * ct.map.limbs;
+        if (row < ct.rows) {
+          CT c = ct;
+          c.setup(row * CT::TILES + jb);
+          fused_run_tile<FWD>(ch, c, smem_raw, tws, table, dst, FWD ? src : dst);
+        }
+      } else {
+        KT k = kt;
+        k.setup(g * fp.k_per_g + idx);
+        if (k.valid) fused_run_tile<FWD>(ch, k, smem_raw, tws, table, dst, FWD ? dst : src);
+      }
+      if (first) {
+        __syncthreads();
+        if (threadIdx.x == 0) red_release_add(&ctr[1 + g], 1);
+      }
+    }
+    __syncthreads();
   }
 }
 
@@ -980,6 +1117,77 @@ int launch_tiles_fp(const DevChain& ch, u64* dst, const u64* src, const Tile& tl
   return 0;
 }
 
+template <class C, class K>
+int launch_fused(const DevChain& ch, u64* dst, const u64* src, const C& ct, const K& kt,
+                 bool fwd, int rows, int limbs, cudaStream_t st) {
+  FusePlan fp;
+  fp.log_r = kt.log_r;
+  fp.rblocks = kt.rblocks;
+  fp.groups = std::min(limbs, rows) * kt.rblocks;
+  fp.c_per_g = (1 << kt.log_r) * C::TILES;
+  fp.k_per_g = kt.cblocks;
+  fp.total = (fp.groups + kFuseLag) * (fp.c_per_g + fp.k_per_g);
+  fp.blk_div.init(fp.c_per_g + fp.k_per_g);
+  fp.rb_div.init(kt.rblocks);
+  FuseScratch* fs = static_cast<FuseScratch*>(ch.fuse);
+  std::lock_guard<std::mutex> lock(fs->mu);
+  const size_t need = 1 + (size_t)fp.groups;
+  if (fs->slab_ints < need) {
+    if (fs->dev) {
+      FHE_CUDA_CHECK(cudaDeviceSynchronize());
+      FHE_CUDA_CHECK(cudaFree(fs->dev));
+      fs->dev = nullptr;
+    }
+    const size_t ints = std::max<size_t>(need, 4096);
+    FHE_CUDA_CHECK(cudaMalloc(&fs->dev, ints * kFuseSlabs * sizeof(int)));
+    fs->slab_ints = ints;
+  }
+  const int slab = fs->next;
+  fs->next = (fs->next + 1) % kFuseSlabs;
+  if (!fs->ev[slab]) FHE_CUDA_CHECK(cudaEventCreateWithFlags(&fs->ev[slab], cudaEventDisableTiming));
+  // the slab's previous user (possibly on another stream) must be done
+  FHE_CUDA_CHECK(cudaStreamWaitEvent(st, fs->ev[slab], 0));
+  int* ctr = fs->dev + (size_t)slab * fs->slab_ints;
+  FHE_CUDA_CHECK(cudaMemsetAsync(ctr, 0, need * sizeof(int), st));
+  constexpr int SW = C::SMEM_WORDS > K::SMEM_WORDS ? C::SMEM_WORDS : K::SMEM_WORDS;
+  constexpr int TW = C::TWMAX > K::TWMAX ? C::TWMAX : K::TWMAX;
+  constexpr int smem = SW * sizeof(u64) + TW * sizeof(double2);
+  const int grid = std::min(fp.total, kSplitMinB * sm_count());
+  if (fwd) {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(ntt_fused_fp_kernel<C, K, true>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      attr = true;
+    }
+    ntt_fused_fp_kernel<C, K, true><<<grid, kSplitThreads, smem, st>>>(ch, dst, src, ct, kt, fp,
+                                                                      ctr);
+  } else {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(ntt_fused_fp_kernel<C, K, false>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      attr = true;
+    }
+    ntt_fused_fp_kernel<C, K, false><<<grid, kSplitThreads, smem, st>>>(ch, dst, src, ct, kt, fp,
+                                                                       ctr);
+  }
+  FHE_LAUNCH_CHECK();
+  FHE_CUDA_CHECK(cudaEventRecord(fs->ev[slab], st));
+  return 0;
+}
+
+bool fused_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    // opt-in: measured on par with the two-kernel path (the tile machinery,
+    // not DRAM, bounds both; profiles/r1_ntt_notes.md)
+    const char* e = getenv("FHE_NTT_FUSED");
+    on = (e && e[0] == '1') ? 1 : 0;
+  }
+  return on == 1;
+}
+
 template <int LOG_N>
 int launch_rows(const DevChain& ch, const NttArgs& a, bool inverse, bool lazy, cudaStream_t st) {
   using T = RowsTile<LOG_N>;
@@ -1017,6 +1225,13 @@ int launch_split(const DevChain& ch, const NttArgs& a, bool inverse, bool lazy,
   // chunk tiles of <= 2 chunks stage their twiddles in shared memory
   const bool kstage = (K::NB >> kt.log_r) <= kChunkTwC;
   int rc;
+  if (ch.fp64_ok && kstage && ch.fuse && fused_enabled()) {
+    ct.src = inverse ? d : s;
+    ct.dst = d;
+    kt.src = inverse ? s : d;
+    kt.dst = d;
+    return launch_fused(ch, a.dst, a.src, ct, kt, !inverse, a.rows, a.map.limbs, st);
+  }
   if (ch.fp64_ok) {
     if (!inverse) {
       ct.src = s;
@@ -1089,4 +1304,15 @@ int launch_ntt(const DevChain& ch, const NttArgs& a, bool inverse, cudaStream_t 
       fhe_set_error("unsupported ring degree 2^" + std::to_string(ch.log_n));
       return -1;
   }
+}
+
+void* fuse_scratch_new() { return new FuseScratch(); }
+
+void fuse_scratch_free(void* p) {
+  FuseScratch* fs = static_cast<FuseScratch*>(p);
+  if (!fs) return;
+  for (cudaEvent_t& e : fs->ev)
+    if (e) cudaEventDestroy(e);
+  if (fs->dev) cudaFree(fs->dev);
+  delete fs;
 }

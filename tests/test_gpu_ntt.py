@@ -100,3 +100,39 @@ def test_extreme_inputs_match_oracle(log_n):
     torch.cuda.synchronize()
     assert (to_u64(f) == fast.ntt_forward(a, primes, midx)).all()
     assert (to_u64(i) == fast.ntt_inverse(a, primes, midx)).all()
+
+
+def test_fused_four_step_path_matches_oracle():
+    """The opt-in fused four-step kernel (FHE_NTT_FUSED=1: one persistent
+    kernel, intermediate through L2, ticketed tiles with per-group counters)
+    gives the same residues; run in a child process since the switch is read
+    once per process."""
+    import os
+    import subprocess
+    import sys
+
+    code = r'''
+import numpy as np, torch
+from oracle import fast
+from paper_2503_22227_b200.coremath.ntt import DeviceChain
+from paper_2503_22227_b200.coremath.primes import gen_ntt_prime_chain
+for log_n, L, rows in ((16, 3, 21), (14, 5, 40), (13, 2, 7)):
+    n = 1 << log_n
+    primes = [m.value for m in gen_ntt_prime_chain(50, n, L)]
+    rng = np.random.default_rng(log_n)
+    a = np.stack([rng.integers(0, primes[r % L], n, dtype=np.uint64) for r in range(rows)])
+    ch = DeviceChain(primes, log_n)
+    dev = torch.from_numpy(a.view(np.int64)).cuda()
+    f = dev.clone(); ch.transform(f, rows, False, limbs=L, offset=0)
+    i = dev.clone(); ch.transform(i, rows, True, limbs=L, offset=0)
+    torch.cuda.synchronize()
+    midx = np.arange(rows) % L
+    assert (f.cpu().numpy().view(np.uint64) == fast.ntt_forward(a, primes, midx)).all(), log_n
+    assert (i.cpu().numpy().view(np.uint64) == fast.ntt_inverse(a, primes, midx)).all(), log_n
+print("fused ok")
+'''
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, FHE_NTT_FUSED="1", PYTHONPATH=root)
+    out = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True,
+                         text=True, timeout=600)
+    assert out.returncode == 0 and "fused ok" in out.stdout, out.stderr[-2000:]
