@@ -26,8 +26,11 @@ def main(path: str, out: str | None = None):
     items = list(launches.values())
     names = [short(x["name"]) for x in items]
     tens = [i for i, n in enumerate(names) if n.startswith("tensor_kernel")]
-    # bench: warm-up (>= 3) + 2 timed steps, each starting with the tensor launch
-    start = tens[-2] if len(tens) >= 2 else 0
+    # the list is either a whole run (warm-up + 2 timed steps + later phases:
+    # take the last two steps before the first non-step kernel) or an
+    # nvtx-filtered "timed/" list (the 2 timed batched steps come first)
+    nvtx_first = "--nvtx-first" in sys.argv
+    start = tens[0] if nvtx_first else (tens[-2] if len(tens) >= 2 else 0)
     end = len(items)
     for i in range(start + 1, len(items)):
         if names[i].startswith("tensor_kernel") and i > tens[-1]:
@@ -48,6 +51,8 @@ def main(path: str, out: str | None = None):
         t = it.get("gpu__time_duration.sum", 0.0) / 1e3
         agg[n] += t
         cnt[n] += 1
+        if seen_tensor == 2 and n.startswith("moddown_finish"):
+            break  # end of the last timed step (the NTT roofline legs follow)
         byt[n] += it.get("dram__bytes_read.sum", 0.0) + it.get("dram__bytes_write.sum", 0.0)
         tot += t
     lines = ["# ncu launch list (gpu__time_duration.sum, --clock-control none; cold-cache and",
@@ -63,4 +68,5 @@ def main(path: str, out: str | None = None):
 
 
 if __name__ == "__main__":
+    sys.argv = [a for a in sys.argv if a != "--nvtx-first"] + (["--nvtx-first"] if "--nvtx-first" in sys.argv else [])
     main(*sys.argv[1:])
