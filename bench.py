@@ -185,6 +185,23 @@ def hmult_relin_step(w, batch: int):
                     out_stride=2 * L * n)
 
 
+# FP64-pipe work of one config-4 HMult+Relin (hybrid dnum=3), lane-operations,
+# counted from the kernels (profiles/r1_ntt_notes.md):
+# 150 forward + 50 inverse N=2^16 limb NTTs, ModUp / ModDown base conversions,
+# key inner product.
+FP64_OPS_PER_HMULT = 150 * 4.98e6 + 50 * 5.5e6 + 476e6 + 136e6 + 317e6
+DFMA_PER_CLK_PER_SM = 57.9  # measured, profiles/r1_microbench_pipes.txt
+
+
+def fp64_bound(ops_s: float, sm_mhz: float | None, sms: int = 148) -> dict:
+    peak = DFMA_PER_CLK_PER_SM * sms * (sm_mhz or 1965.0) * 1e6
+    bound = peak / FP64_OPS_PER_HMULT
+    return {"fp64_lane_ops_per_op": FP64_OPS_PER_HMULT, "peak_lane_ops_s": peak,
+            "bound_ops_s": bound, "frac": ops_s / bound,
+            "note": "HMult+Relin is FP64-pipe bound (200 limb NTTs + base conversions per op); "
+                    "the HBM bound of 420*B per op is ~3.4x higher"}
+
+
 def launches_per_step(level: int) -> int:
     # tensor 1; key switch: INTT 2, ModUp 1, NTT 2, inner 1, INTT(P) 2, conv 1, NTT 2, finish 1
     return 1 + 12
@@ -435,6 +452,7 @@ def main():
                 "forward_gbs": fwd_gbs, "inverse_gbs": inv_gbs, "rows": rows, "N": n},
         "gpu_launches": launches_per_step(LEVELS) * args.steps,
         "clocks": clk.summary(),
+        "fp64_roofline": fp64_bound(ops, clk.summary().get("sm_max_mhz")),
         "decrypt_err_hmult_relin_rescale": decrypt_err,
         "pdq_1024_rows": pdq,
     }
