@@ -53,7 +53,7 @@ constexpr int kLogSplitTile = 11;
 #define FHE_SPLIT_NBUF 1
 #endif
 #ifndef FHE_CHUNK_MINB
-#define FHE_CHUNK_MINB FHE_SPLIT_MINB
+#define FHE_CHUNK_MINB 5
 #endif
 #ifndef FHE_CHUNK_NBUF
 #define FHE_CHUNK_NBUF FHE_SPLIT_NBUF
@@ -69,6 +69,22 @@ constexpr bool NOCOMP = false;
 #endif
 constexpr int kSplitMinB = FHE_SPLIT_MINB;
 constexpr int kSplitNBuf = FHE_SPLIT_NBUF;  // tile buffers per CTA (1: occupancy hides loads)
+#ifndef FHE_COLS_LOG_TILE
+#define FHE_COLS_LOG_TILE 12
+#endif
+#ifndef FHE_COLS_THREADS
+#define FHE_COLS_THREADS kSplitThreads
+#endif
+#ifndef FHE_COLS_MINB
+#define FHE_COLS_MINB 5
+#endif
+constexpr int kColsLogTile = FHE_COLS_LOG_TILE;
+constexpr int kColsThreads = FHE_COLS_THREADS;
+constexpr int kColsMinB = FHE_COLS_MINB;
+#ifndef FHE_CHUNK_LOG_TILE
+#define FHE_CHUNK_LOG_TILE 12
+#endif
+constexpr int kChunkLogTile = FHE_CHUNK_LOG_TILE;
 constexpr int kChunkMinB = FHE_CHUNK_MINB;
 constexpr int kChunkNBuf = FHE_CHUNK_NBUF;
 constexpr int kChunkTwC = FHE_CHUNK_TWC;    // chunks per tile whose twiddles can be staged
@@ -155,6 +171,7 @@ struct RowsTile {
   static constexpr int TILE = 1 << kLogRowTile;
   static constexpr int NB = S >= TILE ? 1 : (TILE / S > 32 ? 32 : TILE / S);
   static constexpr int GS0 = 0;  // global stage of local stage 0
+  static constexpr bool LANE_MAJOR = false;
   static constexpr int THREADS = kRowThreads;
   static constexpr int MINB = 2;
   static constexpr int NBUF = 2;
@@ -211,14 +228,17 @@ struct ColsTile {
   static constexpr bool EPI = true;
   static constexpr int N2 = 1 << (LOG_N - LOG_N1);
   static constexpr long GSTEP_PER_K = N2;
-  static constexpr int LOG_CN = kLogSplitTile - LOG_N1;
+  static constexpr int LOG_CN = kColsLogTile - LOG_N1;
   static constexpr int CN = 1 << LOG_CN;
   static constexpr int LOG_CN_OR0 = LOG_CN;
   static constexpr int TILES = N2 / CN;
-  static constexpr int THREADS = kSplitThreads;
-  static constexpr int MINB = kSplitMinB;
+  static constexpr int THREADS = kColsThreads;
+  static constexpr int MINB = kColsMinB;
   static constexpr int NBUF = kSplitNBuf;
-  static constexpr int TILE = 1 << kLogSplitTile;
+  static constexpr int TILE = 1 << kColsLogTile;
+  // >= 16 columns: lanes run across the columns of a k-row (conflict-free
+  // with any row layout); passes then exchange under __syncthreads
+  static constexpr bool LANE_MAJOR = CN >= 16;
   // padded index: k-rows of CN words + 2, and 2 more per 16 k-rows, so both
   // stride-16 and contiguous-16 groups along k are bank-conflict free
   __device__ static __forceinline__ int pad(int t) {
@@ -257,7 +277,10 @@ struct ColsTile {
   // 8 groups of both columns so its 8-byte shared accesses (serviced per
   // half-warp) hit 16 distinct bank pairs in both passes.
   __device__ __forceinline__ void split(int G, int gpa_log, int& b, int& g) const {
-    if (gpa_log == 4) {
+    if (LANE_MAJOR) {
+      b = G & (CN - 1);
+      g = G >> LOG_CN;
+    } else if (gpa_log == 4) {
       const int lane = G & 31;
       b = ((G >> 5) << 1) + ((lane >> 3) & 1);
       g = ((lane >> 4) << 3) | (lane & 7);
@@ -287,8 +310,9 @@ template <int LOG_N, int LOG_N1>
 struct ChunksTile {
   static constexpr int LOG_S = LOG_N - LOG_N1;
   static constexpr int GS0 = LOG_N1;
+  static constexpr bool LANE_MAJOR = false;
   static constexpr int S = 1 << LOG_S;
-  static constexpr int TILE = 1 << kLogSplitTile;
+  static constexpr int TILE = 1 << kChunkLogTile;
   static constexpr int NB = TILE / S;
   static constexpr int THREADS = kSplitThreads;
   static constexpr int MINB = kChunkMinB;
@@ -321,7 +345,7 @@ struct ChunksTile {
     const int u = t >> log_cb;
     const int cls = rb_div.div(u);
     const int rb = u - cls * rblocks;
-    log_c = kLogSplitTile - LOG_S - log_r;
+    log_c = kChunkLogTile - LOG_S - log_r;
     c0 = cb << log_c;
     const int i0 = rb << log_r;
     const int row0 = cls + i0 * map.limbs;
@@ -636,7 +660,7 @@ __device__ __forceinline__ void run_pass_fp(u64* sm, const double2* tws, const T
   // results of the last pass go back to shared memory and leave in 16-byte
   // coalesced stores (no strided 8-byte STGs from the butterfly registers)
   constexpr bool EPI = Tile::EPI;
-  constexpr bool WL = warp_local(LOG_S);
+  constexpr bool WL = warp_local(LOG_S) && !Tile::LANE_MAJOR;
   // staged twiddles of the last pass are stored transposed (staged_perm)
   constexpr bool TT = STW && R0 == pass_r0(LOG_S, npass(LOG_S) - 1) && TMIN_LOG == 0;
   const int total = tl.arrays() << GPA_LOG;
@@ -773,7 +797,7 @@ __device__ __forceinline__ void fwd_passes_fp(u64* sm, const double2* tws, const
     run_pass_fp<LOG_S, pass_r0(LOG_S, P), pass_e(LOG_S, P), true, P == 0, last, IN, OUT, STW>(
         sm, tws, tl, gout, ch);
     if constexpr (!last) {
-      if constexpr (warp_local(LOG_S)) __syncwarp(); else __syncthreads();
+      if constexpr (warp_local(LOG_S) && !Tile::LANE_MAJOR) __syncwarp(); else __syncthreads();
       fwd_passes_fp<LOG_S, P + 1, IN, OUT, STW>(sm, tws, tl, gout, ch);
     }
   }
@@ -787,7 +811,7 @@ __device__ __forceinline__ void inv_passes_fp(u64* sm, const double2* tws, const
     run_pass_fp<LOG_S, pass_r0(LOG_S, P), pass_e(LOG_S, P), false, P == npass(LOG_S) - 1, last,
                 IN, OUT, STW>(sm, tws, tl, gout, ch);
     if constexpr (!last) {
-      if constexpr (warp_local(LOG_S)) __syncwarp(); else __syncthreads();
+      if constexpr (warp_local(LOG_S) && !Tile::LANE_MAJOR) __syncwarp(); else __syncthreads();
       inv_passes_fp<LOG_S, P - 1, IN, OUT, STW>(sm, tws, tl, gout, ch);
     }
   }
@@ -1225,7 +1249,7 @@ int launch_split(const DevChain& ch, const NttArgs& a, bool inverse, bool lazy,
   // chunk tiles of <= 2 chunks stage their twiddles in shared memory
   const bool kstage = (K::NB >> kt.log_r) <= kChunkTwC;
   int rc;
-  if (ch.fp64_ok && kstage && ch.fuse && fused_enabled()) {
+  if (C::THREADS == K::THREADS && ch.fp64_ok && kstage && ch.fuse && fused_enabled()) {
     ct.src = inverse ? d : s;
     ct.dst = d;
     kt.src = inverse ? s : d;
