@@ -21,8 +21,11 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kMaxAlpha = 16;
+#ifndef FHE_INNER_BU
+#define FHE_INNER_BU 2
+#endif
 #ifndef FHE_INNER_MINB
-#define FHE_INNER_MINB 2
+#define FHE_INNER_MINB 3
 #endif
 #ifndef FHE_MODUP_U
 #define FHE_MODUP_U 6
@@ -433,6 +436,7 @@ __global__ void __launch_bounds__(kThreads, 3)
 // the key words are variable operands, so their quotient estimates key/p
 // are formed on the fly (one DMUL); each term is an exact fp_mulmod, the
 // digit sum (|.| <= 4 * 0.75 p) is reduced once.
+template <int kD>
 __global__ void __launch_bounds__(kThreads, FHE_INNER_MINB)
     ks_inner_fp_kernel(const DevChain ch, const u64* __restrict__ d, long d_stride,
                        const u64* __restrict__ ext, long ext_stride, const u64* __restrict__ key,
@@ -440,7 +444,7 @@ __global__ void __launch_bounds__(kThreads, FHE_INNER_MINB)
                        u64* __restrict__ accQ, u64* __restrict__ accP, const u64* add0,
                        const u64* add1, long add_stride, u64* out0, u64* out1, long out_stride,
                        int batch) {
-  constexpr int kD = 4;
+  // kD: digits (template: registers sized to the key's dnum)
   extern __shared__ int sinfo[];
   for (int i = threadIdx.x; i < 4 * D; i += blockDim.x) sinfo[i] = dig_info[i];
   __syncthreads();
@@ -470,15 +474,15 @@ __global__ void __launch_bounds__(kThreads, FHE_INNER_MINB)
         sstr[di] = own ? d_stride : ext_stride;
       }
     }
-    for (int b0 = 0; b0 < batch; b0 += 4) {
-      u64 v[4][kD];
+    for (int b0 = 0; b0 < batch; b0 += FHE_INNER_BU) {
+      u64 v[FHE_INNER_BU][kD];
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
+      for (int u = 0; u < FHE_INNER_BU; ++u)
 #pragma unroll
         for (int di = 0; di < kD; ++di)
           if (di < D && b0 + u < batch) v[u][di] = __ldg(src[di] + (b0 + u) * sstr[di]);
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < FHE_INNER_BU; ++u) {
         if (b0 + u >= batch) break;
         const int b = b0 + u;
         double sb = 0.0, sa = 0.0;
@@ -596,10 +600,17 @@ int run_keyswitch(const FheContext& ctx, int level, const u64* d, long d_stride,
   // 3. inner product with the key digits (K == 0 writes the result directly)
   {
     const long work = (long)(level + K) << log_n;
-    if (ch.fp64_ok && lp.digits <= 4)
-      ks_inner_fp_kernel<<<grid_for(work), kThreads, 4 * lp.digits * sizeof(int), st>>>(
+    auto go = [&](auto kern) {
+      kern<<<grid_for(work), kThreads, 4 * lp.digits * sizeof(int), st>>>(
           ch, d, d_stride, ext, (long)lp.ext_rows * n, key, L + K, lp.dig_info, lp.digits, level,
           K, L, accQ, accP, add0, add1, add_stride, out0, out1, out_stride, batch);
+    };
+    if (ch.fp64_ok && lp.digits <= 2)
+      go(ks_inner_fp_kernel<2>);
+    else if (ch.fp64_ok && lp.digits == 3)
+      go(ks_inner_fp_kernel<3>);
+    else if (ch.fp64_ok && lp.digits == 4)
+      go(ks_inner_fp_kernel<4>);
     else
       ks_inner_kernel<<<grid_for(work), kThreads, 4 * lp.digits * sizeof(int), st>>>(
           ch, d, d_stride, ext, (long)lp.ext_rows * n, key, L + K, lp.dig_info, lp.digits, level,
