@@ -513,6 +513,66 @@ __global__ void __launch_bounds__(kThreads, FHE_INNER_MINB)
   }
 }
 
+// FP64 key inner product for many digits (the reference's per-prime gadget,
+// alpha = 1, D = level digits): digits stream through one accumulator pair
+// per output, reduced every 8 terms (|sum| <= 8 * 0.75p + p < 2^53).
+__global__ void __launch_bounds__(kThreads)
+    ks_inner_fp_many_kernel(const DevChain ch, const u64* __restrict__ d, long d_stride,
+                            const u64* __restrict__ ext, long ext_stride,
+                            const u64* __restrict__ key, int keyL,
+                            const int* __restrict__ dig_info, int D, int level, int K, int L,
+                            u64* __restrict__ accQ, u64* __restrict__ accP, const u64* add0,
+                            const u64* add1, long add_stride, u64* out0, u64* out1,
+                            long out_stride, int batch) {
+  extern __shared__ int sinfo[];
+  for (int i = threadIdx.x; i < 4 * D; i += blockDim.x) sinfo[i] = dig_info[i];
+  __syncthreads();
+  const int log_n = ch.log_n;
+  const long n = 1L << log_n;
+  const long total = (long)(level + K) << log_n;
+  for (long t = blockIdx.x * (long)blockDim.x + threadIdx.x; t < total;
+       t += (long)gridDim.x * blockDim.x) {
+    const int m = (int)(t >> log_n);
+    const long i = t & (n - 1);
+    const int p = m < level ? m : L + (m - level);
+    const double2 qd = ch.qd[p];
+    const u64 q = ch.mc[p].q;
+    for (int b = 0; b < batch; ++b) {
+      double sb = 0.0, sa = 0.0;
+#pragma unroll 4
+      for (int di = 0; di < D; ++di) {
+        const int s0 = sinfo[4 * di], na = sinfo[4 * di + 1], ro = sinfo[4 * di + 2];
+        const bool own = m >= s0 && m < s0 + na;
+        const u64* src = own ? d + b * d_stride + (long)m * n + i
+                             : ext + b * ext_stride + (long)(ro + (m < s0 ? m : m - na)) * n + i;
+        const double x = fp_from_u52(__ldg(src));
+        const double kbv = fp_from_u52(__ldg(key + ((long)(2 * di) * keyL + p) * n + i));
+        const double kav = fp_from_u52(__ldg(key + ((long)(2 * di + 1) * keyL + p) * n + i));
+        sb = __dadd_rn(sb, fp_mulmod(x, make_double2(kbv, __dmul_rn(kbv, qd.y)), qd.x));
+        sa = __dadd_rn(sa, fp_mulmod(x, make_double2(kav, __dmul_rn(kav, qd.y)), qd.x));
+        if ((di & 7) == 7) {
+          sb = fp_reduce(sb, qd);
+          sa = fp_reduce(sa, qd);
+        }
+      }
+      const u64 rb = fp_canon_half(fp_reduce(sb, qd), qd.x);
+      const u64 ra = fp_canon_half(fp_reduce(sa, qd), qd.x);
+      if (K == 0) {
+        const long o = b * out_stride + (long)m * n + i;
+        const long ai = b * add_stride + (long)m * n + i;
+        out0[o] = add0 ? add_mod(add0[ai], rb, q) : rb;
+        out1[o] = add1 ? add_mod(add1[ai], ra, q) : ra;
+      } else if (m < level) {
+        accQ[((long)(b * 2 + 0) * level + m) * n + i] = rb;
+        accQ[((long)(b * 2 + 1) * level + m) * n + i] = ra;
+      } else {
+        accP[((long)(b * 2 + 0) * K + (m - level)) * n + i] = rb;
+        accP[((long)(b * 2 + 1) * K + (m - level)) * n + i] = ra;
+      }
+    }
+  }
+}
+
 int mac_chunk(const std::vector<u64>& primes) {
   u64 mx = 0;
   for (u64 p : primes) mx = p > mx ? p : mx;
@@ -611,6 +671,8 @@ int run_keyswitch(const FheContext& ctx, int level, const u64* d, long d_stride,
       go(ks_inner_fp_kernel<3>);
     else if (ch.fp64_ok && lp.digits == 4)
       go(ks_inner_fp_kernel<4>);
+    else if (ch.fp64_ok)
+      go(ks_inner_fp_many_kernel);
     else
       ks_inner_kernel<<<grid_for(work), kThreads, 4 * lp.digits * sizeof(int), st>>>(
           ch, d, d_stride, ext, (long)lp.ext_rows * n, key, L + K, lp.dig_info, lp.digits, level,
