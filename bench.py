@@ -202,6 +202,61 @@ def fp64_bound(ops_s: float, sm_mhz: float | None, sms: int = 148) -> dict:
                     "the HBM bound of 420*B per op is ~3.4x higher"}
 
 
+def rotate_rescale_legs(w, batch: int, steps: int, warmup: int, world: int):
+    """Config-4 Rotate (Galois automorphism + hybrid key switch with the step-1
+    Galois key) and Rescale throughput over B resident ciphertexts, each leg
+    checked against the public API (ckks_rotate / ckks_rescale) on item 0.
+    Algorithmic bytes per op: rotate 360*B, rescale 118*B."""
+    import torch
+
+    from paper_2503_22227_b200 import _native
+    from paper_2503_22227_b200.coremath.sampling import Rng
+    from paper_2503_22227_b200.keys import galois_keygen, key_switch_into
+    from paper_2503_22227_b200.schemes import ckks
+
+    ctx, lib = w["ctx"], _native.lib()
+    L, n = LEVELS, ctx.n
+    gks = galois_keygen(ctx, w["sk"], [1], Rng((45).to_bytes(32, "little")))
+    elt = ctx.galois_elt_for_step(1)
+    ksk = gks.for_elt(elt)
+    X = w["X"]
+    P = torch.empty_like(X)
+    R = torch.empty_like(X)
+
+    def rot():
+        _native.check(lib.fhe_automorph(P.data_ptr(), X.data_ptr(), batch * 2 * L, ctx.log_n, elt,
+                                        _native.stream_handle()), "fhe_automorph")
+        key_switch_into(ctx, L, P[:, 1], ksk, R[:, 0], R[:, 1], add0=P[:, 0], batch=batch,
+                        d_stride=2 * L * n, add_stride=2 * L * n, out_stride=2 * L * n)
+
+    S = torch.empty((batch, 2, L - 1, n), dtype=torch.int64, device="cuda")
+    ws_bytes = lib.fhe_rescale_workspace(ctx.handle, 2 * batch, L)
+    ws = ctx.workspace(ws_bytes, "rescale")
+
+    def resc():
+        _native.check(lib.fhe_rescale(ctx.handle, S.data_ptr(), X.data_ptr(), 2 * batch, L, 0,
+                                      ws.data_ptr(), ws_bytes, _native.stream_handle()),
+                      "fhe_rescale")
+
+    rot_ms = max_over_ranks(time_steps(rot, steps, warmup, world), world)
+    resc_ms = max_over_ranks(time_steps(resc, steps, warmup, world), world)
+    want = ckks.ckks_rotate(ctx, w["cx"], 1, gks)
+    if not torch.equal(R[0], want.data.view()):
+        raise AssertionError("batched rotate differs from ckks_rotate")
+    want = ckks.ckks_rescale(ctx, w["cx"])
+    if not torch.equal(S[0], want.data.view()):
+        raise AssertionError("batched rescale differs from ckks_rescale")
+    peak, _ = _peaks()
+    B = n * 8
+    out = {}
+    for name, ms, per_op in (("rotate", rot_ms, 360 * B), ("rescale", resc_ms, 118 * B)):
+        ops = batch * world / (ms / 1000.0)
+        gbs = ops * per_op / 1e9
+        out[name] = {"ops_s": ops, "ms_per_step": ms, "algorithmic_bytes_per_op": per_op,
+                     "achieved_gbs": gbs, "hbm_frac": gbs / peak}
+    return out
+
+
 def launches_per_step(level: int) -> int:
     # tensor 1; key switch: INTT 2, ModUp 1, NTT 2, inner 1, INTT(P) 2, conv 1, NTT 2, finish 1
     return 1 + 12
@@ -398,6 +453,9 @@ def main():
     if not torch.equal(w["OUT"][0], ref.data.view()):
         raise AssertionError("batched step differs from the public API result")
 
+    # config-4 Rotate and Rescale throughput (same resident batch)
+    legs = rotate_rescale_legs(w, B, max(4, args.steps // 2), 3, world)
+
     # end to end through the public API with host buffers
     L, n = LEVELS, 1 << N_LOG
     host_in = torch.empty((B, 2, 2, L, n), dtype=torch.int64).pin_memory()
@@ -455,6 +513,8 @@ def main():
         "fp64_roofline": fp64_bound(ops, clk.summary().get("sm_max_mhz")),
         "decrypt_err_hmult_relin_rescale": decrypt_err,
         "pdq_1024_rows": pdq,
+        "config4_rotate": legs["rotate"],
+        "config4_rescale": legs["rescale"],
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline_hmult()
