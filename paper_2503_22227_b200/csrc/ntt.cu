@@ -919,8 +919,16 @@ __global__ void __launch_bounds__(Tile::THREADS, Tile::MINB)
   if (t >= t_end) return;
   Tile cur = tl;
   if constexpr (Tile::NBUF == 1) {
-    // single buffer: the other resident CTAs overlap this one's loads
+    // single buffer: the other resident CTAs overlap this one's loads.
+    // Round-robin tile order: the CTAs resident at one time work on
+    // consecutive tiles (for column tiles: all column blocks of the same
+    // rows), so HBM sees whole contiguous k-rows at once instead of scattered
+    // 128-byte segments.
+#ifdef FHE_NTT_CONTIG_ORDER
     for (; t < t_end; ++t) {
+#else
+    for (t = blockIdx.x; t < ntiles; t += gridDim.x) {
+#endif
       cur.setup(t);
       if (!cur.valid) continue;
       if (STW) load_tw(tw_raw, cur, table + 2 * ch.tws_dir * cur.tw_prime());
