@@ -33,6 +33,8 @@
 #include "fparith.cuh"
 #include "ntt_plan.cuh"
 
+#include <cuda.h>
+
 #include <cstdlib>
 #include <mutex>
 
@@ -172,6 +174,8 @@ struct RowsTile {
   static constexpr int NB = S >= TILE ? 1 : (TILE / S > 32 ? 32 : TILE / S);
   static constexpr int GS0 = 0;  // global stage of local stage 0
   static constexpr bool LANE_MAJOR = false;
+  static constexpr bool DENSE = false;  // unpadded smem rows (TMA tiles)
+  static constexpr bool TMA = false;
   static constexpr int THREADS = kRowThreads;
   static constexpr int MINB = 2;
   static constexpr int NBUF = 2;
@@ -239,6 +243,8 @@ struct ColsTile {
   // >= 16 columns: lanes run across the columns of a k-row (conflict-free
   // with any row layout); passes then exchange under __syncthreads
   static constexpr bool LANE_MAJOR = CN >= 16;
+  static constexpr bool DENSE = false;
+  static constexpr bool TMA = false;
   // padded index: k-rows of CN words + 2, and 2 more per 16 k-rows, so both
   // stride-16 and contiguous-16 groups along k are bank-conflict free
   __device__ static __forceinline__ int pad(int t) {
@@ -311,6 +317,8 @@ struct ChunksTile {
   static constexpr int LOG_S = LOG_N - LOG_N1;
   static constexpr int GS0 = LOG_N1;
   static constexpr bool LANE_MAJOR = false;
+  static constexpr bool DENSE = false;  // unpadded smem rows (TMA tiles)
+  static constexpr bool TMA = false;
   static constexpr int S = 1 << LOG_S;
   static constexpr int TILE = 1 << kChunkLogTile;
   static constexpr int NB = TILE / S;
@@ -428,7 +436,12 @@ __device__ __forceinline__ void epilogue_store(const u64* sm, const Tile& tl, u6
   constexpr int LOG_S = Tile::LOG_S;
   constexpr int S = 1 << LOG_S;
   constexpr int T = Tile::THREADS;
-  if constexpr (Tile::COLS) {
+  if constexpr (Tile::TMA) {
+    // results are in the dense tile: one bulk tensor store by thread 0
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    if (threadIdx.x == 0) tl.tma_store(sm);
+  } else if constexpr (Tile::COLS) {
     constexpr int CN = 1 << Tile::LOG_CN_OR0;
     constexpr int PPR = CN / 2;
     constexpr int KSTEP = T / PPR;
@@ -486,7 +499,8 @@ __device__ __forceinline__ void run_pass(u64* sm, const Tile& tl, u64* gout,
   constexpr int GPA_LOG = LOG_S - E_LOG;
   constexpr bool VEC = (TMIN_LOG == 0) && !Tile::COLS && E >= 2;
   // padded stride between consecutive elements of the thread (0: not affine)
-  constexpr int PSTEP = pad_step(Tile::COLS ? (1 << Tile::LOG_CN_OR0) : 0, TMIN, E);
+  constexpr int PSTEP = Tile::DENSE ? (Tile::COLS ? TMIN << Tile::LOG_CN_OR0 : TMIN)
+                                    : pad_step(Tile::COLS ? (1 << Tile::LOG_CN_OR0) : 0, TMIN, E);
   const int total = tl.arrays() << GPA_LOG;
   for (int G = threadIdx.x; G < total; G += blockDim.x) {
     int b, g;
@@ -653,7 +667,8 @@ __device__ __forceinline__ void run_pass_fp(u64* sm, const double2* tws, const T
   constexpr int TMIN = 1 << TMIN_LOG;
   constexpr int GPA_LOG = LOG_S - E_LOG;
   constexpr bool VEC = (TMIN_LOG == 0) && !Tile::COLS && E >= 2;
-  constexpr int PSTEP = pad_step(Tile::COLS ? (1 << Tile::LOG_CN_OR0) : 0, TMIN, E);
+  constexpr int PSTEP = Tile::DENSE ? (Tile::COLS ? TMIN << Tile::LOG_CN_OR0 : TMIN)
+                                    : pad_step(Tile::COLS ? (1 << Tile::LOG_CN_OR0) : 0, TMIN, E);
   // twiddles of the whole pass are loaded up front (E - 1 pairs) when they
   // fit the register budget, so their L1/L2 latency overlaps the tile reads
   constexpr bool PRELOAD = !STW && E <= 16;
@@ -980,6 +995,128 @@ __global__ void __launch_bounds__(Tile::THREADS, Tile::MINB)
 }
 
 // ---------------------------------------------------------------------------
+// TMA column tiles (FP64 path, N1 = 256): the [256 k-rows x 16 columns] tile
+// (32 KB, one 128-byte segment per k-row) moves with ONE bulk tensor copy in
+// each direction, issued by one thread and completed on an mbarrier; the
+// twiddle block follows with a 1D bulk copy on the same barrier.  Lanes run
+// across the 16 columns of a k-row, so the dense (unpadded) layout is
+// bank-conflict free in both passes.
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_5d(void* dst, const CUtensorMap* map, int c0, int c1,
+                                            int c2, int c3, int c4, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, "
+      "{%2, %3, %4, %5, %6}], [%7];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_store_5d(const CUtensorMap* map, int c0, int c1, int c2, int c3,
+                                             int c4, const void* src) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4, %5}], [%6];" ::
+          "l"(map),
+      "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(smem_u32(src))
+      : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read0() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait0() {
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+// Column tile moved by TMA.  Rows are addressed as the 5D tensor
+// (16 elements, N2/16 column blocks, N1 k-rows, limbs, batches) so both the
+// contiguous and the batch-strided row layouts map to one box.
+template <int LOG_N, int LOG_N1>
+struct ColsTmaTile : ColsTile<LOG_N, LOG_N1> {
+  using Base = ColsTile<LOG_N, LOG_N1>;
+  static constexpr bool DENSE = true;
+  static constexpr bool TMA = true;
+  static constexpr int SMEM_WORDS = Base::TILE;
+  __device__ static __forceinline__ int pad(int t) { return t; }
+  const CUtensorMap* dmap = nullptr;  // set in-kernel to the __grid_constant__ param
+  int ccol = 0, climb = 0, cbat = 0;  // box coordinates of the tile
+  __device__ __forceinline__ void setup(int t) {
+    Base::setup(t);
+    ccol = this->j0 >> 4;
+    climb = this->row % this->map.limbs;
+    cbat = this->row / this->map.limbs;
+  }
+  __device__ __forceinline__ void tma_store(const u64* sm) const {
+    tma_store_5d(dmap, 0, ccol, 0, climb, cbat, sm);
+  }
+};
+
+template <class Tile, bool FWD, int IN, int OUT>
+__global__ void __launch_bounds__(Tile::THREADS, Tile::MINB)
+    ntt_cols_tma_kernel(const DevChain ch, const __grid_constant__ CUtensorMap smap,
+                        const __grid_constant__ CUtensorMap dmap, Tile tl, int ntiles) {
+  // dynamic smem only (no static smem ahead of it): the TMA box lands at the
+  // 1024-byte aligned window base; the mbarrier sits after the twiddles
+  extern __shared__ __align__(1024) u64 smem_raw[];
+  double2* tws = reinterpret_cast<double2*>(smem_raw + Tile::SMEM_WORDS);
+  uint64_t& bar = *reinterpret_cast<uint64_t*>(tws + Tile::TWMAX);
+  const double2* table = ch.tws + (FWD ? 0 : ch.tws_dir);
+  constexpr unsigned kDataBytes = Tile::SMEM_WORDS * sizeof(u64);
+  constexpr unsigned kTwBytes = Tile::TWMAX * sizeof(double2);
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  unsigned phase = 0;
+  Tile cur = tl;
+  cur.dmap = &dmap;
+  for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    cur.setup(t);
+    if (threadIdx.x == 0) {
+      bulk_wait_read0();  // the previous tile's store has left shared memory
+      mbar_expect_tx(&bar, kDataBytes + kTwBytes);
+      tma_load_5d(smem_raw, &smap, 0, cur.ccol, 0, cur.climb, cur.cbat, &bar);
+      bulk_g2s(tws, table + 2 * ch.tws_dir * cur.tw_prime(), kTwBytes, &bar);
+    }
+    mbar_wait(&bar, phase);
+    phase ^= 1;
+    if (FWD)
+      fwd_passes_fp<Tile::LOG_S, 0, IN, OUT, true>(smem_raw, tws, cur, nullptr, ch);
+    else
+      inv_passes_fp<Tile::LOG_S, npass(Tile::LOG_S) - 1, IN, OUT, true>(smem_raw, tws, cur,
+                                                                        nullptr, ch);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) bulk_wait0();
+}
+
+// ---------------------------------------------------------------------------
 // Fused four-step transform (FP64 path): one persistent kernel runs both the
 // column and the chunk tiles, so the intermediate never goes back to HBM --
 // it is written to and re-read from the 126 MB L2 a few microseconds later.
@@ -1220,6 +1357,76 @@ bool fused_enabled() {
   return on == 1;
 }
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no
+// libcuda link dependency); null when unavailable.
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn encode_tiled() {
+  static EncodeTiledFn fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+bool tma_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("FHE_NTT_TMA");
+    on = (e && e[0] == '0') ? 0 : (encode_tiled() ? 1 : 0);
+  }
+  return on == 1;
+}
+
+// Column-tile view of a row set: (16 elements, N2/16 blocks, N1 k-rows,
+// limbs, batches); row r = batch r / limbs, limb r % limbs.
+bool cols_tensor_map(CUtensorMap* m, const u64* base, int log_n, int log_n1, int limbs,
+                     long bstride, int rows) {
+  const cuuint64_t n = 1ull << log_n, n1 = 1ull << log_n1, n2 = n / n1;
+  const cuuint64_t bs = bstride ? (cuuint64_t)bstride : (cuuint64_t)limbs * n;
+  const cuuint64_t nb = ((cuuint64_t)rows + limbs - 1) / limbs;
+  const cuuint64_t dims[5] = {16, n2 / 16, n1, (cuuint64_t)limbs, nb};
+  const cuuint64_t strides[4] = {128, n2 * 8, n * 8, bs * 8};
+  const cuuint32_t box[5] = {16, 1, (cuuint32_t)n1, 1, 1};
+  const cuuint32_t es[5] = {1, 1, 1, 1, 1};
+  return encode_tiled()(m, CU_TENSOR_MAP_DATA_TYPE_UINT64, 5, const_cast<u64*>(base), dims,
+                        strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <class Tile, bool FWD, int IN, int OUT>
+int launch_cols_tma(const DevChain& ch, u64* dst, const u64* src, const Tile& tl, int ntiles,
+                    long src_bstride, long dst_bstride, cudaStream_t st, bool& done) {
+  done = false;
+  CUtensorMap smap, dmap;
+  if (!cols_tensor_map(&smap, src, ch.log_n, Tile::LOG_S, tl.map.limbs, src_bstride, tl.rows) ||
+      !cols_tensor_map(&dmap, dst, ch.log_n, Tile::LOG_S, tl.map.limbs, dst_bstride, tl.rows))
+    return 0;  // fall back to the cp.async path
+  constexpr int smem = Tile::SMEM_WORDS * sizeof(u64) + Tile::TWMAX * sizeof(double2) + 16;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(ntt_cols_tma_kernel<Tile, FWD, IN, OUT>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr = true;
+  }
+  const int grid = std::min(ntiles, Tile::MINB * sm_count());
+  ntt_cols_tma_kernel<Tile, FWD, IN, OUT><<<grid, Tile::THREADS, smem, st>>>(ch, smap, dmap, tl,
+                                                                             ntiles);
+  FHE_LAUNCH_CHECK();
+  done = true;
+  return 0;
+}
+
 template <int LOG_N>
 int launch_rows(const DevChain& ch, const NttArgs& a, bool inverse, bool lazy, cudaStream_t st) {
   using T = RowsTile<LOG_N>;
@@ -1264,13 +1471,27 @@ int launch_split(const DevChain& ch, const NttArgs& a, bool inverse, bool lazy,
     kt.dst = d;
     return launch_fused(ch, a.dst, a.src, ct, kt, !inverse, a.rows, a.map.limbs, st);
   }
+  // TMA column tiles: N1 = 256 (one 256-k-row box), 16 columns per tile
+  using CT = ColsTmaTile<LOG_N, LOG_N1>;
+  constexpr bool kTmaShape = (LOG_N1 == 8) && (C::CN == 16);
+  const bool use_tma = kTmaShape && ch.fp64_ok && tma_enabled();
   if (ch.fp64_ok) {
     if (!inverse) {
       ct.src = s;
       ct.dst = d;
       kt.src = d;
       kt.dst = d;
-      rc = launch_tiles_fp<C, true, FPIN_U64, FPOUT_DOUBLE, true>(ch, a.dst, a.src, ct, nc, st);
+      bool done = false;
+      if (use_tma) {
+        CT tt;
+        static_cast<C&>(tt) = ct;
+        rc = launch_cols_tma<CT, true, FPIN_U64, FPOUT_DOUBLE>(ch, a.dst, a.src, tt, nc,
+                                                              a.src_bstride, a.dst_bstride, st,
+                                                              done);
+        if (rc) return rc;
+      }
+      if (!done)
+        rc = launch_tiles_fp<C, true, FPIN_U64, FPOUT_DOUBLE, true>(ch, a.dst, a.src, ct, nc, st);
       if (!rc)
         rc = kstage ? launch_tiles_fp<K, true, FPIN_DOUBLE, FPOUT_U64, true>(ch, a.dst, a.dst, kt, nk, st)
                     : launch_tiles_fp<K, true, FPIN_DOUBLE, FPOUT_U64>(ch, a.dst, a.dst, kt, nk, st);
@@ -1281,7 +1502,15 @@ int launch_split(const DevChain& ch, const NttArgs& a, bool inverse, bool lazy,
       ct.dst = d;
       rc = kstage ? launch_tiles_fp<K, false, FPIN_U64, FPOUT_DOUBLE, true>(ch, a.dst, a.src, kt, nk, st)
                   : launch_tiles_fp<K, false, FPIN_U64, FPOUT_DOUBLE>(ch, a.dst, a.src, kt, nk, st);
-      if (!rc)
+      bool done = false;
+      if (!rc && use_tma) {
+        CT tt;
+        static_cast<C&>(tt) = ct;
+        rc = launch_cols_tma<CT, false, FPIN_DOUBLE, FPOUT_U64>(ch, a.dst, a.dst, tt, nc,
+                                                               a.dst_bstride, a.dst_bstride, st,
+                                                               done);
+      }
+      if (!rc && !done)
         rc = launch_tiles_fp<C, false, FPIN_DOUBLE, FPOUT_U64, true>(ch, a.dst, a.dst, ct, nc, st);
     }
     return rc;
