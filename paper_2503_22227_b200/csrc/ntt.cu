@@ -176,6 +176,7 @@ struct RowsTile {
   static constexpr bool LANE_MAJOR = false;
   static constexpr bool DENSE = false;  // unpadded smem rows (TMA tiles)
   static constexpr bool TMA = false;
+  static constexpr bool SWZ = false;   // 128B-swizzled rows (TMA chunk tiles)
   static constexpr int THREADS = kRowThreads;
   static constexpr int MINB = 2;
   static constexpr int NBUF = 2;
@@ -245,6 +246,7 @@ struct ColsTile {
   static constexpr bool LANE_MAJOR = CN >= 16;
   static constexpr bool DENSE = false;
   static constexpr bool TMA = false;
+  static constexpr bool SWZ = false;
   // padded index: k-rows of CN words + 2, and 2 more per 16 k-rows, so both
   // stride-16 and contiguous-16 groups along k are bank-conflict free
   __device__ static __forceinline__ int pad(int t) {
@@ -319,6 +321,7 @@ struct ChunksTile {
   static constexpr bool LANE_MAJOR = false;
   static constexpr bool DENSE = false;  // unpadded smem rows (TMA tiles)
   static constexpr bool TMA = false;
+  static constexpr bool SWZ = false;   // 128B-swizzled rows (TMA chunk tiles)
   static constexpr int S = 1 << LOG_S;
   static constexpr int TILE = 1 << kChunkLogTile;
   static constexpr int NB = TILE / S;
@@ -342,6 +345,7 @@ struct ChunksTile {
   int cblocks = 1;  // chunk blocks per row = N1 / C
   bool valid = true;
   int log_c, c0, p, nb;
+  int cls_ = 0, i0_ = 0;  // residue class and first row ordinal of the tile
   long so, dof, sstep, dstep;  // word offsets of array (0, 0) and the per-row steps
   // Tile order: (residue class, row block, chunk block): consecutive tiles of
   // a CTA share the prime and walk the chunks of the same rows.
@@ -356,6 +360,8 @@ struct ChunksTile {
     log_c = kChunkLogTile - LOG_S - log_r;
     c0 = cb << log_c;
     const int i0 = rb << log_r;
+    cls_ = cls;
+    i0_ = i0;
     const int row0 = cls + i0 * map.limbs;
     valid = row0 < rows;
     if (!valid) return;
@@ -699,7 +705,30 @@ __device__ __forceinline__ void run_pass_fp(u64* sm, const double2* tws, const T
       }
     }
     u64 raw[E];
-    if (VEC) {
+    // 128B-swizzled tiles (TMA chunk tiles, S = 256, radix 16): element t
+    // sits at word t ^ (((t >> 4) & 7) << 1).  Contiguous groups are one
+    // 128-byte row (pair j at unit j ^ row); stride-16 groups take one word
+    // per row, whose xor offset only depends on i & 7 (8 base addresses).
+    const int lin = tl.tile_index(b, base);
+    int swz_off[Tile::SWZ && TMIN_LOG != 0 ? 8 : 1];
+    if constexpr (Tile::SWZ && TMIN_LOG != 0) {
+      static_assert(TMIN == 16, "swizzled tiles: stride-16 or contiguous groups only");
+#pragma unroll
+      for (int c = 0; c < 8; ++c) swz_off[c] = (lin & ~14) + ((lin & 14) ^ (c << 1));
+    }
+    if constexpr (Tile::SWZ && TMIN_LOG == 0) {
+      const int r7 = (lin >> 4) & 7;
+#pragma unroll
+      for (int i = 0; i < E; i += 2) {
+        const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(
+            &sm[(lin & ~15) + ((i & ~15) << 0) + ((((i & 15) >> 1) ^ r7) << 1)]);
+        raw[i] = v.x;
+        raw[i + 1] = v.y;
+      }
+    } else if constexpr (Tile::SWZ) {
+#pragma unroll
+      for (int i = 0; i < E; ++i) raw[i] = sm[swz_off[i & 7] + 16 * i];
+    } else if (VEC) {
 #pragma unroll
       for (int i = 0; i < E; i += 2) {
         const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(&sm[pb + i + ((i >> 4) << 1)]);
@@ -787,7 +816,17 @@ __device__ __forceinline__ void run_pass_fp(u64* sm, const double2* tws, const T
         for (int i = 0; i < E; ++i) o[i * GSTEP] = raw[i];
       }
     } else {
-      if (VEC) {
+      if constexpr (Tile::SWZ && TMIN_LOG == 0) {
+        const int r7 = (lin >> 4) & 7;
+#pragma unroll
+        for (int i = 0; i < E; i += 2)
+          *reinterpret_cast<ulonglong2*>(
+              &sm[(lin & ~15) + (i & ~15) + ((((i & 15) >> 1) ^ r7) << 1)]) =
+              make_ulonglong2(raw[i], raw[i + 1]);
+      } else if constexpr (Tile::SWZ) {
+#pragma unroll
+        for (int i = 0; i < E; ++i) sm[swz_off[i & 7] + 16 * i] = raw[i];
+      } else if (VEC) {
 #pragma unroll
         for (int i = 0; i < E; i += 2)
           *reinterpret_cast<ulonglong2*>(&sm[pb + i + ((i >> 4) << 1)]) = make_ulonglong2(raw[i], raw[i + 1]);
@@ -1046,6 +1085,23 @@ __device__ __forceinline__ void tma_store_5d(const CUtensorMap* map, int c0, int
       : "memory");
   asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, int c0, int c1,
+                                            int c2, int c3, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, "
+      "{%2, %3, %4, %5}], [%6];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_store_4d(const CUtensorMap* map, int c0, int c1, int c2,
+                                             int c3, const void* src) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4}], [%5];" ::
+          "l"(map),
+      "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(src))
+      : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
 __device__ __forceinline__ void bulk_wait_read0() {
   asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
@@ -1063,7 +1119,8 @@ struct ColsTmaTile : ColsTile<LOG_N, LOG_N1> {
   static constexpr bool TMA = true;
   static constexpr int SMEM_WORDS = Base::TILE;
   __device__ static __forceinline__ int pad(int t) { return t; }
-  const CUtensorMap* dmap = nullptr;  // set in-kernel to the __grid_constant__ param
+  const CUtensorMap* smap_p = nullptr;  // the kernel's __grid_constant__ maps
+  const CUtensorMap* dmap_p = nullptr;
   int ccol = 0, climb = 0, cbat = 0;  // box coordinates of the tile
   __device__ __forceinline__ void setup(int t) {
     Base::setup(t);
@@ -1071,23 +1128,49 @@ struct ColsTmaTile : ColsTile<LOG_N, LOG_N1> {
     climb = this->row % this->map.limbs;
     cbat = this->row / this->map.limbs;
   }
+  __device__ __forceinline__ void tma_load(u64* sm, uint64_t* bar) const {
+    tma_load_5d(sm, smap_p, 0, ccol, 0, climb, cbat, bar);
+  }
   __device__ __forceinline__ void tma_store(const u64* sm) const {
-    tma_store_5d(dmap, 0, ccol, 0, climb, cbat, sm);
+    tma_store_5d(dmap_p, 0, ccol, 0, climb, cbat, sm);
+  }
+};
+
+// Chunk tile moved by TMA with the 128B swizzle: R rows of one residue class
+// x C chunks as the box (16 elements, 16 C row segments, 1 limb, R batches)
+// of the 4D view (16, N/16, limbs, batches).  The swizzle keeps both the
+// stride-16 and the contiguous register passes bank-conflict free without
+// padding (run_pass_fp's SWZ addressing).
+template <int LOG_N, int LOG_N1>
+struct ChunksTmaTile : ChunksTile<LOG_N, LOG_N1> {
+  using Base = ChunksTile<LOG_N, LOG_N1>;
+  static constexpr bool DENSE = true;
+  static constexpr bool TMA = true;
+  static constexpr bool SWZ = true;
+  static constexpr int SMEM_WORDS = Base::TILE;
+  __device__ static __forceinline__ int pad(int t) { return t ^ ((t >> 3) & 14); }
+  const CUtensorMap* smap_p = nullptr;
+  const CUtensorMap* dmap_p = nullptr;
+  __device__ __forceinline__ void tma_load(u64* sm, uint64_t* bar) const {
+    tma_load_4d(sm, smap_p, 0, this->c0 << (Base::LOG_S - 4), this->cls_, this->i0_, bar);
+  }
+  __device__ __forceinline__ void tma_store(const u64* sm) const {
+    tma_store_4d(dmap_p, 0, this->c0 << (Base::LOG_S - 4), this->cls_, this->i0_, sm);
   }
 };
 
 template <class Tile, bool FWD, int IN, int OUT>
 __global__ void __launch_bounds__(Tile::THREADS, Tile::MINB)
-    ntt_cols_tma_kernel(const DevChain ch, const __grid_constant__ CUtensorMap smap,
+    ntt_tma_kernel(const DevChain ch, const __grid_constant__ CUtensorMap smap,
                         const __grid_constant__ CUtensorMap dmap, Tile tl, int ntiles) {
   // dynamic smem only (no static smem ahead of it): the TMA box lands at the
   // 1024-byte aligned window base; the mbarrier sits after the twiddles
-  extern __shared__ __align__(1024) u64 smem_raw[];
+  extern __shared__ __align__(1024) u64 tma_smem[];
+  u64* smem_raw = tma_smem;
   double2* tws = reinterpret_cast<double2*>(smem_raw + Tile::SMEM_WORDS);
   uint64_t& bar = *reinterpret_cast<uint64_t*>(tws + Tile::TWMAX);
   const double2* table = ch.tws + (FWD ? 0 : ch.tws_dir);
   constexpr unsigned kDataBytes = Tile::SMEM_WORDS * sizeof(u64);
-  constexpr unsigned kTwBytes = Tile::TWMAX * sizeof(double2);
   if (threadIdx.x == 0) {
     mbar_init(&bar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -1095,14 +1178,17 @@ __global__ void __launch_bounds__(Tile::THREADS, Tile::MINB)
   __syncthreads();
   unsigned phase = 0;
   Tile cur = tl;
-  cur.dmap = &dmap;
+  cur.smap_p = &smap;
+  cur.dmap_p = &dmap;
   for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
     cur.setup(t);
+    if (!cur.valid) continue;
     if (threadIdx.x == 0) {
+      const unsigned tw_bytes = cur.tw_pairs() * sizeof(double2);
       bulk_wait_read0();  // the previous tile's store has left shared memory
-      mbar_expect_tx(&bar, kDataBytes + kTwBytes);
-      tma_load_5d(smem_raw, &smap, 0, cur.ccol, 0, cur.climb, cur.cbat, &bar);
-      bulk_g2s(tws, table + 2 * ch.tws_dir * cur.tw_prime(), kTwBytes, &bar);
+      mbar_expect_tx(&bar, kDataBytes + tw_bytes);
+      cur.tma_load(smem_raw, &bar);
+      bulk_g2s(tws, table + 2 * ch.tws_dir * cur.tw_prime() + cur.tw_src_off(), tw_bytes, &bar);
     }
     mbar_wait(&bar, phase);
     phase ^= 1;
@@ -1404,6 +1490,63 @@ bool cols_tensor_map(CUtensorMap* m, const u64* base, int log_n, int log_n1, int
                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// Chunk-tile view: (16 elements, N/16 row segments, limbs, batches) with the
+// 128B swizzle; box = (16, 16 C, 1, R).
+bool chunks_tensor_map(CUtensorMap* m, const u64* base, int log_n, int log_s, int limbs,
+                       long bstride, int rows, int log_r, int log_c) {
+  const cuuint64_t n = 1ull << log_n;
+  const cuuint64_t bs = bstride ? (cuuint64_t)bstride : (cuuint64_t)limbs * n;
+  const cuuint64_t nb = ((cuuint64_t)rows + limbs - 1) / limbs;
+  const cuuint64_t dims[4] = {16, n / 16, (cuuint64_t)limbs, nb};
+  const cuuint64_t strides[3] = {128, n * 8, bs * 8};
+  const cuuint32_t box[4] = {16, (cuuint32_t)(1u << (log_s - 4 + log_c)), 1, 1u << log_r};
+  const cuuint32_t es[4] = {1, 1, 1, 1};
+  return encode_tiled()(m, CU_TENSOR_MAP_DATA_TYPE_UINT64, 4, const_cast<u64*>(base), dims,
+                        strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <class Tile, bool FWD, int IN, int OUT>
+int launch_chunks_tma(const DevChain& ch, u64* dst, const u64* src, const Tile& tl, int ntiles,
+                      long src_bstride, long dst_bstride, cudaStream_t st, bool& done) {
+  done = false;
+  const int log_c = kChunkLogTile - Tile::LOG_S - tl.log_r;
+  CUtensorMap smap, dmap;
+  if (!chunks_tensor_map(&smap, src, ch.log_n, Tile::LOG_S, tl.map.limbs, src_bstride, tl.rows,
+                         tl.log_r, log_c) ||
+      !chunks_tensor_map(&dmap, dst, ch.log_n, Tile::LOG_S, tl.map.limbs, dst_bstride, tl.rows,
+                         tl.log_r, log_c))
+    return 0;
+  constexpr int smem = Tile::SMEM_WORDS * sizeof(u64) + Tile::TWMAX * sizeof(double2) + 16;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(ntt_tma_kernel<Tile, FWD, IN, OUT>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr = true;
+  }
+  const int grid = std::min(ntiles, Tile::MINB * sm_count());
+  ntt_tma_kernel<Tile, FWD, IN, OUT><<<grid, Tile::THREADS, smem, st>>>(ch, smap, dmap, tl,
+                                                                        ntiles);
+  FHE_LAUNCH_CHECK();
+  done = true;
+  return 0;
+}
+
+template <int LOG_N, int LOG_N1, bool FWD, int IN, int OUT, class K>
+int maybe_chunks_tma(const DevChain& ch, u64* dst, const u64* src, const K& kt, int nk,
+                     long src_bstride, long dst_bstride, cudaStream_t st, bool& done) {
+  done = false;
+  if constexpr (LOG_N - LOG_N1 == 8) {
+    using KT = ChunksTmaTile<LOG_N, LOG_N1>;
+    KT tk;
+    static_cast<K&>(tk) = kt;
+    return launch_chunks_tma<KT, FWD, IN, OUT>(ch, dst, src, tk, nk, src_bstride, dst_bstride, st,
+                                               done);
+  }
+  return 0;
+}
+
 template <class Tile, bool FWD, int IN, int OUT>
 int launch_cols_tma(const DevChain& ch, u64* dst, const u64* src, const Tile& tl, int ntiles,
                     long src_bstride, long dst_bstride, cudaStream_t st, bool& done) {
@@ -1415,12 +1558,12 @@ int launch_cols_tma(const DevChain& ch, u64* dst, const u64* src, const Tile& tl
   constexpr int smem = Tile::SMEM_WORDS * sizeof(u64) + Tile::TWMAX * sizeof(double2) + 16;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(ntt_cols_tma_kernel<Tile, FWD, IN, OUT>,
+    cudaFuncSetAttribute(ntt_tma_kernel<Tile, FWD, IN, OUT>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     attr = true;
   }
   const int grid = std::min(ntiles, Tile::MINB * sm_count());
-  ntt_cols_tma_kernel<Tile, FWD, IN, OUT><<<grid, Tile::THREADS, smem, st>>>(ch, smap, dmap, tl,
+  ntt_tma_kernel<Tile, FWD, IN, OUT><<<grid, Tile::THREADS, smem, st>>>(ch, smap, dmap, tl,
                                                                              ntiles);
   FHE_LAUNCH_CHECK();
   done = true;
@@ -1475,6 +1618,10 @@ int launch_split(const DevChain& ch, const NttArgs& a, bool inverse, bool lazy,
   using CT = ColsTmaTile<LOG_N, LOG_N1>;
   constexpr bool kTmaShape = (LOG_N1 == 8) && (C::CN == 16);
   const bool use_tma = kTmaShape && ch.fp64_ok && tma_enabled();
+  // TMA chunk tiles: 256-point chunks, staged twiddles, and whole batches of
+  // rows (rows % limbs == 0: no box row can fall past the buffer's end)
+  const bool use_ktma = (LOG_N - LOG_N1 == 8) && ch.fp64_ok && kstage && tma_enabled() &&
+                        a.rows % a.map.limbs == 0 && std::getenv("FHE_NTT_KTMA") == nullptr;
   if (ch.fp64_ok) {
     if (!inverse) {
       ct.src = s;
@@ -1492,7 +1639,11 @@ int launch_split(const DevChain& ch, const NttArgs& a, bool inverse, bool lazy,
       }
       if (!done)
         rc = launch_tiles_fp<C, true, FPIN_U64, FPOUT_DOUBLE, true>(ch, a.dst, a.src, ct, nc, st);
-      if (!rc)
+      bool kdone = false;
+      if (!rc && use_ktma)
+        rc = maybe_chunks_tma<LOG_N, LOG_N1, true, FPIN_DOUBLE, FPOUT_U64>(
+            ch, a.dst, a.dst, kt, nk, a.dst_bstride, a.dst_bstride, st, kdone);
+      if (!rc && !kdone)
         rc = kstage ? launch_tiles_fp<K, true, FPIN_DOUBLE, FPOUT_U64, true>(ch, a.dst, a.dst, kt, nk, st)
                     : launch_tiles_fp<K, true, FPIN_DOUBLE, FPOUT_U64>(ch, a.dst, a.dst, kt, nk, st);
     } else {
@@ -1500,8 +1651,14 @@ int launch_split(const DevChain& ch, const NttArgs& a, bool inverse, bool lazy,
       kt.dst = d;
       ct.src = d;
       ct.dst = d;
-      rc = kstage ? launch_tiles_fp<K, false, FPIN_U64, FPOUT_DOUBLE, true>(ch, a.dst, a.src, kt, nk, st)
-                  : launch_tiles_fp<K, false, FPIN_U64, FPOUT_DOUBLE>(ch, a.dst, a.src, kt, nk, st);
+      bool kdone = false;
+      rc = 0;
+      if (use_ktma)
+        rc = maybe_chunks_tma<LOG_N, LOG_N1, false, FPIN_U64, FPOUT_DOUBLE>(
+            ch, a.dst, a.src, kt, nk, a.src_bstride, a.dst_bstride, st, kdone);
+      if (!rc && !kdone)
+        rc = kstage ? launch_tiles_fp<K, false, FPIN_U64, FPOUT_DOUBLE, true>(ch, a.dst, a.src, kt, nk, st)
+                    : launch_tiles_fp<K, false, FPIN_U64, FPOUT_DOUBLE>(ch, a.dst, a.src, kt, nk, st);
       bool done = false;
       if (!rc && use_tma) {
         CT tt;
