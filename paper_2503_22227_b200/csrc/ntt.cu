@@ -80,6 +80,15 @@ constexpr int kSplitNBuf = FHE_SPLIT_NBUF;  // tile buffers per CTA (1: occupanc
 #ifndef FHE_COLS_MINB
 #define FHE_COLS_MINB 5
 #endif
+#ifndef FHE_TMA_STAGES
+#define FHE_TMA_STAGES 1
+#endif
+#ifndef FHE_TMA_COLS_MINB
+#define FHE_TMA_COLS_MINB FHE_COLS_MINB
+#endif
+#ifndef FHE_TMA_CHUNK_MINB
+#define FHE_TMA_CHUNK_MINB FHE_CHUNK_MINB
+#endif
 constexpr int kColsLogTile = FHE_COLS_LOG_TILE;
 constexpr int kColsThreads = FHE_COLS_THREADS;
 constexpr int kColsMinB = FHE_COLS_MINB;
@@ -1115,6 +1124,8 @@ __device__ __forceinline__ void bulk_wait0() {
 template <int LOG_N, int LOG_N1>
 struct ColsTmaTile : ColsTile<LOG_N, LOG_N1> {
   using Base = ColsTile<LOG_N, LOG_N1>;
+  static constexpr int TMA_STAGES = FHE_TMA_STAGES;
+  static constexpr int MINB = FHE_TMA_COLS_MINB;
   static constexpr bool DENSE = true;
   static constexpr bool TMA = true;
   static constexpr int SMEM_WORDS = Base::TILE;
@@ -1144,6 +1155,8 @@ struct ColsTmaTile : ColsTile<LOG_N, LOG_N1> {
 template <int LOG_N, int LOG_N1>
 struct ChunksTmaTile : ChunksTile<LOG_N, LOG_N1> {
   using Base = ChunksTile<LOG_N, LOG_N1>;
+  static constexpr int TMA_STAGES = FHE_TMA_STAGES;
+  static constexpr int MINB = FHE_TMA_CHUNK_MINB;
   static constexpr bool DENSE = true;
   static constexpr bool TMA = true;
   static constexpr bool SWZ = true;
@@ -1162,41 +1175,61 @@ struct ChunksTmaTile : ChunksTile<LOG_N, LOG_N1> {
 template <class Tile, bool FWD, int IN, int OUT>
 __global__ void __launch_bounds__(Tile::THREADS, Tile::MINB)
     ntt_tma_kernel(const DevChain ch, const __grid_constant__ CUtensorMap smap,
-                        const __grid_constant__ CUtensorMap dmap, Tile tl, int ntiles) {
-  // dynamic smem only (no static smem ahead of it): the TMA box lands at the
-  // 1024-byte aligned window base; the mbarrier sits after the twiddles
+                   const __grid_constant__ CUtensorMap dmap, Tile tl, int ntiles) {
+  // dynamic smem only (no static smem ahead of it): the TMA boxes land at
+  // 1024-byte aligned stage bases; twiddles and mbarriers follow the data.
+  // NB stages: thread 0 keeps the next NB - 1 tiles' loads in flight.
+  constexpr int NB = Tile::TMA_STAGES;
   extern __shared__ __align__(1024) u64 tma_smem[];
-  u64* smem_raw = tma_smem;
-  double2* tws = reinterpret_cast<double2*>(smem_raw + Tile::SMEM_WORDS);
-  uint64_t& bar = *reinterpret_cast<uint64_t*>(tws + Tile::TWMAX);
+  double2* tws0 = reinterpret_cast<double2*>(tma_smem + NB * Tile::SMEM_WORDS);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(tws0 + NB * Tile::TWMAX);
   const double2* table = ch.tws + (FWD ? 0 : ch.tws_dir);
   constexpr unsigned kDataBytes = Tile::SMEM_WORDS * sizeof(u64);
   if (threadIdx.x == 0) {
-    mbar_init(&bar, 1);
+    for (int i = 0; i < NB; ++i) mbar_init(&bars[i], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  unsigned phase = 0;
   Tile cur = tl;
   cur.smap_p = &smap;
   cur.dmap_p = &dmap;
-  for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+  // thread 0: issue tile `tt` into stage `s` (invalid / past-the-end: nothing)
+  auto issue = [&](int tt, int s) {
+    if (tt >= ntiles) return;
+    Tile nx = tl;
+    nx.smap_p = &smap;
+    nx.setup(tt);
+    if (!nx.valid) return;
+    const unsigned tw_bytes = nx.tw_pairs() * sizeof(double2);
+    mbar_expect_tx(&bars[s], kDataBytes + tw_bytes);
+    nx.tma_load(tma_smem + s * Tile::SMEM_WORDS, &bars[s]);
+    bulk_g2s(tws0 + s * Tile::TWMAX, table + 2 * ch.tws_dir * nx.tw_prime() + nx.tw_src_off(),
+             tw_bytes, &bars[s]);
+  };
+  const int stride = gridDim.x;
+  if (threadIdx.x == 0)
+    for (int s = 0; s < NB - 1; ++s) issue(blockIdx.x + s * stride, s);
+  unsigned phases = 0;  // bit s: parity of stage s
+  int k = 0;
+  for (int t = blockIdx.x; t < ntiles; t += stride, ++k) {
+    const int s = k % NB;
+    if (threadIdx.x == 0) {
+      // the stage refilled now was last used by tile k - 1: its store must
+      // have left shared memory first
+      bulk_wait_read0();
+      issue(t + (NB - 1) * stride, (k + NB - 1) % NB);
+    }
     cur.setup(t);
     if (!cur.valid) continue;
-    if (threadIdx.x == 0) {
-      const unsigned tw_bytes = cur.tw_pairs() * sizeof(double2);
-      bulk_wait_read0();  // the previous tile's store has left shared memory
-      mbar_expect_tx(&bar, kDataBytes + tw_bytes);
-      cur.tma_load(smem_raw, &bar);
-      bulk_g2s(tws, table + 2 * ch.tws_dir * cur.tw_prime() + cur.tw_src_off(), tw_bytes, &bar);
-    }
-    mbar_wait(&bar, phase);
-    phase ^= 1;
+    mbar_wait(&bars[s], (phases >> s) & 1);
+    phases ^= 1u << s;
+    u64* sm = tma_smem + s * Tile::SMEM_WORDS;
+    const double2* tws = tws0 + s * Tile::TWMAX;
     if (FWD)
-      fwd_passes_fp<Tile::LOG_S, 0, IN, OUT, true>(smem_raw, tws, cur, nullptr, ch);
+      fwd_passes_fp<Tile::LOG_S, 0, IN, OUT, true>(sm, tws, cur, nullptr, ch);
     else
-      inv_passes_fp<Tile::LOG_S, npass(Tile::LOG_S) - 1, IN, OUT, true>(smem_raw, tws, cur,
-                                                                        nullptr, ch);
+      inv_passes_fp<Tile::LOG_S, npass(Tile::LOG_S) - 1, IN, OUT, true>(sm, tws, cur, nullptr,
+                                                                        ch);
     __syncthreads();
   }
   if (threadIdx.x == 0) bulk_wait0();
@@ -1518,7 +1551,8 @@ int launch_chunks_tma(const DevChain& ch, u64* dst, const u64* src, const Tile& 
       !chunks_tensor_map(&dmap, dst, ch.log_n, Tile::LOG_S, tl.map.limbs, dst_bstride, tl.rows,
                          tl.log_r, log_c))
     return 0;
-  constexpr int smem = Tile::SMEM_WORDS * sizeof(u64) + Tile::TWMAX * sizeof(double2) + 16;
+  constexpr int smem =
+      Tile::TMA_STAGES * (Tile::SMEM_WORDS * sizeof(u64) + Tile::TWMAX * sizeof(double2) + 8);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(ntt_tma_kernel<Tile, FWD, IN, OUT>,
@@ -1555,7 +1589,8 @@ int launch_cols_tma(const DevChain& ch, u64* dst, const u64* src, const Tile& tl
   if (!cols_tensor_map(&smap, src, ch.log_n, Tile::LOG_S, tl.map.limbs, src_bstride, tl.rows) ||
       !cols_tensor_map(&dmap, dst, ch.log_n, Tile::LOG_S, tl.map.limbs, dst_bstride, tl.rows))
     return 0;  // fall back to the cp.async path
-  constexpr int smem = Tile::SMEM_WORDS * sizeof(u64) + Tile::TWMAX * sizeof(double2) + 16;
+  constexpr int smem =
+      Tile::TMA_STAGES * (Tile::SMEM_WORDS * sizeof(u64) + Tile::TWMAX * sizeof(double2) + 8);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(ntt_tma_kernel<Tile, FWD, IN, OUT>,
