@@ -39,7 +39,7 @@ def main(path: str, out: str | None = None):
     # stop at the first non key-switch kernel after the last step (e2e / NTT phases)
     agg, cnt, byt = defaultdict(float), defaultdict(int), defaultdict(float)
     tot = 0.0
-    step_kernels = ("tensor_kernel", "ntt_tiles", "modup", "ks_inner", "moddown")
+    step_kernels = ("tensor_kernel", "ntt_tiles", "ntt_tma", "ntt_fused", "modup", "ks_inner", "moddown")
     seen_tensor = 0
     for it, n in zip(items[start:], names[start:]):
         if n.startswith("tensor_kernel"):
