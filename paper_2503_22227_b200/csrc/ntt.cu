@@ -1247,6 +1247,9 @@ __global__ void __launch_bounds__(Tile::THREADS, Tile::MINB)
 // every first-phase tile of its group has signalled its counter.  Tickets
 // are taken by resident CTAs only and a CTA only ever waits on tickets issued
 // before its own, so the wait cannot deadlock.
+#ifndef FHE_FUSE_MIN_LOG_R
+#define FHE_FUSE_MIN_LOG_R 4
+#endif
 #ifndef FHE_FUSE_LAG
 #define FHE_FUSE_LAG 4
 #endif
@@ -1356,6 +1359,124 @@ __global__ void __launch_bounds__(kSplitThreads, kSplitMinB)
   }
 }
 
+// Fused four-step transform on TMA tiles: the ticketed persistent scheme of
+// ntt_fused_fp_kernel with both tile kinds moved by bulk tensor copies.  A
+// first-phase tile signals its group only after its TMA store has completed
+// (cp.async.bulk.wait_group 0, then a release add); a second-phase tile
+// acquires the counter and orders its TMA load after it with a proxy fence.
+// The signal of a CTA's last first-phase tile is flushed before the CTA
+// waits on anything, so no CTA can wait on its own pending signal.
+template <class CT, class KT, bool FWD>
+__global__ void __launch_bounds__(kSplitThreads, 5)
+    ntt_fused_tma_kernel(const DevChain ch, const __grid_constant__ CUtensorMap cs_map,
+                         const __grid_constant__ CUtensorMap cd_map,
+                         const __grid_constant__ CUtensorMap ks_map,
+                         const __grid_constant__ CUtensorMap kd_map, CT ct, KT kt, FusePlan fp,
+                         int* ctr) {
+  extern __shared__ __align__(1024) u64 fused_tma_smem[];
+  u64* sm = fused_tma_smem;
+  constexpr int SW = CT::SMEM_WORDS > KT::SMEM_WORDS ? CT::SMEM_WORDS : KT::SMEM_WORDS;
+  constexpr int TW = CT::TWMAX > KT::TWMAX ? CT::TWMAX : KT::TWMAX;
+  double2* tws = reinterpret_cast<double2*>(sm + SW);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(tws + TW);
+  int* s_tk = reinterpret_cast<int*>(bar + 1);
+  const double2* table = ch.tws + (FWD ? 0 : ch.tws_dir);
+  constexpr unsigned kDataBytes = SW * sizeof(u64);
+  const int per_block = fp.c_per_g + fp.k_per_g;
+  const int first_n = FWD ? fp.c_per_g : fp.k_per_g;
+  int pending = -1;  // group whose counter this CTA still owes (thread 0)
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    s_tk[0] = atomicAdd(&ctr[0], 1);
+  }
+  __syncthreads();
+  unsigned phase = 0;
+  for (int cur = 0;; cur ^= 1) {
+    const int t = s_tk[cur];
+    if (t >= fp.total) break;
+    if (threadIdx.x == 0) {
+      s_tk[cur ^ 1] = atomicAdd(&ctr[0], 1);
+      // previous tile's store: complete (and signalled) before anything else
+      bulk_wait0();
+      if (pending >= 0) {
+        red_release_add(&ctr[1 + pending], 1);
+        pending = -1;
+      }
+    }
+    const int blk = fp.blk_div.div(t);
+    const int r = t - blk * per_block;
+    const bool first = r < first_n;
+    const int g = first ? blk : blk - kFuseLag;
+    bool work = false;
+    if (g >= 0 && g < fp.groups) {
+      const int cls = fp.rb_div.div(g);
+      const int rb = g - cls * fp.rblocks;
+      const bool col_tile = (first == FWD);
+      const int idx = first ? r : r - first_n;
+      if (threadIdx.x == 0 && !first) {
+        const int target = FWD ? fp.c_per_g : fp.k_per_g;
+        while (ld_acquire(&ctr[1 + g]) < target) __nanosleep(128);
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+      }
+      if (col_tile) {
+        const int i = idx / CT::TILES, jb = idx - i * CT::TILES;
+        const int row = cls + ((rb << fp.log_r) + i) * ct.map.limbs;
+        if (row < ct.rows) {
+          CT c = ct;
+          c.smap_p = &cs_map;
+          c.dmap_p = &cd_map;
+          c.setup(row * CT::TILES + jb);
+          if (threadIdx.x == 0) {
+            const unsigned twb = c.tw_pairs() * sizeof(double2);
+            mbar_expect_tx(bar, kDataBytes + twb);
+            c.tma_load(sm, bar);
+            bulk_g2s(tws, table + 2 * ch.tws_dir * c.tw_prime() + c.tw_src_off(), twb, bar);
+          }
+          mbar_wait(bar, phase);
+          phase ^= 1;
+          if (FWD)
+            fwd_passes_fp<CT::LOG_S, 0, FPIN_U64, FPOUT_DOUBLE, true>(sm, tws, c, nullptr, ch);
+          else
+            inv_passes_fp<CT::LOG_S, npass(CT::LOG_S) - 1, FPIN_DOUBLE, FPOUT_U64, true>(
+                sm, tws, c, nullptr, ch);
+          work = true;
+        }
+      } else {
+        KT k = kt;
+        k.smap_p = &ks_map;
+        k.dmap_p = &kd_map;
+        k.setup(g * fp.k_per_g + idx);
+        if (k.valid) {
+          if (threadIdx.x == 0) {
+            const unsigned twb = k.tw_pairs() * sizeof(double2);
+            mbar_expect_tx(bar, kDataBytes + twb);
+            k.tma_load(sm, bar);
+            bulk_g2s(tws, table + 2 * ch.tws_dir * k.tw_prime() + k.tw_src_off(), twb, bar);
+          }
+          mbar_wait(bar, phase);
+          phase ^= 1;
+          if (FWD)
+            fwd_passes_fp<KT::LOG_S, 0, FPIN_DOUBLE, FPOUT_U64, true>(sm, tws, k, nullptr, ch);
+          else
+            inv_passes_fp<KT::LOG_S, npass(KT::LOG_S) - 1, FPIN_U64, FPOUT_DOUBLE, true>(
+                sm, tws, k, nullptr, ch);
+          work = true;
+        }
+      }
+      if (first && threadIdx.x == 0) {
+        if (work) pending = g;  // signalled once the store has completed
+        else red_release_add(&ctr[1 + g], 1);
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    bulk_wait0();
+    if (pending >= 0) red_release_add(&ctr[1 + pending], 1);
+  }
+}
+
 int g_sm_count = 0;
 int sm_count() {
   if (!g_sm_count) {
@@ -1405,38 +1526,61 @@ int launch_tiles_fp(const DevChain& ch, u64* dst, const u64* src, const Tile& tl
   return 0;
 }
 
-template <class C, class K>
-int launch_fused(const DevChain& ch, u64* dst, const u64* src, const C& ct, const K& kt,
-                 bool fwd, int rows, int limbs, cudaStream_t st) {
+// Counters of one fused launch: a slab of the chain's scratch, zeroed on the
+// stream after the slab's previous user (any stream) has finished.
+int* fuse_slab(const DevChain& ch, size_t need, cudaStream_t st, int& slab) {
+  FuseScratch* fs = static_cast<FuseScratch*>(ch.fuse);
+  std::lock_guard<std::mutex> lock(fs->mu);
+  if (fs->slab_ints < need) {
+    if (fs->dev) {
+      if (cudaDeviceSynchronize() != cudaSuccess || cudaFree(fs->dev) != cudaSuccess) return nullptr;
+      fs->dev = nullptr;
+    }
+    const size_t ints = std::max<size_t>(need, 4096);
+    if (cudaMalloc(&fs->dev, ints * kFuseSlabs * sizeof(int)) != cudaSuccess) return nullptr;
+    fs->slab_ints = ints;
+  }
+  slab = fs->next;
+  fs->next = (fs->next + 1) % kFuseSlabs;
+  if (!fs->ev[slab] && cudaEventCreateWithFlags(&fs->ev[slab], cudaEventDisableTiming) != cudaSuccess)
+    return nullptr;
+  if (cudaStreamWaitEvent(st, fs->ev[slab], 0) != cudaSuccess) return nullptr;
+  int* ctr = fs->dev + (size_t)slab * fs->slab_ints;
+  if (cudaMemsetAsync(ctr, 0, need * sizeof(int), st) != cudaSuccess) return nullptr;
+  return ctr;
+}
+
+int fuse_release(const DevChain& ch, int slab, cudaStream_t st) {
+  FuseScratch* fs = static_cast<FuseScratch*>(ch.fuse);
+  std::lock_guard<std::mutex> lock(fs->mu);
+  FHE_CUDA_CHECK(cudaEventRecord(fs->ev[slab], st));
+  return 0;
+}
+
+template <class K>
+FusePlan make_fuse_plan(const K& kt, int cols_tiles_per_row, int rows, int limbs) {
   FusePlan fp;
   fp.log_r = kt.log_r;
   fp.rblocks = kt.rblocks;
   fp.groups = std::min(limbs, rows) * kt.rblocks;
-  fp.c_per_g = (1 << kt.log_r) * C::TILES;
+  fp.c_per_g = (1 << kt.log_r) * cols_tiles_per_row;
   fp.k_per_g = kt.cblocks;
   fp.total = (fp.groups + kFuseLag) * (fp.c_per_g + fp.k_per_g);
   fp.blk_div.init(fp.c_per_g + fp.k_per_g);
   fp.rb_div.init(kt.rblocks);
-  FuseScratch* fs = static_cast<FuseScratch*>(ch.fuse);
-  std::lock_guard<std::mutex> lock(fs->mu);
-  const size_t need = 1 + (size_t)fp.groups;
-  if (fs->slab_ints < need) {
-    if (fs->dev) {
-      FHE_CUDA_CHECK(cudaDeviceSynchronize());
-      FHE_CUDA_CHECK(cudaFree(fs->dev));
-      fs->dev = nullptr;
-    }
-    const size_t ints = std::max<size_t>(need, 4096);
-    FHE_CUDA_CHECK(cudaMalloc(&fs->dev, ints * kFuseSlabs * sizeof(int)));
-    fs->slab_ints = ints;
+  return fp;
+}
+
+template <class C, class K>
+int launch_fused(const DevChain& ch, u64* dst, const u64* src, const C& ct, const K& kt,
+                 bool fwd, int rows, int limbs, cudaStream_t st) {
+  const FusePlan fp = make_fuse_plan(kt, C::TILES, rows, limbs);
+  int slab = 0;
+  int* ctr = fuse_slab(ch, 1 + (size_t)fp.groups, st, slab);
+  if (!ctr) {
+    fhe_set_error("fused NTT scratch setup failed");
+    return -2;
   }
-  const int slab = fs->next;
-  fs->next = (fs->next + 1) % kFuseSlabs;
-  if (!fs->ev[slab]) FHE_CUDA_CHECK(cudaEventCreateWithFlags(&fs->ev[slab], cudaEventDisableTiming));
-  // the slab's previous user (possibly on another stream) must be done
-  FHE_CUDA_CHECK(cudaStreamWaitEvent(st, fs->ev[slab], 0));
-  int* ctr = fs->dev + (size_t)slab * fs->slab_ints;
-  FHE_CUDA_CHECK(cudaMemsetAsync(ctr, 0, need * sizeof(int), st));
   constexpr int SW = C::SMEM_WORDS > K::SMEM_WORDS ? C::SMEM_WORDS : K::SMEM_WORDS;
   constexpr int TW = C::TWMAX > K::TWMAX ? C::TWMAX : K::TWMAX;
   constexpr int smem = SW * sizeof(u64) + TW * sizeof(double2);
@@ -1461,8 +1605,16 @@ int launch_fused(const DevChain& ch, u64* dst, const u64* src, const C& ct, cons
                                                                        ctr);
   }
   FHE_LAUNCH_CHECK();
-  FHE_CUDA_CHECK(cudaEventRecord(fs->ev[slab], st));
-  return 0;
+  return fuse_release(ch, slab, st);
+}
+
+bool fused_tma_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("FHE_NTT_FUSED_TMA");
+    on = (e && e[0] == '0') ? 0 : 1;
+  }
+  return on == 1;
 }
 
 bool fused_enabled() {
@@ -1567,6 +1719,51 @@ int launch_chunks_tma(const DevChain& ch, u64* dst, const u64* src, const Tile& 
   return 0;
 }
 
+template <class CT, class KT>
+int launch_fused_tma(const DevChain& ch, u64* dst, const u64* src, const CT& ct, const KT& kt,
+                     bool fwd, long src_bstride, long dst_bstride, int rows, int limbs,
+                     cudaStream_t st, bool& done) {
+  done = false;
+  const int log_c = kChunkLogTile - KT::LOG_S - kt.log_r;
+  // forward: columns read src, chunks work in place on dst; inverse: chunks
+  // read src, columns work in place on dst
+  CUtensorMap cs, cd, ks, kd;
+  const u64* col_src = fwd ? src : dst;
+  const u64* chk_src = fwd ? dst : src;
+  const long col_sb = fwd ? src_bstride : dst_bstride, chk_sb = fwd ? dst_bstride : src_bstride;
+  if (!cols_tensor_map(&cs, col_src, ch.log_n, CT::LOG_S, limbs, col_sb, rows) ||
+      !cols_tensor_map(&cd, dst, ch.log_n, CT::LOG_S, limbs, dst_bstride, rows) ||
+      !chunks_tensor_map(&ks, chk_src, ch.log_n, KT::LOG_S, limbs, chk_sb, rows, kt.log_r, log_c) ||
+      !chunks_tensor_map(&kd, dst, ch.log_n, KT::LOG_S, limbs, dst_bstride, rows, kt.log_r, log_c))
+    return 0;
+  const FusePlan fp = make_fuse_plan(kt, CT::TILES, rows, limbs);
+  int slab = 0;
+  int* ctr = fuse_slab(ch, 1 + (size_t)fp.groups, st, slab);
+  if (!ctr) {
+    fhe_set_error("fused NTT scratch setup failed");
+    return -2;
+  }
+  constexpr int SW = CT::SMEM_WORDS > KT::SMEM_WORDS ? CT::SMEM_WORDS : KT::SMEM_WORDS;
+  constexpr int TW = CT::TWMAX > KT::TWMAX ? CT::TWMAX : KT::TWMAX;
+  constexpr int smem = SW * sizeof(u64) + TW * sizeof(double2) + 16;
+  const int grid = std::min(fp.total, 5 * sm_count());
+  auto go = [&](auto kern) {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      attr = true;
+    }
+    kern<<<grid, kSplitThreads, smem, st>>>(ch, cs, cd, ks, kd, ct, kt, fp, ctr);
+  };
+  if (fwd)
+    go(ntt_fused_tma_kernel<CT, KT, true>);
+  else
+    go(ntt_fused_tma_kernel<CT, KT, false>);
+  FHE_LAUNCH_CHECK();
+  done = true;
+  return fuse_release(ch, slab, st);
+}
+
 template <int LOG_N, int LOG_N1, bool FWD, int IN, int OUT, class K>
 int maybe_chunks_tma(const DevChain& ch, u64* dst, const u64* src, const K& kt, int nk,
                      long src_bstride, long dst_bstride, cudaStream_t st, bool& done) {
@@ -1642,13 +1839,6 @@ int launch_split(const DevChain& ch, const NttArgs& a, bool inverse, bool lazy,
   // chunk tiles of <= 2 chunks stage their twiddles in shared memory
   const bool kstage = (K::NB >> kt.log_r) <= kChunkTwC;
   int rc;
-  if (C::THREADS == K::THREADS && ch.fp64_ok && kstage && ch.fuse && fused_enabled()) {
-    ct.src = inverse ? d : s;
-    ct.dst = d;
-    kt.src = inverse ? s : d;
-    kt.dst = d;
-    return launch_fused(ch, a.dst, a.src, ct, kt, !inverse, a.rows, a.map.limbs, st);
-  }
   // TMA column tiles: N1 = 256 (one 256-k-row box), 16 columns per tile
   using CT = ColsTmaTile<LOG_N, LOG_N1>;
   constexpr bool kTmaShape = (LOG_N1 == 8) && (C::CN == 16);
@@ -1657,6 +1847,31 @@ int launch_split(const DevChain& ch, const NttArgs& a, bool inverse, bool lazy,
   // rows (rows % limbs == 0: no box row can fall past the buffer's end)
   const bool use_ktma = (LOG_N - LOG_N1 == 8) && ch.fp64_ok && kstage && tma_enabled() &&
                         a.rows % a.map.limbs == 0 && std::getenv("FHE_NTT_KTMA") == nullptr;
+  if constexpr (LOG_N1 == 8 && LOG_N - LOG_N1 == 8) {
+    // fused only for 16-row groups (one chunk per tile): measured faster
+    // there (5120-row sweep +3-6%), slower for 8-row groups (key-switch ModUp)
+    if (use_tma && use_ktma && ch.fuse && fused_tma_enabled() && kt.log_r >= FHE_FUSE_MIN_LOG_R) {
+      ColsTmaTile<LOG_N, LOG_N1> tc;
+      static_cast<C&>(tc) = ct;
+      tc.src = inverse ? d : s;
+      tc.dst = d;
+      ChunksTmaTile<LOG_N, LOG_N1> tk;
+      static_cast<K&>(tk) = kt;
+      tk.src = inverse ? s : d;
+      tk.dst = d;
+      bool done = false;
+      rc = launch_fused_tma(ch, a.dst, a.src, tc, tk, !inverse, a.src_bstride, a.dst_bstride,
+                            a.rows, a.map.limbs, st, done);
+      if (rc || done) return rc;
+    }
+  }
+  if (C::THREADS == K::THREADS && ch.fp64_ok && kstage && ch.fuse && fused_enabled()) {
+    ct.src = inverse ? d : s;
+    ct.dst = d;
+    kt.src = inverse ? s : d;
+    kt.dst = d;
+    return launch_fused(ch, a.dst, a.src, ct, kt, !inverse, a.rows, a.map.limbs, st);
+  }
   if (ch.fp64_ok) {
     if (!inverse) {
       ct.src = s;
