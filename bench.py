@@ -481,7 +481,9 @@ def main():
     try:
         with open(os.path.join(ROOT, "profiles", "r1_ntt_traffic.json")) as f:
             tr = json.load(f)
-        traffic = (tr["cols_kernel_dram_bytes"] + tr["chunks_kernel_dram_bytes"]) * rows / tr["rows"]
+        per = tr.get("fused_kernel_dram_bytes") or (tr["cols_kernel_dram_bytes"]
+                                                    + tr["chunks_kernel_dram_bytes"])
+        traffic = per * rows / tr["rows"]
     except Exception:
         pass
     inv_gbs = algo / (ntt_ms["inverse"] / 1000.0) / 1e9
@@ -500,7 +502,7 @@ def main():
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "path": "host_io.hmult_relin_host_batch: ckks_multiply + ckks_relinearize per "
                         "pair, pinned host buffers, H2D/compute/D2H on 3 streams"},
-        "roofline": {"bound": "hbm", "kernel": "batched NTT forward (cols+chunks passes), "
+        "roofline": {"bound": "hbm", "kernel": "batched NTT forward (fused four-step TMA kernel), "
                      f"N=2^16, {rows} rows", "achieved": fwd_gbs, "peak": peak,
                      "peak_kind": peak_kind, "unit": "GB/s", "frac": fwd_gbs / peak,
                      "traffic": traffic, "traffic_source": "profiles/r1_ntt_traffic.json (ncu, "
