@@ -41,6 +41,25 @@ class ShardGroup:
             return results
         return [self._bcast(res, self.owner(i)) for i, res in enumerate(results)]
 
+    def map_units_batched(self, units: list, fn, batch_fn, key):
+        """map_units, but the units a rank owns are grouped by key(unit) and
+        each group goes to batch_fn(list of units) (one lockstep batch);
+        batch_fn may return None to fall back to fn per unit."""
+        mine = [i for i in range(len(units)) if self.owner(i) == self.rank]
+        groups: dict = {}
+        for i in mine:
+            groups.setdefault(key(units[i]), []).append(i)
+        results: list = [None] * len(units)
+        for idx in groups.values():
+            res = batch_fn([units[i] for i in idx]) if len(idx) > 1 else None
+            if res is None:
+                res = [fn(units[i]) for i in idx]
+            for i, r in zip(idx, res):
+                results[i] = r
+        if self.world == 1:
+            return results
+        return [self._bcast(res, self.owner(i)) for i, res in enumerate(results)]
+
     # -- exchange -------------------------------------------------------------
     def _bcast(self, res, src: int):
         import torch.distributed as dist
