@@ -27,6 +27,12 @@ constexpr int kMaxAlpha = 16;
 #ifndef FHE_INNER_MINB
 #define FHE_INNER_MINB 3
 #endif
+#ifndef FHE_MODUP_CPT
+#define FHE_MODUP_CPT 2
+#endif
+#ifndef FHE_MODUP_MINB
+#define FHE_MODUP_MINB 2
+#endif
 #ifndef FHE_MODUP_U
 #define FHE_MODUP_U 6
 #endif
@@ -313,8 +319,8 @@ __device__ __forceinline__ double fp_pos(double x, double q) { return x < 0.0 ? 
 
 // Per-target constants staged in shared memory; NSM bounds the digit size
 // (registers), U targets are accumulated at once (independent FP64 chains).
-template <int NSM, int U>
-__global__ void __launch_bounds__(kThreads, 3)
+template <int NSM, int U, int CPT = FHE_MODUP_CPT>
+__global__ void __launch_bounds__(kThreads, FHE_MODUP_MINB)
     modup_fp_kernel(const DevChain ch, const u64* __restrict__ c, long c_stride,
                     u64* __restrict__ ext, long ext_stride, const int* __restrict__ dig_info,
                     const double2* __restrict__ up_inv, const double2* __restrict__ up_w, int level,
@@ -335,44 +341,62 @@ __global__ void __launch_bounds__(kThreads, 3)
   const long n = 1L << log_n;
   const u64* cb = c + b * c_stride;
   u64* eb = ext + b * ext_stride + (long)row_off * n;
-  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n;
-       i += (long)gridDim.x * blockDim.x) {
-    double y[NSM];
+  // CPT coefficients per thread (i, i + n/CPT): each staged constant read
+  // serves CPT independent accumulator chains
+  for (long i0 = blockIdx.x * (long)blockDim.x + threadIdx.x; i0 < n / CPT;
+       i0 += (long)gridDim.x * blockDim.x) {
+    double y[CPT][NSM];
 #pragma unroll
     for (int s = 0; s < NSM; ++s) {
       if (s < na) {
         const double q = ch.qd[s0 + s].x;
         // y_s = [c_s (Q_d/q_s)^-1]_{q_s}, canonical: the conversion is an
         // integer-level formula, so the representative matters
-        y[s] = fp_pos(fp_mulmod(fp_from_u52(cb[(long)(s0 + s) * n + i]), up_inv[s0 + s], q), q);
+#pragma unroll
+        for (int c = 0; c < CPT; ++c)
+          y[c][s] = fp_pos(fp_mulmod(fp_from_u52(cb[(long)(s0 + s) * n + i0 + c * (n / CPT)]),
+                                     up_inv[s0 + s], q),
+                           q);
       }
     }
     int t = 0;
     for (; t + U <= nt; t += U) {
-      double acc[U];
+      double acc[CPT][U];
 #pragma unroll
-      for (int u = 0; u < U; ++u) acc[u] = 0.0;
+      for (int c = 0; c < CPT; ++c)
+#pragma unroll
+        for (int u = 0; u < U; ++u) acc[c][u] = 0.0;
 #pragma unroll
       for (int s = 0; s < NSM; ++s) {
         if (s < na) {
 #pragma unroll
-          for (int u = 0; u < U; ++u)
-            acc[u] = __dadd_rn(acc[u], fp_mulmod(y[s], swd[s * nt + t + u], tq[t + u].x));
+          for (int u = 0; u < U; ++u) {
+            const double2 w = swd[s * nt + t + u];
+            const double qv = tq[t + u].x;
+#pragma unroll
+            for (int c = 0; c < CPT; ++c)
+              acc[c][u] = __dadd_rn(acc[c][u], fp_mulmod(y[c][s], w, qv));
+          }
         }
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const double2 qd = tq[t + u];
-        eb[(long)(t + u) * n + i] = fp_canon(fp_reduce(acc[u], qd), qd.x);
+#pragma unroll
+        for (int c = 0; c < CPT; ++c)
+          eb[(long)(t + u) * n + i0 + c * (n / CPT)] = fp_canon(fp_reduce(acc[c][u], qd), qd.x);
       }
     }
     for (; t < nt; ++t) {
       const double2 qd = tq[t];
-      double acc = 0.0;
 #pragma unroll
-      for (int s = 0; s < NSM; ++s)
-        if (s < na) acc = __dadd_rn(acc, fp_mulmod(y[s], swd[s * nt + t], qd.x));
-      eb[(long)t * n + i] = fp_canon(fp_reduce(acc, qd), qd.x);
+      for (int c = 0; c < CPT; ++c) {
+        double acc = 0.0;
+#pragma unroll
+        for (int s = 0; s < NSM; ++s)
+          if (s < na) acc = __dadd_rn(acc, fp_mulmod(y[c][s], swd[s * nt + t], qd.x));
+        eb[(long)t * n + i0 + c * (n / CPT)] = fp_canon(fp_reduce(acc, qd), qd.x);
+      }
     }
   }
 }
