@@ -8,6 +8,22 @@ int grid_for(long work);
 // ntt.cu: transform `rows` rows of src into dst (may alias).  Row r uses
 // chain position map(r) and lives at (r / map.limbs) * bstride +
 // (r % map.limbs) * N words (bstride 0: contiguous rows).
+// Optional ModDown finish applied in the forward NTT's last-pass epilogue
+// instead of storing the transform: row r (= (b * 2 + poly) * level + j) of
+// the result x gives  out_poly[b][j] = add_poly[b][j] + (accQ[r] - x) P^-1_j
+// (keyswitch.cu moddown_finish_kernel; NTT rows are the ModDown conv rows).
+struct NttFinish {
+  const u64* accQ;
+  const WPair* p_inv;  // [level] (P^-1 mod q_j, Shoup)
+  const u64* add0;
+  const u64* add1;
+  long add_stride;
+  u64* out0;
+  u64* out1;
+  long out_stride;
+  int level;
+};
+
 struct NttArgs {
   u64* dst;
   const u64* src;
@@ -15,6 +31,8 @@ struct NttArgs {
   RowMap map;
   long src_bstride;
   long dst_bstride;
+  const NttFinish* fin = nullptr;  // forward only; *fin_done tells if it was applied
+  bool* fin_done = nullptr;
 };
 int launch_ntt(const DevChain& ch, const NttArgs& a, bool inverse, cudaStream_t st);
 // per-chain scratch of the fused four-step NTT (tile tickets, group counters)

@@ -597,6 +597,16 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
+bool fuse_finish_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    // opt-in: measured on par with the separate finish pass (profiles/r1_ntt_notes.md)
+    const char* e = getenv("FHE_FUSE_MODDOWN");
+    on = (e && e[0] == '1') ? 1 : 0;
+  }
+  return on == 1;
+}
+
 int mac_chunk(const std::vector<u64>& primes) {
   u64 mx = 0;
   for (u64 p : primes) mx = p > mx ? p : mx;
@@ -726,8 +736,18 @@ int run_keyswitch(const FheContext& ctx, int level, const u64* d, long d_stride,
                                                         level, K, L, chunk);
     FHE_LAUNCH_CHECK();
   }
-  rc = launch_ntt(ch, conv, conv, batch * 2 * level, RowMap{nullptr, level, 0}, false, st);
+  // forward NTT of the conversion with the ModDown finish fused into its
+  // last pass when the TMA chunk path runs it; otherwise a separate pass
+  const NttFinish fin{accQ, lp.p_inv, add0, add1, add_stride, out0, out1, out_stride, level};
+  bool fin_done = false;
+  NttArgs na{conv, conv, batch * 2 * level, RowMap{nullptr, level, 0}, 0, 0};
+  if (fuse_finish_enabled()) {
+    na.fin = &fin;
+    na.fin_done = &fin_done;
+  }
+  rc = launch_ntt(ch, na, false, st);
   if (rc) return rc;
+  if (fin_done) return 0;
   moddown_finish_kernel<<<grid_for((long)batch * 2 * level * n), kThreads, 0, st>>>(
       ch, accQ, conv, lp.p_inv, add0, add1, add_stride, out0, out1, out_stride, level, batch);
   FHE_LAUNCH_CHECK();

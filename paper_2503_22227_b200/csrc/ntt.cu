@@ -447,11 +447,19 @@ constexpr bool warp_local(int log_s) {
 //  * array tiles, warp-local passes: each warp stores the arrays it computed;
 //  * array tiles otherwise: CTA-wide over all arrays.
 template <class Tile, int GPA_LOG, bool WL>
-__device__ __forceinline__ void epilogue_store(const u64* sm, const Tile& tl, u64* gout) {
+__device__ __forceinline__ void epilogue_store(const u64* sm, const Tile& tl, u64* gout,
+                                               const DevChain& ch) {
   constexpr int LOG_S = Tile::LOG_S;
   constexpr int S = 1 << LOG_S;
   constexpr int T = Tile::THREADS;
   if constexpr (Tile::TMA) {
+    if constexpr (Tile::SWZ) {
+      if (tl.has_fin) {  // fused ModDown finish instead of the transform store
+        __syncthreads();
+        tl.finish_store(sm, ch);
+        return;
+      }
+    }
     // results are in the dense tile: one bulk tensor store by thread 0
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncthreads();
@@ -848,7 +856,7 @@ __device__ __forceinline__ void run_pass_fp(u64* sm, const double2* tws, const T
       }
     }
   }
-  if (LAST && EPI) epilogue_store<Tile, GPA_LOG, WL>(sm, tl, gout);
+  if (LAST && EPI) epilogue_store<Tile, GPA_LOG, WL>(sm, tl, gout, ch);
 }
 
 template <int LOG_S, int P, int IN, int OUT, bool STW, class Tile>
@@ -1164,8 +1172,43 @@ struct ChunksTmaTile : ChunksTile<LOG_N, LOG_N1> {
   __device__ static __forceinline__ int pad(int t) { return t ^ ((t >> 3) & 14); }
   const CUtensorMap* smap_p = nullptr;
   const CUtensorMap* dmap_p = nullptr;
+  bool has_fin = false;
+  NttFinish fin{};
   __device__ __forceinline__ void tma_load(u64* sm, uint64_t* bar) const {
     tma_load_4d(sm, smap_p, 0, this->c0 << (Base::LOG_S - 4), this->cls_, this->i0_, bar);
+  }
+  // ModDown finish from the swizzled result tile, 16 bytes per step: every
+  // element is read once from smem, accQ and the add-in once from HBM, and
+  // the output written once (no transform store, no separate finish pass)
+  __device__ __forceinline__ void finish_store(const u64* sm, const DevChain& ch) const {
+    constexpr int S = 1 << Base::LOG_S;
+    const int lc = this->log_c;
+    const int arrays = this->nb;
+    for (int q = threadIdx.x; q < (arrays * S) >> 1; q += Base::THREADS) {
+      const int b = q / (S >> 1), k = (q % (S >> 1)) << 1;
+      const int t = b * S + k;
+      const ulonglong2 x = *reinterpret_cast<const ulonglong2*>(&sm[t ^ ((t >> 3) & 14)]);
+      const int i = b >> lc, c = b & ((1 << lc) - 1);
+      const int row = this->cls_ + (this->i0_ + i) * this->map.limbs;  // conv row
+      const long col = ((long)(this->c0 + c) << Base::LOG_S) + k;
+      const int j = row % fin.level;
+      const int bp = row / fin.level;  // b * 2 + poly
+      const int bb = bp >> 1, poly = bp & 1;
+      const u64 qj = ch.mc[j].q;
+      const WPair pi = fin.p_inv[j];
+      const ulonglong2 a = *reinterpret_cast<const ulonglong2*>(fin.accQ + ((long)row << ch.log_n) + col);
+      u64 v0 = shoup_mul(sub_mod(a.x, x.x, qj), pi.w, pi.sh, qj);
+      u64 v1 = shoup_mul(sub_mod(a.y, x.y, qj), pi.w, pi.sh, qj);
+      const u64* add = poly ? fin.add1 : fin.add0;
+      const long w = ((long)j << ch.log_n) + col;
+      if (add) {
+        const ulonglong2 d = *reinterpret_cast<const ulonglong2*>(add + bb * fin.add_stride + w);
+        v0 = add_mod(d.x, v0, qj);
+        v1 = add_mod(d.y, v1, qj);
+      }
+      u64* out = poly ? fin.out1 : fin.out0;
+      *reinterpret_cast<ulonglong2*>(out + bb * fin.out_stride + w) = make_ulonglong2(v0, v1);
+    }
   }
   __device__ __forceinline__ void tma_store(const u64* sm) const {
     tma_store_4d(dmap_p, 0, this->c0 << (Base::LOG_S - 4), this->cls_, this->i0_, sm);
@@ -1766,12 +1809,17 @@ int launch_fused_tma(const DevChain& ch, u64* dst, const u64* src, const CT& ct,
 
 template <int LOG_N, int LOG_N1, bool FWD, int IN, int OUT, class K>
 int maybe_chunks_tma(const DevChain& ch, u64* dst, const u64* src, const K& kt, int nk,
-                     long src_bstride, long dst_bstride, cudaStream_t st, bool& done) {
+                     long src_bstride, long dst_bstride, cudaStream_t st, bool& done,
+                     const NttFinish* fin = nullptr) {
   done = false;
   if constexpr (LOG_N - LOG_N1 == 8) {
     using KT = ChunksTmaTile<LOG_N, LOG_N1>;
     KT tk;
     static_cast<K&>(tk) = kt;
+    if (fin) {
+      tk.has_fin = true;
+      tk.fin = *fin;
+    }
     return launch_chunks_tma<KT, FWD, IN, OUT>(ch, dst, src, tk, nk, src_bstride, dst_bstride, st,
                                                done);
   }
@@ -1850,7 +1898,8 @@ int launch_split(const DevChain& ch, const NttArgs& a, bool inverse, bool lazy,
   if constexpr (LOG_N1 == 8 && LOG_N - LOG_N1 == 8) {
     // fused only for 16-row groups (one chunk per tile): measured faster
     // there (5120-row sweep +3-6%), slower for 8-row groups (key-switch ModUp)
-    if (use_tma && use_ktma && ch.fuse && fused_tma_enabled() && kt.log_r >= FHE_FUSE_MIN_LOG_R) {
+    if (use_tma && use_ktma && ch.fuse && fused_tma_enabled() && kt.log_r >= FHE_FUSE_MIN_LOG_R &&
+        !a.fin) {
       ColsTmaTile<LOG_N, LOG_N1> tc;
       static_cast<C&>(tc) = ct;
       tc.src = inverse ? d : s;
@@ -1865,7 +1914,7 @@ int launch_split(const DevChain& ch, const NttArgs& a, bool inverse, bool lazy,
       if (rc || done) return rc;
     }
   }
-  if (C::THREADS == K::THREADS && ch.fp64_ok && kstage && ch.fuse && fused_enabled()) {
+  if (C::THREADS == K::THREADS && ch.fp64_ok && kstage && ch.fuse && fused_enabled() && !a.fin) {
     ct.src = inverse ? d : s;
     ct.dst = d;
     kt.src = inverse ? s : d;
@@ -1890,9 +1939,11 @@ int launch_split(const DevChain& ch, const NttArgs& a, bool inverse, bool lazy,
       if (!done)
         rc = launch_tiles_fp<C, true, FPIN_U64, FPOUT_DOUBLE, true>(ch, a.dst, a.src, ct, nc, st);
       bool kdone = false;
-      if (!rc && use_ktma)
+      if (!rc && use_ktma) {
         rc = maybe_chunks_tma<LOG_N, LOG_N1, true, FPIN_DOUBLE, FPOUT_U64>(
-            ch, a.dst, a.dst, kt, nk, a.dst_bstride, a.dst_bstride, st, kdone);
+            ch, a.dst, a.dst, kt, nk, a.dst_bstride, a.dst_bstride, st, kdone, a.fin);
+        if (!rc && kdone && a.fin && a.fin_done) *a.fin_done = true;
+      }
       if (!rc && !kdone)
         rc = kstage ? launch_tiles_fp<K, true, FPIN_DOUBLE, FPOUT_U64, true>(ch, a.dst, a.dst, kt, nk, st)
                     : launch_tiles_fp<K, true, FPIN_DOUBLE, FPOUT_U64>(ch, a.dst, a.dst, kt, nk, st);

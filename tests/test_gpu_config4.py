@@ -116,3 +116,40 @@ def test_hybrid_boosted_rotate_within_tolerance(hybrid):
     plain = ckks.ckks_rotate(ctx, cx, 1, hybrid["gks"])
     dec2 = ckks.ckks_decode(ctx, ckks.ckks_decrypt(ctx, plain, sk))
     assert float(np.max(np.abs(dec2 - np.roll(x, -1)))) < 1e-6
+
+
+def test_fused_moddown_finish_matches_separate_pass():
+    """The opt-in ModDown finish fused into the conversion NTT's epilogue
+    (FHE_FUSE_MODDOWN=1) gives the same relinearized words as the separate
+    finish pass (child processes: the switch is read once per process)."""
+    import hashlib
+    import os
+    import subprocess
+    import sys
+
+    code = r'''
+import hashlib, numpy as np, torch
+from paper_2503_22227_b200.context import Context, PoolConfig, hybrid_params
+from paper_2503_22227_b200.coremath.sampling import Rng
+from paper_2503_22227_b200.keys import keygen, pk_gen, relin_keygen
+from paper_2503_22227_b200.schemes import ckks
+ctx = Context(hybrid_params(1 << 16, 30, bits=50, special=10, special_bits=50, dnum=3,
+                            scale=float(2 ** 49)), PoolConfig(unit_mb=200, cap_mb=4096))
+seed = lambda s: Rng(int(s).to_bytes(32, "little"))
+sk = keygen(ctx, seed(4)); pk = pk_gen(ctx, sk, seed(41)); rlk = relin_keygen(ctx, sk, seed(42))
+r = np.random.default_rng(9)
+x = ckks.ckks_encrypt(ctx, ckks.ckks_encode(ctx, r.uniform(-1, 1, ctx.n // 2)), pk, seed(43))
+y = ckks.ckks_encrypt(ctx, ckks.ckks_encode(ctx, r.uniform(-1, 1, ctx.n // 2)), pk, seed(44))
+out = ckks.ckks_relinearize(ctx, ckks.ckks_multiply(ctx, x, y), rlk)
+print(hashlib.sha256(out.data.view().cpu().numpy().tobytes()).hexdigest())
+'''
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    digests = []
+    for flag in ("0", "1"):
+        env = dict(os.environ, FHE_FUSE_MODDOWN=flag, PYTHONPATH=root)
+        out = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True,
+                             text=True, timeout=900)
+        assert out.returncode == 0, out.stderr[-2000:]
+        digests.append(out.stdout.strip().splitlines()[-1])
+    assert digests[0] == digests[1]
+    del hashlib
