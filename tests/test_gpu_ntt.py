@@ -136,3 +136,32 @@ print("fused ok")
     out = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True,
                          text=True, timeout=600)
     assert out.returncode == 0 and "fused ok" in out.stdout, out.stderr[-2000:]
+
+
+def test_empty_and_partial_batches():
+    """Zero rows is a no-op; a row count that is not a multiple of the limb
+    count (the TMA tiles' box cannot cover a partial batch) takes the
+    cp.async tiles and still matches the oracle."""
+    import torch
+
+    from oracle import fast
+    from paper_2503_22227_b200.coremath.ntt import DeviceChain
+    from paper_2503_22227_b200.coremath.primes import gen_ntt_prime_chain
+
+    n, L = 1 << 16, 3
+    primes = [m.value for m in gen_ntt_prime_chain(50, n, L)]
+    ch = DeviceChain(primes, 16)
+    buf = torch.arange(16, dtype=torch.int64, device="cuda")
+    before = buf.clone()
+    ch.transform(buf, 0, False, limbs=L, offset=0)
+    ch.transform(buf, 0, True, limbs=L, offset=0)
+    torch.cuda.synchronize()
+    assert torch.equal(buf, before)
+    rows = 2 * L + 1  # partial last batch of rows
+    rng = np.random.default_rng(17)
+    a = np.stack([rng.integers(0, primes[r % L], n, dtype=np.uint64) for r in range(rows)])
+    dev = torch.from_numpy(a.view(np.int64)).cuda()
+    f = dev.clone()
+    ch.transform(f, rows, False, limbs=L, offset=0)
+    torch.cuda.synchronize()
+    assert (to_u64(f) == fast.ntt_forward(a, primes, np.arange(rows) % L)).all()
