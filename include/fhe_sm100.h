@@ -52,6 +52,11 @@ enum {
 };
 
 const char* fhe_last_error(void);
+
+/* Number of kernels this library has launched in the process (every entry
+ * point's launches; cudaMemsetAsync is not counted).  No reference
+ * counterpart: evidence for benchmarks (bench.py gpu_launches). */
+uint64_t fhe_launch_count(void);
 int fhe_device_sm_count(void);
 
 /* ---- chains: NttTables / NttChain precompute (coremath/ntt.py:52-137,

@@ -27,6 +27,7 @@ _sz = ctypes.c_size_t
 # name -> (restype, argtypes)
 SIGNATURES = {
     "fhe_last_error": (ctypes.c_char_p, []),
+    "fhe_launch_count": (ctypes.c_uint64, []),
     "fhe_device_sm_count": (_int, []),
     "fhe_chain_create": (_int, [_vp, _int, _int, ctypes.POINTER(_vp)]),
     "fhe_chain_destroy": (_int, [_vp]),

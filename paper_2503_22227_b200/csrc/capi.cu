@@ -1,13 +1,16 @@
 // extern "C" boundary (include/fhe_sm100.h).  Argument checking that needs
 // no device access happens here; everything else is forwarded to the
 // launchers, which enqueue asynchronously on the caller's stream.
+#include <atomic>
 #include <exception>
 
 #include "fhe_context.cuh"
 
 static thread_local std::string g_err;
+static std::atomic<unsigned long long> g_launches{0};
 
 void fhe_set_error(const std::string& msg) { g_err = msg; }
+void fhe_count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 #define FHE_TRY(body)                   \
   try {                                 \
@@ -20,6 +23,8 @@ void fhe_set_error(const std::string& msg) { g_err = msg; }
 extern "C" {
 
 const char* fhe_last_error(void) { return g_err.c_str(); }
+
+uint64_t fhe_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 
 int fhe_device_sm_count(void) {
   int dev = 0, n = 0;

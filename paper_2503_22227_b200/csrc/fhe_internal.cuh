@@ -69,8 +69,13 @@ void fhe_set_error(const std::string& msg);
     }                                                                          \
   } while (0)
 
+// every kernel launch of the library is followed by FHE_LAUNCH_CHECK, which
+// also counts it (fhe_launch_count())
+void fhe_count_launch();
+
 #define FHE_LAUNCH_CHECK()                                                     \
   do {                                                                         \
+    fhe_count_launch();                                                        \
     cudaError_t _e = cudaGetLastError();                                       \
     if (_e != cudaSuccess) {                                                   \
       fhe_set_error(std::string("kernel launch: ") + cudaGetErrorString(_e));  \
