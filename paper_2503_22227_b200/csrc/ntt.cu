@@ -332,7 +332,7 @@ __global__ void __launch_bounds__(Tile::THREADS, Tile::MINB)
 #define FHE_FUSE_MIN_LOG_R 4
 #endif
 #ifndef FHE_FUSE_LAG
-#define FHE_FUSE_LAG 4
+#define FHE_FUSE_LAG 8
 #endif
 constexpr int kFuseLag = FHE_FUSE_LAG;
 constexpr int kFuseSlabs = 8;
