@@ -328,6 +328,9 @@ __global__ void __launch_bounds__(Tile::THREADS, Tile::MINB)
 // every first-phase tile of its group has signalled its counter.  Tickets
 // are taken by resident CTAs only and a CTA only ever waits on tickets issued
 // before its own, so the wait cannot deadlock.
+#ifndef FHE_FUSE_MAX_LOG_R
+#define FHE_FUSE_MAX_LOG_R 4
+#endif
 #ifndef FHE_FUSE_MIN_LOG_R
 #define FHE_FUSE_MIN_LOG_R 4
 #endif
@@ -944,6 +947,8 @@ int launch_split(const DevChain& ch, const NttArgs& a, bool inverse, bool lazy,
       tc.dst = d;
       ChunksTmaTile<LOG_N, LOG_N1> tk;
       static_cast<K&>(tk) = kt;
+      // smaller row groups keep the L2-resident window (lag x group) small
+      if (tk.log_r > FHE_FUSE_MAX_LOG_R) tk.plan(a.rows, a.map.limbs, FHE_FUSE_MAX_LOG_R);
       tk.src = inverse ? s : d;
       tk.dst = d;
       bool done = false;

@@ -373,10 +373,10 @@ struct ChunksTile {
   }
   __device__ __forceinline__ int arrays() const { return nb; }
   // host: tiles for `rows` rows with residue classes of `limbs`
-  int plan(int rows_, int limbs) {
+  int plan(int rows_, int limbs, int max_log_r = 30) {
     const int rpc = (rows_ + limbs - 1) / limbs;
     log_r = 0;
-    while ((2 << log_r) <= NB && (2 << log_r) <= rpc) ++log_r;
+    while ((2 << log_r) <= NB && (2 << log_r) <= rpc && log_r < max_log_r) ++log_r;
     rblocks = (rpc + (1 << log_r) - 1) >> log_r;
     const int C = NB >> log_r;
     cblocks = N1 / C;
