@@ -401,8 +401,8 @@ __global__ void __launch_bounds__(kThreads, FHE_MODUP_MINB)
   }
 }
 
-template <int NSM, int U>
-__global__ void __launch_bounds__(kThreads, 3)
+template <int NSM, int U, int CPT = FHE_MODUP_CPT>
+__global__ void __launch_bounds__(kThreads, FHE_MODUP_MINB)
     moddown_conv_fp_kernel(const DevChain ch, const u64* __restrict__ accP,
                            u64* __restrict__ conv, const double2* __restrict__ down_inv,
                            const double2* __restrict__ down_w, int level, int K, int L) {
@@ -416,42 +416,59 @@ __global__ void __launch_bounds__(kThreads, 3)
   const long n = 1L << log_n;
   const u64* src = accP + (long)bp * K * n;
   u64* dst = conv + (long)bp * level * n;
-  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n;
-       i += (long)gridDim.x * blockDim.x) {
-    double y[NSM];
+  // CPT coefficients per thread (i, i + n/CPT) share each staged constant
+  for (long i0 = blockIdx.x * (long)blockDim.x + threadIdx.x; i0 < n / CPT;
+       i0 += (long)gridDim.x * blockDim.x) {
+    double y[CPT][NSM];
 #pragma unroll
     for (int k = 0; k < NSM; ++k) {
       if (k < K) {
         const double p = ch.qd[L + k].x;
-        y[k] = fp_pos(fp_mulmod(fp_from_u52(src[(long)k * n + i]), down_inv[k], p), p);
+#pragma unroll
+        for (int c = 0; c < CPT; ++c)
+          y[c][k] = fp_pos(fp_mulmod(fp_from_u52(src[(long)k * n + i0 + c * (n / CPT)]),
+                                     down_inv[k], p),
+                           p);
       }
     }
     int j = 0;
     for (; j + U <= level; j += U) {
-      double acc[U];
+      double acc[CPT][U];
 #pragma unroll
-      for (int u = 0; u < U; ++u) acc[u] = 0.0;
+      for (int c = 0; c < CPT; ++c)
+#pragma unroll
+        for (int u = 0; u < U; ++u) acc[c][u] = 0.0;
 #pragma unroll
       for (int k = 0; k < NSM; ++k) {
         if (k < K) {
 #pragma unroll
-          for (int u = 0; u < U; ++u)
-            acc[u] = __dadd_rn(acc[u], fp_mulmod(y[k], swd[k * level + j + u], tq[j + u].x));
+          for (int u = 0; u < U; ++u) {
+            const double2 w = swd[k * level + j + u];
+            const double qv = tq[j + u].x;
+#pragma unroll
+            for (int c = 0; c < CPT; ++c)
+              acc[c][u] = __dadd_rn(acc[c][u], fp_mulmod(y[c][k], w, qv));
+          }
         }
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const double2 qd = tq[j + u];
-        dst[(long)(j + u) * n + i] = fp_canon(fp_reduce(acc[u], qd), qd.x);
+#pragma unroll
+        for (int c = 0; c < CPT; ++c)
+          dst[(long)(j + u) * n + i0 + c * (n / CPT)] = fp_canon(fp_reduce(acc[c][u], qd), qd.x);
       }
     }
     for (; j < level; ++j) {
       const double2 qd = tq[j];
-      double acc = 0.0;
 #pragma unroll
-      for (int k = 0; k < NSM; ++k)
-        if (k < K) acc = __dadd_rn(acc, fp_mulmod(y[k], swd[k * level + j], qd.x));
-      dst[(long)j * n + i] = fp_canon(fp_reduce(acc, qd), qd.x);
+      for (int c = 0; c < CPT; ++c) {
+        double acc = 0.0;
+#pragma unroll
+        for (int k = 0; k < NSM; ++k)
+          if (k < K) acc = __dadd_rn(acc, fp_mulmod(y[c][k], swd[k * level + j], qd.x));
+        dst[(long)j * n + i0 + c * (n / CPT)] = fp_canon(fp_reduce(acc, qd), qd.x);
+      }
     }
   }
 }
