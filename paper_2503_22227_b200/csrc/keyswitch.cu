@@ -477,24 +477,29 @@ __global__ void __launch_bounds__(kThreads, FHE_MODUP_MINB)
 // the key words are variable operands, so their quotient estimates key/p
 // are formed on the fly (one DMUL); each term is an exact fp_mulmod, the
 // digit sum (|.| <= 4 * 0.75 p) is reduced once.
-template <int kD>
+// Output limbs m in [m_begin, m_end).  FIN: Q limbs only, and instead of
+// storing accQ the ModDown finish is applied in place of moddown_finish_kernel:
+// out = add + (acc - conv) P^-1 (conv = the NTT'd P->Q conversion), so accQ
+// never round-trips HBM.
+template <int kD, bool FIN = false>
 __global__ void __launch_bounds__(kThreads, FHE_INNER_MINB)
     ks_inner_fp_kernel(const DevChain ch, const u64* __restrict__ d, long d_stride,
                        const u64* __restrict__ ext, long ext_stride, const u64* __restrict__ key,
                        int keyL, const int* __restrict__ dig_info, int D, int level, int K, int L,
                        u64* __restrict__ accQ, u64* __restrict__ accP, const u64* add0,
                        const u64* add1, long add_stride, u64* out0, u64* out1, long out_stride,
-                       int batch) {
+                       int batch, int m_begin, int m_end, const u64* __restrict__ conv,
+                       const WPair* __restrict__ p_inv) {
   // kD: digits (template: registers sized to the key's dnum)
   extern __shared__ int sinfo[];
   for (int i = threadIdx.x; i < 4 * D; i += blockDim.x) sinfo[i] = dig_info[i];
   __syncthreads();
   const int log_n = ch.log_n;
   const long n = 1L << log_n;
-  const long total = (long)(level + K) << log_n;
+  const long total = (long)(m_end - m_begin) << log_n;
   for (long t = blockIdx.x * (long)blockDim.x + threadIdx.x; t < total;
        t += (long)gridDim.x * blockDim.x) {
-    const int m = (int)(t >> log_n);
+    const int m = m_begin + (int)(t >> log_n);
     const long i = t & (n - 1);
     const int p = m < level ? m : L + (m - level);
     const double2 qd = ch.qd[p];
@@ -537,6 +542,19 @@ __global__ void __launch_bounds__(kThreads, FHE_INNER_MINB)
         }
         const u64 rb = fp_canon_half(fp_reduce(sb, qd), qd.x);
         const u64 ra = fp_canon_half(fp_reduce(sa, qd), qd.x);
+        if (FIN) {
+          const WPair pi = p_inv[m];
+          const long w = (long)m * n + i;
+          const long c0 = ((long)(b * 2 + 0) * level + m) * n + i;
+          const long c1 = ((long)(b * 2 + 1) * level + m) * n + i;
+          u64 v0 = shoup_mul(sub_mod(rb, conv[c0], q), pi.w, pi.sh, q);
+          u64 v1 = shoup_mul(sub_mod(ra, conv[c1], q), pi.w, pi.sh, q);
+          if (add0) v0 = add_mod(add0[b * add_stride + w], v0, q);
+          if (add1) v1 = add_mod(add1[b * add_stride + w], v1, q);
+          out0[b * out_stride + w] = v0;
+          out1[b * out_stride + w] = v1;
+          continue;
+        }
         if (K == 0) {
           const long o = b * out_stride + (long)m * n + i;
           const long ai = b * add_stride + (long)m * n + i;
@@ -612,6 +630,15 @@ __global__ void __launch_bounds__(kThreads)
       }
     }
   }
+}
+
+bool fin_inner_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("FHE_FUSE_INNER_FINISH");
+    on = (e && e[0] == '0') ? 0 : 1;
+  }
+  return on == 1;
 }
 
 bool fuse_finish_enabled() {
@@ -708,13 +735,18 @@ int run_keyswitch(const FheContext& ctx, int level, const u64* d, long d_stride,
       if (rc) return rc;
     }
   }
-  // 3. inner product with the key digits (K == 0 writes the result directly)
+  // 3. inner product with the key digits (K == 0 writes the result directly).
+  // With the fused finish (FP64 path, <= 4 digits, K > 0) only the P limbs
+  // are produced here; the Q limbs are folded into the ModDown finish below.
+  const bool fin_inner = K > 0 && ch.fp64_ok && lp.digits <= 4 && fin_inner_enabled();
   {
-    const long work = (long)(level + K) << log_n;
+    const int m_end = level + K, m_begin = fin_inner ? level : 0;
+    const long work = (long)(m_end - m_begin) << log_n;
     auto go = [&](auto kern) {
       kern<<<grid_for(work), kThreads, 4 * lp.digits * sizeof(int), st>>>(
           ch, d, d_stride, ext, (long)lp.ext_rows * n, key, L + K, lp.dig_info, lp.digits, level,
-          K, L, accQ, accP, add0, add1, add_stride, out0, out1, out_stride, batch);
+          K, L, accQ, accP, add0, add1, add_stride, out0, out1, out_stride, batch, m_begin, m_end,
+          nullptr, nullptr);
     };
     if (ch.fp64_ok && lp.digits <= 2)
       go(ks_inner_fp_kernel<2>);
@@ -723,7 +755,9 @@ int run_keyswitch(const FheContext& ctx, int level, const u64* d, long d_stride,
     else if (ch.fp64_ok && lp.digits == 4)
       go(ks_inner_fp_kernel<4>);
     else if (ch.fp64_ok)
-      go(ks_inner_fp_many_kernel);
+      ks_inner_fp_many_kernel<<<grid_for(work), kThreads, 4 * lp.digits * sizeof(int), st>>>(
+          ch, d, d_stride, ext, (long)lp.ext_rows * n, key, L + K, lp.dig_info, lp.digits, level,
+          K, L, accQ, accP, add0, add1, add_stride, out0, out1, out_stride, batch);
     else
       ks_inner_kernel<<<grid_for(work), kThreads, 4 * lp.digits * sizeof(int), st>>>(
           ch, d, d_stride, ext, (long)lp.ext_rows * n, key, L + K, lp.dig_info, lp.digits, level,
@@ -758,13 +792,27 @@ int run_keyswitch(const FheContext& ctx, int level, const u64* d, long d_stride,
   const NttFinish fin{accQ, lp.p_inv, add0, add1, add_stride, out0, out1, out_stride, level};
   bool fin_done = false;
   NttArgs na{conv, conv, batch * 2 * level, RowMap{nullptr, level, 0}, 0, 0};
-  if (fuse_finish_enabled()) {
+  if (fuse_finish_enabled() && !fin_inner) {
     na.fin = &fin;
     na.fin_done = &fin_done;
   }
   rc = launch_ntt(ch, na, false, st);
   if (rc) return rc;
   if (fin_done) return 0;
+  if (fin_inner) {
+    // Q-limb inner product + ModDown finish in one pass
+    auto go = [&](auto kern) {
+      kern<<<grid_for((long)level << log_n), kThreads, 4 * lp.digits * sizeof(int), st>>>(
+          ch, d, d_stride, ext, (long)lp.ext_rows * n, key, L + K, lp.dig_info, lp.digits, level,
+          K, L, nullptr, nullptr, add0, add1, add_stride, out0, out1, out_stride, batch, 0, level,
+          conv, lp.p_inv);
+    };
+    if (lp.digits <= 2) go(ks_inner_fp_kernel<2, true>);
+    else if (lp.digits == 3) go(ks_inner_fp_kernel<3, true>);
+    else go(ks_inner_fp_kernel<4, true>);
+    FHE_LAUNCH_CHECK();
+    return 0;
+  }
   moddown_finish_kernel<<<grid_for((long)batch * 2 * level * n), kThreads, 0, st>>>(
       ch, accQ, conv, lp.p_inv, add0, add1, add_stride, out0, out1, out_stride, level, batch);
   FHE_LAUNCH_CHECK();
