@@ -522,11 +522,24 @@ __global__ void __launch_bounds__(kThreads, FHE_INNER_MINB)
     }
     for (int b0 = 0; b0 < batch; b0 += FHE_INNER_BU) {
       u64 v[FHE_INNER_BU][kD];
+      // FIN: the finish operands are loaded with the digits (all in flight)
+      u64 cv[FIN ? FHE_INNER_BU : 1][2], av[FIN ? FHE_INNER_BU : 1][2];
 #pragma unroll
-      for (int u = 0; u < FHE_INNER_BU; ++u)
+      for (int u = 0; u < FHE_INNER_BU; ++u) {
 #pragma unroll
         for (int di = 0; di < kD; ++di)
           if (di < D && b0 + u < batch) v[u][di] = __ldg(src[di] + (b0 + u) * sstr[di]);
+        if constexpr (FIN) {
+          if (b0 + u < batch) {
+            const int bb = b0 + u;
+            const long w = (long)m * n + i;
+            cv[u][0] = conv[((long)(bb * 2 + 0) * level + m) * n + i];
+            cv[u][1] = conv[((long)(bb * 2 + 1) * level + m) * n + i];
+            av[u][0] = add0 ? add0[bb * add_stride + w] : 0;
+            av[u][1] = add1 ? add1[bb * add_stride + w] : 0;
+          }
+        }
+      }
 #pragma unroll
       for (int u = 0; u < FHE_INNER_BU; ++u) {
         if (b0 + u >= batch) break;
@@ -542,15 +555,13 @@ __global__ void __launch_bounds__(kThreads, FHE_INNER_MINB)
         }
         const u64 rb = fp_canon_half(fp_reduce(sb, qd), qd.x);
         const u64 ra = fp_canon_half(fp_reduce(sa, qd), qd.x);
-        if (FIN) {
+        if constexpr (FIN) {
           const WPair pi = p_inv[m];
           const long w = (long)m * n + i;
-          const long c0 = ((long)(b * 2 + 0) * level + m) * n + i;
-          const long c1 = ((long)(b * 2 + 1) * level + m) * n + i;
-          u64 v0 = shoup_mul(sub_mod(rb, conv[c0], q), pi.w, pi.sh, q);
-          u64 v1 = shoup_mul(sub_mod(ra, conv[c1], q), pi.w, pi.sh, q);
-          if (add0) v0 = add_mod(add0[b * add_stride + w], v0, q);
-          if (add1) v1 = add_mod(add1[b * add_stride + w], v1, q);
+          u64 v0 = shoup_mul(sub_mod(rb, cv[u][0], q), pi.w, pi.sh, q);
+          u64 v1 = shoup_mul(sub_mod(ra, cv[u][1], q), pi.w, pi.sh, q);
+          if (add0) v0 = add_mod(av[u][0], v0, q);
+          if (add1) v1 = add_mod(av[u][1], v1, q);
           out0[b * out_stride + w] = v0;
           out1[b * out_stride + w] = v1;
           continue;
