@@ -24,6 +24,9 @@ constexpr int kMaxAlpha = 16;
 #ifndef FHE_INNER_BU
 #define FHE_INNER_BU 2
 #endif
+#ifndef FHE_FIN_MINB
+#define FHE_FIN_MINB 3
+#endif
 #ifndef FHE_INNER_MINB
 #define FHE_INNER_MINB 3
 #endif
@@ -482,7 +485,7 @@ __global__ void __launch_bounds__(kThreads, FHE_MODUP_MINB)
 // out = add + (acc - conv) P^-1 (conv = the NTT'd P->Q conversion), so accQ
 // never round-trips HBM.
 template <int kD, bool FIN = false>
-__global__ void __launch_bounds__(kThreads, FHE_INNER_MINB)
+__global__ void __launch_bounds__(kThreads, FIN ? FHE_FIN_MINB : FHE_INNER_MINB)
     ks_inner_fp_kernel(const DevChain ch, const u64* __restrict__ d, long d_stride,
                        const u64* __restrict__ ext, long ext_stride, const u64* __restrict__ key,
                        int keyL, const int* __restrict__ dig_info, int D, int level, int K, int L,
