@@ -68,5 +68,4 @@ def main(path: str, out: str | None = None):
 
 
 if __name__ == "__main__":
-    sys.argv = [a for a in sys.argv if a != "--nvtx-first"] + (["--nvtx-first"] if "--nvtx-first" in sys.argv else [])
-    main(*sys.argv[1:])
+    main(*[a for a in sys.argv[1:] if not a.startswith("--")])
