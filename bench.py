@@ -170,13 +170,18 @@ def build_workload(batch: int):
 
 
 def hmult_relin_step(w, batch: int):
-    """One step: batched fused tensor + batched hybrid key switch (2 calls)."""
+    """One step: one batched fhe_hmult_relin (tensor product formed inside the
+    hybrid key switch).  BENCH_HMULT=split: fhe_tensor + fhe_keyswitch (the
+    ckks_multiply / ckks_relinearize pair; same words)."""
     from paper_2503_22227_b200 import _native
-    from paper_2503_22227_b200.keys import key_switch_into
+    from paper_2503_22227_b200.keys import hmult_relin_into, key_switch_into
 
     ctx, lib = w["ctx"], _native.lib()
     L, n = LEVELS, ctx.n
     X, Y, T3, OUT = w["X"], w["Y"], w["T3"], w["OUT"]
+    if os.environ.get("BENCH_HMULT", "fused") != "split":
+        hmult_relin_into(ctx, L, X, Y, w["rlk"], OUT[:, 0], OUT[:, 1], batch=batch)
+        return
     _native.check(lib.fhe_tensor(ctx.chain.handle, T3.data_ptr(), X.data_ptr(), Y.data_ptr(), L,
                                  batch, 2 * L * n, 2 * L * n, 3 * L * n, 0,
                                  _native.stream_handle()), "fhe_tensor")

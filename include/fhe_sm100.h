@@ -126,6 +126,20 @@ int fhe_keyswitch(const FheContext* ctx, int level, const uint64_t* d, int64_t d
                   int64_t add_stride, uint64_t* out0, uint64_t* out1, int64_t out_stride,
                   int batch, void* workspace, size_t ws_bytes, void* stream);
 
+/* ---- fused HMult+Relin: ckks_multiply (ckks.py:308-349, tensor product)
+ *      followed by ckks_relinearize (ckks.py:369-379) in one call.
+ *      x, y: batch x (2, level, n) eval ciphertexts, in_stride words apart
+ *      (y may equal x: squaring).  out0 = d0 + b, out1 = d1 + a with
+ *      (d0, d1, d2) the tensor product and (b, a) the key switch of d2;
+ *      out0/out1 may alias x's polys.  The words equal those of fhe_tensor
+ *      followed by fhe_keyswitch (with FHE_HMULT_TENS=1, d0/d1 are formed
+ *      in the key switch's finishing kernel and never written to HBM). */
+size_t fhe_hmult_relin_workspace(const FheContext* ctx, int level, int batch);
+int fhe_hmult_relin(const FheContext* ctx, int level, const uint64_t* x, const uint64_t* y,
+                    int64_t in_stride, const uint64_t* key, uint64_t* out0, uint64_t* out1,
+                    int64_t out_stride, int batch, void* workspace, size_t ws_bytes,
+                    void* stream);
+
 /* ---- BEHZ BFV multiplication (schemes/behz.py:58-270).  `big` is the
  *      chain Q | B | m_sk (L + S primes, S = |B| + 1).  Coefficient domain.
  *      lift : in (polys, L, n) -> out (polys, L + S, n)   extend_to_bsk

@@ -48,6 +48,9 @@ SIGNATURES = {
     "fhe_behz_floor": (_int, [_vp, _u64p, _u64p, _int, _int, _int, _u64p, _vp]),
     "fhe_keyswitch": (_int, [_vp, _int, _u64p, _i64, _u64p, _u64p, _u64p, _i64, _u64p, _u64p,
                              _i64, _int, _vp, _sz, _vp]),
+    "fhe_hmult_relin_workspace": (_sz, [_vp, _int, _int]),
+    "fhe_hmult_relin": (_int, [_vp, _int, _u64p, _u64p, _i64, _u64p, _u64p, _u64p, _i64, _int,
+                               _vp, _sz, _vp]),
 }
 
 

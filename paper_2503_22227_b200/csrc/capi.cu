@@ -247,4 +247,23 @@ int fhe_keyswitch(const FheContext* ctx, int level, const uint64_t* d, int64_t d
   })
 }
 
+size_t fhe_hmult_relin_workspace(const FheContext* ctx, int level, int batch) {
+  if (!ctx || level < 1 || level > ctx->L || batch < 1) return 0;
+  return hmult_relin_workspace(*ctx, level, batch);
+}
+
+int fhe_hmult_relin(const FheContext* ctx, int level, const uint64_t* x, const uint64_t* y,
+                    int64_t in_stride, const uint64_t* key, uint64_t* out0, uint64_t* out1,
+                    int64_t out_stride, int batch, void* workspace, size_t ws_bytes,
+                    void* stream) {
+  if (!ctx || !x || !y || !key || !out0 || !out1 || batch < 1) {
+    fhe_set_error("fhe_hmult_relin: bad arguments");
+    return -1;
+  }
+  FHE_TRY({
+    return run_hmult_relin(*ctx, level, x, y, in_stride, key, out0, out1, out_stride, batch,
+                           workspace, ws_bytes, (cudaStream_t)stream);
+  })
+}
+
 }  // extern "C"

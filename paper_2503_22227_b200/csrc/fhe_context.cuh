@@ -65,7 +65,12 @@ const PlainPlan* get_plain_plan(FheContext* ctx, u64 t);
 size_t keyswitch_workspace(const FheContext& ctx, int level, int batch);
 int run_keyswitch(const FheContext& ctx, int level, const u64* d, long d_stride, const u64* key,
                   const u64* add0, const u64* add1, long add_stride, u64* out0, u64* out1,
-                  long out_stride, int batch, void* ws, size_t ws_bytes, cudaStream_t st);
+                  long out_stride, int batch, void* ws, size_t ws_bytes, cudaStream_t st,
+                  bool tens = false);
+size_t hmult_relin_workspace(const FheContext& ctx, int level, int batch);
+int run_hmult_relin(const FheContext& ctx, int level, const u64* x, const u64* y, long in_stride,
+                    const u64* key, u64* out0, u64* out1, long out_stride, int batch, void* ws,
+                    size_t ws_bytes, cudaStream_t st);
 size_t rescale_workspace(const FheContext& ctx, int polys, int level);
 int run_rescale(FheContext& ctx, u64* out, const u64* in, int polys, int level, u64 t_plain,
                 void* ws, size_t ws_bytes, cudaStream_t st);

@@ -24,6 +24,9 @@ constexpr int kMaxAlpha = 16;
 #ifndef FHE_INNER_BU
 #define FHE_INNER_BU 2
 #endif
+#ifndef FHE_TENS_MINB
+#define FHE_TENS_MINB 2
+#endif
 #ifndef FHE_FIN_MINB
 #define FHE_FIN_MINB 3
 #endif
@@ -484,8 +487,13 @@ __global__ void __launch_bounds__(kThreads, FHE_MODUP_MINB)
 // storing accQ the ModDown finish is applied in place of moddown_finish_kernel:
 // out = add + (acc - conv) P^-1 (conv = the NTT'd P->Q conversion), so accQ
 // never round-trips HBM.
-template <int kD, bool FIN = false>
-__global__ void __launch_bounds__(kThreads, FIN ? FHE_FIN_MINB : FHE_INNER_MINB)
+// TENS (fused HMult+Relin, with FIN): add0/add1 are the two input ciphertexts
+// x, y ((2, level, n) each, add_stride apart); the tensor terms
+// d0 = x0 y0, d1 = x0 y1 + x1 y0 and the own-digit word d2 = x1 y1 are formed
+// here from the inputs (ckks.py ckks_multiply), so d0/d1 never touch HBM.
+template <int kD, bool FIN = false, bool TENS = false>
+__global__ void __launch_bounds__(kThreads, TENS  ? FHE_TENS_MINB
+                                            : (FIN ? FHE_FIN_MINB : FHE_INNER_MINB))
     ks_inner_fp_kernel(const DevChain ch, const u64* __restrict__ d, long d_stride,
                        const u64* __restrict__ ext, long ext_stride, const u64* __restrict__ key,
                        int keyL, const int* __restrict__ dig_info, int D, int level, int K, int L,
@@ -510,6 +518,7 @@ __global__ void __launch_bounds__(kThreads, FIN ? FHE_FIN_MINB : FHE_INNER_MINB)
     double2 kb[kD], ka[kD];
     const u64* src[kD];
     long sstr[kD];
+    int own_di = -1;
 #pragma unroll
     for (int di = 0; di < kD; ++di) {
       if (di < D) {
@@ -519,6 +528,7 @@ __global__ void __launch_bounds__(kThreads, FIN ? FHE_FIN_MINB : FHE_INNER_MINB)
         ka[di] = make_double2(a, __dmul_rn(a, qd.y));
         const int s0 = sinfo[4 * di], na = sinfo[4 * di + 1], ro = sinfo[4 * di + 2];
         const bool own = m >= s0 && m < s0 + na;
+        if (own) own_di = di;
         src[di] = own ? d + (long)m * n + i : ext + (long)(ro + (m < s0 ? m : m - na)) * n + i;
         sstr[di] = own ? d_stride : ext_stride;
       }
@@ -527,19 +537,30 @@ __global__ void __launch_bounds__(kThreads, FIN ? FHE_FIN_MINB : FHE_INNER_MINB)
       u64 v[FHE_INNER_BU][kD];
       // FIN: the finish operands are loaded with the digits (all in flight)
       u64 cv[FIN ? FHE_INNER_BU : 1][2], av[FIN ? FHE_INNER_BU : 1][2];
+      u64 tx[TENS ? FHE_INNER_BU : 1][2], ty[TENS ? FHE_INNER_BU : 1][2];
 #pragma unroll
       for (int u = 0; u < FHE_INNER_BU; ++u) {
 #pragma unroll
         for (int di = 0; di < kD; ++di)
-          if (di < D && b0 + u < batch) v[u][di] = __ldg(src[di] + (b0 + u) * sstr[di]);
+          if (di < D && b0 + u < batch && !(TENS && di == own_di))
+            v[u][di] = __ldg(src[di] + (b0 + u) * sstr[di]);
         if constexpr (FIN) {
           if (b0 + u < batch) {
             const int bb = b0 + u;
             const long w = (long)m * n + i;
             cv[u][0] = conv[((long)(bb * 2 + 0) * level + m) * n + i];
             cv[u][1] = conv[((long)(bb * 2 + 1) * level + m) * n + i];
-            av[u][0] = add0 ? add0[bb * add_stride + w] : 0;
-            av[u][1] = add1 ? add1[bb * add_stride + w] : 0;
+            if constexpr (TENS) {
+              const u64* xb = add0 + bb * add_stride + w;
+              const u64* yb = add1 + bb * add_stride + w;
+              tx[u][0] = __ldg(xb);
+              tx[u][1] = __ldg(xb + (long)level * n);
+              ty[u][0] = __ldg(yb);
+              ty[u][1] = __ldg(yb + (long)level * n);
+            } else {
+              av[u][0] = add0 ? add0[bb * add_stride + w] : 0;
+              av[u][1] = add1 ? add1[bb * add_stride + w] : 0;
+            }
           }
         }
       }
@@ -547,11 +568,21 @@ __global__ void __launch_bounds__(kThreads, FIN ? FHE_FIN_MINB : FHE_INNER_MINB)
       for (int u = 0; u < FHE_INNER_BU; ++u) {
         if (b0 + u >= batch) break;
         const int b = b0 + u;
+        u64 d2 = 0;
+        if constexpr (TENS) {
+          const ModConst mc = ch.mc[p];
+          u64 h, l;
+          av[u][0] = mul_mod(tx[u][0], ty[u][0], mc);
+          mul_wide(tx[u][0], ty[u][1], h, l);
+          mac_wide(h, l, tx[u][1], ty[u][0]);
+          av[u][1] = reduce_prod(h, l, mc);
+          d2 = mul_mod(tx[u][1], ty[u][1], mc);
+        }
         double sb = 0.0, sa = 0.0;
 #pragma unroll
         for (int di = 0; di < kD; ++di) {
           if (di < D) {
-            const double x = fp_from_u52(v[u][di]);
+            const double x = fp_from_u52((TENS && di == own_di) ? d2 : v[u][di]);
             sb = __dadd_rn(sb, fp_mulmod(x, kb[di], qd.x));
             sa = __dadd_rn(sa, fp_mulmod(x, ka[di], qd.x));
           }
@@ -563,8 +594,8 @@ __global__ void __launch_bounds__(kThreads, FIN ? FHE_FIN_MINB : FHE_INNER_MINB)
           const long w = (long)m * n + i;
           u64 v0 = shoup_mul(sub_mod(rb, cv[u][0], q), pi.w, pi.sh, q);
           u64 v1 = shoup_mul(sub_mod(ra, cv[u][1], q), pi.w, pi.sh, q);
-          if (add0) v0 = add_mod(av[u][0], v0, q);
-          if (add1) v1 = add_mod(av[u][1], v1, q);
+          if (TENS || add0) v0 = add_mod(av[u][0], v0, q);
+          if (TENS || add1) v1 = add_mod(av[u][1], v1, q);
           out0[b * out_stride + w] = v0;
           out1[b * out_stride + w] = v1;
           continue;
@@ -684,9 +715,17 @@ size_t keyswitch_workspace(const FheContext& ctx, int level, int batch) {
   return rows * n * sizeof(u64);
 }
 
+// The fused inner-product/finish kernel handles this level (FP64 chain, hybrid
+// key with at most 4 digits, not disabled by FHE_FUSE_INNER_FINISH=0).
+static bool fin_inner_path(const FheContext& ctx, int level) {
+  return ctx.K > 0 && ctx.chain->dev.fp64_ok && ctx.levels[level].digits <= 4 &&
+         fin_inner_enabled();
+}
+
 int run_keyswitch(const FheContext& ctx, int level, const u64* d, long d_stride, const u64* key,
                   const u64* add0, const u64* add1, long add_stride, u64* out0, u64* out1,
-                  long out_stride, int batch, void* ws, size_t ws_bytes, cudaStream_t st) {
+                  long out_stride, int batch, void* ws, size_t ws_bytes, cudaStream_t st,
+                  bool tens) {
   if (level < 1 || level > ctx.L) {
     fhe_set_error("keyswitch level out of range");
     return -1;
@@ -752,7 +791,11 @@ int run_keyswitch(const FheContext& ctx, int level, const u64* d, long d_stride,
   // 3. inner product with the key digits (K == 0 writes the result directly).
   // With the fused finish (FP64 path, <= 4 digits, K > 0) only the P limbs
   // are produced here; the Q limbs are folded into the ModDown finish below.
-  const bool fin_inner = K > 0 && ch.fp64_ok && lp.digits <= 4 && fin_inner_enabled();
+  const bool fin_inner = fin_inner_path(ctx, level);
+  if (tens && !fin_inner) {
+    fhe_set_error("keyswitch: tensor inputs need the fused finish path");
+    return -1;
+  }
   {
     const int m_end = level + K, m_begin = fin_inner ? level : 0;
     const long work = (long)(m_end - m_begin) << log_n;
@@ -821,9 +864,15 @@ int run_keyswitch(const FheContext& ctx, int level, const u64* d, long d_stride,
           K, L, nullptr, nullptr, add0, add1, add_stride, out0, out1, out_stride, batch, 0, level,
           conv, lp.p_inv);
     };
-    if (lp.digits <= 2) go(ks_inner_fp_kernel<2, true>);
-    else if (lp.digits == 3) go(ks_inner_fp_kernel<3, true>);
-    else go(ks_inner_fp_kernel<4, true>);
+    if (tens) {
+      if (lp.digits <= 2) go(ks_inner_fp_kernel<2, true, true>);
+      else if (lp.digits == 3) go(ks_inner_fp_kernel<3, true, true>);
+      else go(ks_inner_fp_kernel<4, true, true>);
+    } else {
+      if (lp.digits <= 2) go(ks_inner_fp_kernel<2, true>);
+      else if (lp.digits == 3) go(ks_inner_fp_kernel<3, true>);
+      else go(ks_inner_fp_kernel<4, true>);
+    }
     FHE_LAUNCH_CHECK();
     return 0;
   }
@@ -831,6 +880,78 @@ int run_keyswitch(const FheContext& ctx, int level, const u64* d, long d_stride,
       ch, accQ, conv, lp.p_inv, add0, add1, add_stride, out0, out1, out_stride, level, batch);
   FHE_LAUNCH_CHECK();
   return 0;
+}
+
+// d2 = x1 * y1 of the tensor product only (the key switch's input); d0/d1 are
+// formed inside the fused finish.  One read of x1, y1 and one write of d2.
+__global__ void __launch_bounds__(kThreads)
+    tensor_d2_kernel(const DevChain ch, u64* __restrict__ d2, const u64* __restrict__ x,
+                     const u64* __restrict__ y, int level, int log_n, long batch, long in_stride) {
+  const long n = 1L << log_n;
+  const long per = (long)level << (log_n - 1);  // coefficient pairs per poly
+  for (long t = blockIdx.x * (long)blockDim.x + threadIdx.x; t < batch * per;
+       t += (long)gridDim.x * blockDim.x) {
+    const long bi = t / per;
+    const long w = t - bi * per;
+    const ModConst m = ch.mc[(int)(w >> (log_n - 1))];
+    const ulonglong2 a = reinterpret_cast<const ulonglong2*>(x + bi * in_stride + level * n)[w];
+    const ulonglong2 b = reinterpret_cast<const ulonglong2*>(y + bi * in_stride + level * n)[w];
+    reinterpret_cast<ulonglong2*>(d2 + bi * level * n)[w] =
+        make_ulonglong2(mul_mod(a.x, b.x, m), mul_mod(a.y, b.y, m));
+  }
+}
+
+// Opt-in (FHE_HMULT_TENS=1): form d0/d1/d2 inside the fused finish kernel.
+// It saves three polynomials of HBM traffic per op but moves ~40 integer
+// instructions per word into the FP64-bound finishing kernel: measured 1.4%
+// slower (profiles/r1_ntt_notes.md), so the default materialises the tensor.
+static bool hmult_tens_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("FHE_HMULT_TENS");
+    on = (e && e[0] == '1') ? 1 : 0;
+  }
+  return on == 1;
+}
+
+size_t hmult_relin_workspace(const FheContext& ctx, int level, int batch) {
+  const size_t n = (size_t)1 << ctx.chain->log_n;
+  return keyswitch_workspace(ctx, level, batch) + (size_t)batch * 3 * level * n * sizeof(u64);
+}
+
+// HMult+Relin in one call (ckks_multiply then ckks_relinearize, ckks.py):
+// x, y are batch x (2, level, n) evaluation-domain ciphertexts in_stride words
+// apart; out0/out1 receive the relinearized (c0, c1).  Default: the tensor
+// goes to the workspace and the key switch runs on it; FHE_HMULT_TENS=1 only
+// materialises d2 and forms d0/d1 in the finishing kernel.  Same words.
+int run_hmult_relin(const FheContext& ctx, int level, const u64* x, const u64* y, long in_stride,
+                    const u64* key, u64* out0, u64* out1, long out_stride, int batch, void* ws,
+                    size_t ws_bytes, cudaStream_t st) {
+  if (level < 1 || level > ctx.L) {
+    fhe_set_error("hmult_relin level out of range");
+    return -1;
+  }
+  if (ws_bytes < hmult_relin_workspace(ctx, level, batch)) {
+    fhe_set_error("hmult_relin workspace too small");
+    return -1;
+  }
+  const DevChain& ch = ctx.chain->dev;
+  const long n = 1L << ch.log_n;
+  const size_t ks_bytes = keyswitch_workspace(ctx, level, batch);
+  u64* t = (u64*)((char*)ws + ks_bytes);
+  if (hmult_tens_enabled() && fin_inner_path(ctx, level)) {
+    const long work = (long)batch * level << (ch.log_n - 1);
+    tensor_d2_kernel<<<grid_for(work), kThreads, 0, st>>>(ch, t, x, y, level, ch.log_n, batch,
+                                                          in_stride);
+    FHE_LAUNCH_CHECK();
+    return run_keyswitch(ctx, level, t, (long)level * n, key, x, y, in_stride, out0, out1,
+                         out_stride, batch, ws, ks_bytes, st, true);
+  }
+  const long poly = (long)level * n;
+  int rc = launch_tensor(ch, t, x, y, level, batch, in_stride, in_stride, 3 * poly, 0, st);
+  if (rc) return rc;
+  return run_keyswitch(ctx, level, t + 2 * poly, 3 * poly, key, t, t + poly, 3 * poly, out0,
+                       out1, out_stride, batch, ws, ks_bytes, st, false);
 }
 
 size_t rescale_workspace(const FheContext& ctx, int polys, int level) {

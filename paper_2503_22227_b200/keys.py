@@ -218,6 +218,26 @@ def key_switch_into(ctx: Context, level: int, d, ksk: KSwitchKey, out0, out1, ad
         "fhe_keyswitch")
 
 
+def hmult_relin_into(ctx: Context, level: int, x, y, rlk: KSwitchKey, out0, out1,
+                     batch: int = 1, in_stride: int | None = None,
+                     out_stride: int | None = None, stream=None):
+    """Fused tensor product + relinearization (fhe_hmult_relin): x, y are batch
+    x (2, level, n) ciphertexts in_stride words apart (y may be x); out0/out1
+    receive d0 + b and d1 + a -- the words of ckks_multiply followed by
+    ckks_relinearize (ckks.py:308-379)."""
+    if level > ctx.L or level < 1:
+        raise LevelMismatch(f"polynomial level {level} exceeds key level")
+    lib = _native.lib()
+    n = ctx.n
+    ws_bytes = lib.fhe_hmult_relin_workspace(ctx.handle, level, batch)
+    ws = ctx.workspace(ws_bytes, "hmult_relin")
+    _native.check(lib.fhe_hmult_relin(
+        ctx.handle, level, _native.ptr(x), _native.ptr(y), in_stride or 2 * level * n,
+        rlk.data._buf.data_ptr(), _native.ptr(out0), _native.ptr(out1),
+        out_stride or 2 * level * n, batch, ws.data_ptr(), ws_bytes,
+        _native.stream_handle(stream)), "fhe_hmult_relin")
+
+
 def key_switch(ctx: Context, rows, ksk: KSwitchKey):
     """Apply a key-switch key to an evaluation-domain (level, n) polynomial;
     returns (b_rows, a_rows) on the device (keys.py:186-237)."""

@@ -25,8 +25,8 @@ from ..context import Context
 from ..coremath.crt import crt_centered_floats
 from ..coremath.modmath import ParameterError
 from ..coremath.sampling import Rng, fresh_seed, signed_to_residues
-from ..keys import (KSwitchKey, PublicKey, SecretKey, automorph_rows, key_switch_into,
-                    signed_eval, upload_rows)
+from ..keys import (KSwitchKey, PublicKey, SecretKey, automorph_rows, hmult_relin_into,
+                    key_switch_into, signed_eval, upload_rows)
 from ..rnspoly import CData, Domain, cdata_new, ew
 
 SCALE_RTOL = 1e-6
@@ -380,6 +380,23 @@ def ckks_relinearize(ctx: Context, ct: CkksCiphertext, rlk: KSwitchKey) -> CkksC
     o = out.view()
     key_switch_into(ctx, level, v[2], rlk, o[0], o[1], add0=v[0], add1=v[1])
     return CkksCiphertext(out, ct.scale, level)
+
+
+def ckks_multiply_relinearize(ctx: Context, a: CkksCiphertext, b: CkksCiphertext | None,
+                              rlk: KSwitchKey) -> CkksCiphertext:
+    """ckks_relinearize(ckks_multiply(a, b)) (or of ckks_square(a) when b is
+    None) in one fused call (fhe_hmult_relin): the same words, without the
+    3-component intermediate in HBM."""
+    if b is None:
+        b = a
+    _check_pair(a, b)
+    if a.data.size_poly != 2 or b.data.size_poly != 2:
+        raise ParameterError("multiply requires 2-component operands")
+    level = a.level
+    out = _new_ct(ctx, 2, level)
+    o = out.view()
+    hmult_relin_into(ctx, level, a.data.view(), b.data.view(), rlk, o[0], o[1])
+    return CkksCiphertext(out, a.scale * b.scale, level)
 
 
 def _rescale_data(ctx: Context, data: CData, level: int, t_plain: int = 0) -> CData:

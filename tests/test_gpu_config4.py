@@ -99,6 +99,40 @@ def test_hybrid_hmult_relin_rescale_bit_exact_vs_oracle(hybrid, golden):
     assert err <= golden["ckks_c4"]["err_mul"] + 2.0 ** -20, err
 
 
+def test_fused_hmult_relin_bit_exact(hybrid):
+    """fhe_hmult_relin (tensor product formed inside the key switch's finishing
+    kernel) gives the words of ckks_multiply + ckks_relinearize: full level,
+    squaring, and a batch of 3 at a lower level (ragged last digit)."""
+    import torch
+
+    from paper_2503_22227_b200.keys import hmult_relin_into
+    from paper_2503_22227_b200.schemes import ckks
+
+    ctx, rlk = hybrid["ctx"], hybrid["rlk"]
+    vr = np.random.default_rng(19)
+    cts = [ckks.ckks_encrypt(ctx, ckks.ckks_encode(ctx, vr.uniform(-1, 1, ctx.n // 2)),
+                             hybrid["pk"], seeded_rng(60 + i)) for i in range(4)]
+    want = ckks.ckks_relinearize(ctx, ckks.ckks_multiply(ctx, cts[0], cts[1]), rlk)
+    got = ckks.ckks_multiply_relinearize(ctx, cts[0], cts[1], rlk)
+    assert got.scale == want.scale and got.level == want.level
+    assert torch.equal(got.data.view(), want.data.view())
+    sq_want = ckks.ckks_relinearize(ctx, ckks.ckks_square(ctx, cts[2]), rlk)
+    sq_got = ckks.ckks_multiply_relinearize(ctx, cts[2], None, rlk)
+    assert torch.equal(sq_got.data.view(), sq_want.data.view())
+    # batch of 3 pairs at level 17 (digits 10 + 7), stacked (B, 2, level, n)
+    lv = 17
+    low = [ckks.CkksCiphertext(ckks.CData.wrap(c.data.view()[:, :lv].contiguous().reshape(-1), 2,
+                                               lv, ctx.n, ckks.Domain.EVALUATION), c.scale, lv)
+           for c in cts]
+    X = torch.stack([low[i].data.view() for i in (0, 1, 2)])
+    Y = torch.stack([low[i].data.view() for i in (3, 0, 1)])
+    out = torch.empty_like(X)
+    hmult_relin_into(ctx, lv, X, Y, rlk, out[:, 0], out[:, 1], batch=3)
+    for b, (i, j) in enumerate(((0, 3), (1, 0), (2, 1))):
+        ref = ckks.ckks_relinearize(ctx, ckks.ckks_multiply(ctx, low[i], low[j]), rlk)
+        assert torch.equal(out[b], ref.data.view()), b
+
+
 def test_hybrid_boosted_rotate_within_tolerance(hybrid):
     from paper_2503_22227_b200.schemes import ckks
 
@@ -153,3 +187,45 @@ print(hashlib.sha256(out.data.view().cpu().numpy().tobytes()).hexdigest())
         digests.append(out.stdout.strip().splitlines()[-1])
     assert digests[0] == digests[1]
     del hashlib
+
+
+def test_fused_hmult_relin_switches():
+    """fhe_hmult_relin with the tensor formed inside the finishing kernel
+    (FHE_HMULT_TENS=1), with the default materialised tensor, and with the
+    fused inner/finish kernel disabled (FHE_FUSE_INNER_FINISH=0, the TENS
+    request then falls back): every product and square is the same words as
+    ckks_multiply/ckks_square + ckks_relinearize."""
+    import os
+    import subprocess
+    import sys
+
+    code = r'''
+import hashlib, numpy as np, torch
+from paper_2503_22227_b200.context import Context, PoolConfig, hybrid_params
+from paper_2503_22227_b200.coremath.sampling import Rng
+from paper_2503_22227_b200.keys import keygen, pk_gen, relin_keygen
+from paper_2503_22227_b200.schemes import ckks
+ctx = Context(hybrid_params(1 << 16, 30, bits=50, special=10, special_bits=50, dnum=3,
+                            scale=float(2 ** 49)), PoolConfig(unit_mb=200, cap_mb=4096))
+seed = lambda s: Rng(int(s).to_bytes(32, "little"))
+sk = keygen(ctx, seed(4)); pk = pk_gen(ctx, sk, seed(41)); rlk = relin_keygen(ctx, sk, seed(42))
+r = np.random.default_rng(9)
+x = ckks.ckks_encrypt(ctx, ckks.ckks_encode(ctx, r.uniform(-1, 1, ctx.n // 2)), pk, seed(43))
+y = ckks.ckks_encrypt(ctx, ckks.ckks_encode(ctx, r.uniform(-1, 1, ctx.n // 2)), pk, seed(44))
+a = ckks.ckks_relinearize(ctx, ckks.ckks_multiply(ctx, x, y), rlk)
+b = ckks.ckks_multiply_relinearize(ctx, x, y, rlk)
+c = ckks.ckks_relinearize(ctx, ckks.ckks_square(ctx, x), rlk)
+d = ckks.ckks_multiply_relinearize(ctx, x, None, rlk)
+h = lambda c: hashlib.sha256(c.data.view().cpu().numpy().tobytes()).hexdigest()
+assert h(a) == h(b) and h(c) == h(d)
+print(h(a), h(c))
+'''
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    digests = set()
+    for fin, tens in (("1", "1"), ("1", "0"), ("0", "1")):
+        env = dict(os.environ, FHE_FUSE_INNER_FINISH=fin, FHE_HMULT_TENS=tens, PYTHONPATH=root)
+        out = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True,
+                             text=True, timeout=900)
+        assert out.returncode == 0, out.stderr[-2000:]
+        digests.add(out.stdout.strip().splitlines()[-1])
+    assert len(digests) == 1, digests

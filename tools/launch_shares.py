@@ -25,7 +25,7 @@ def main(path: str, out: str | None = None):
         launches.setdefault(r[ii], {"name": r[ki]})[r[mi]] = float(r[vi].replace(",", ""))
     items = list(launches.values())
     names = [short(x["name"]) for x in items]
-    tens = [i for i, n in enumerate(names) if n.startswith("tensor_kernel")]
+    tens = [i for i, n in enumerate(names) if n.startswith("tensor_")]
     # the list is either a whole run (warm-up + 2 timed steps + later phases:
     # take the last two steps before the first non-step kernel) or an
     # nvtx-filtered "timed/" list (the 2 timed batched steps come first)
@@ -33,16 +33,16 @@ def main(path: str, out: str | None = None):
     start = tens[0] if nvtx_first else (tens[-2] if len(tens) >= 2 else 0)
     end = len(items)
     for i in range(start + 1, len(items)):
-        if names[i].startswith("tensor_kernel") and i > tens[-1]:
+        if names[i].startswith("tensor_") and i > tens[-1]:
             end = i
             break
     # stop at the first non key-switch kernel after the last step (e2e / NTT phases)
     agg, cnt, byt = defaultdict(float), defaultdict(int), defaultdict(float)
     tot = 0.0
-    step_kernels = ("tensor_kernel", "ntt_tiles", "ntt_tma", "ntt_fused", "modup", "ks_inner", "moddown")
+    step_kernels = ("tensor_", "ntt_tiles", "ntt_tma", "ntt_fused", "modup", "ks_inner", "moddown")
     seen_tensor = 0
     for it, n in zip(items[start:], names[start:]):
-        if n.startswith("tensor_kernel"):
+        if n.startswith("tensor_"):
             seen_tensor += 1
             if seen_tensor > 2:
                 break
