@@ -82,13 +82,20 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     return lib
 
 
-def lib() -> ctypes.CDLL:
-    """Library handle for compute calls: requires a CUDA device."""
-    import torch
+_device_ok = False
 
-    if not torch.cuda.is_available():
-        raise NativeUnavailable("no CUDA device: the B200 path has no CPU fallback")
-    return load_library()
+
+def lib() -> ctypes.CDLL:
+    """Library handle for compute calls: requires a CUDA device (probed once;
+    the answer cannot change inside a process)."""
+    global _device_ok
+    if not _device_ok:
+        import torch
+
+        if not torch.cuda.is_available():
+            raise NativeUnavailable("no CUDA device: the B200 path has no CPU fallback")
+        _device_ok = True
+    return _lib if _lib is not None else load_library()
 
 
 def check(rc: int, what: str):
@@ -98,10 +105,13 @@ def check(rc: int, what: str):
 
 
 def stream_handle(stream=None) -> int:
+    """cudaStream_t of `stream`, else of torch's current stream on the current
+    device (read through torch's raw accessor: no Stream object per call)."""
     import torch
 
-    s = stream if stream is not None else torch.cuda.current_stream()
-    return s.cuda_stream
+    if stream is not None:
+        return stream.cuda_stream
+    return torch._C._cuda_getCurrentRawStream(torch._C._cuda_getDevice())
 
 
 def ptr(t) -> int:

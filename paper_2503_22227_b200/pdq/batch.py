@@ -98,25 +98,33 @@ class BatchEval:
 
         ew(self.ctx.chain, op, out, a, bb, None, rows=rows, limbs=level)
 
-    def _const_block(self, values, level: int, scale: float, both: bool, key):
+    def _const_block(self, kind: str, values, level: int, scale: float, both: bool, key):
         """(B, 2, level, N) block of per-unit plaintexts: [pt_i, pt_i] (both)
-        or [pt_i, 0]."""
-        import torch
+        or [pt_i, 0].  Blocks are read-only inputs of the element-wise ops and
+        every query uses the same constants, so they are kept in the
+        context's plaintext LRU (schemes/ckks.py PlaintextCache)."""
+        from ..schemes.ckks import plaintext_cache
 
-        n = self.ctx.n
-        blk = torch.zeros((len(values), 2, level, n), dtype=torch.int64, device="cuda")
-        for i, z in enumerate(values):
-            pt = key(z, level, scale)
-            blk[i, 0].copy_(pt.data.view()[0])
-            if both:
-                blk[i, 1].copy_(pt.data.view()[0])
-        return blk
+        def make():
+            import torch
+
+            n = self.ctx.n
+            blk = torch.zeros((len(values), 2, level, n), dtype=torch.int64, device="cuda")
+            for i, z in enumerate(values):
+                pt = key(z, level, scale)
+                blk[i, 0].copy_(pt.data.view()[0])
+                if both:
+                    blk[i, 1].copy_(pt.data.view()[0])
+            return blk
+
+        ck = ("block", kind, tuple(complex(v) for v in values), level, float(scale), both)
+        return plaintext_cache(self.ctx).get(ck, make)
 
     def _mul_scalar_raw(self, b: CtBatch, zs, scale: float) -> CtBatch:
         """ckks_multiply_scalar per unit (plaintext Re z + Im z X^(n/2) at
         `scale`), keeping the product scale b.scale * scale."""
         out = CtBatch(self._new(b.count, 2, b.level), b.count, b.level, b.scale * scale)
-        blk = self._const_block(zs, b.level, scale, True,
+        blk = self._const_block("scalar", zs, b.level, scale, True,
                                 lambda z, lv, s: scalar_plaintext(self.ctx, complex(z), s, lv))
         self._ew(_native.EW_MUL, out.data._buf, b.data._buf, blk, b.count * 2 * b.level, b.level)
         return out
@@ -162,7 +170,7 @@ class BatchEval:
             return ev._encode_cached(("const", complex(c)),
                                      np.full(ev.slots, c, dtype=np.complex128), lv, s)
 
-        blk = self._const_block(cs, b.level, b.scale, False, pt)
+        blk = self._const_block("const", cs, b.level, b.scale, False, pt)
         out = CtBatch(self._new(b.count, 2, b.level), b.count, b.level, b.scale)
         self._ew(_native.EW_ADD, out.data._buf, b.data._buf, blk, b.count * 2 * b.level, b.level)
         return out
