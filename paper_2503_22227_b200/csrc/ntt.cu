@@ -332,10 +332,10 @@ __global__ void __launch_bounds__(Tile::THREADS, Tile::MINB)
 #define FHE_FUSE_MAX_LOG_R 4
 #endif
 #ifndef FHE_FUSE_MIN_LOG_R
-#define FHE_FUSE_MIN_LOG_R 4
+#define FHE_FUSE_MIN_LOG_R 3
 #endif
 #ifndef FHE_FUSE_LAG
-#define FHE_FUSE_LAG 8
+#define FHE_FUSE_LAG 16
 #endif
 constexpr int kFuseLag = FHE_FUSE_LAG;
 constexpr int kFuseSlabs = 8;
@@ -937,8 +937,9 @@ int launch_split(const DevChain& ch, const NttArgs& a, bool inverse, bool lazy,
   const bool use_ktma = (LOG_N - LOG_N1 == 8) && ch.fp64_ok && kstage && tma_enabled() &&
                         a.rows % a.map.limbs == 0 && std::getenv("FHE_NTT_KTMA") == nullptr;
   if constexpr (LOG_N1 == 8 && LOG_N - LOG_N1 == 8) {
-    // fused only for 16-row groups (one chunk per tile): measured faster
-    // there (5120-row sweep +3-6%), slower for 8-row groups (key-switch ModUp)
+    // fused for groups of >= 8 rows of one residue class: with the second
+    // phase 16 groups behind the first, the key switch's 8-row groups (input
+    // INTT, ModUp NTT) gain too (HMult+Relin +2.5%); at lag 8 they lost 15%
     if (use_tma && use_ktma && ch.fuse && fused_tma_enabled() && kt.log_r >= FHE_FUSE_MIN_LOG_R &&
         !a.fin) {
       ColsTmaTile<LOG_N, LOG_N1> tc;
