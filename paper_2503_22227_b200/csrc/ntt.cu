@@ -338,6 +338,9 @@ __global__ void __launch_bounds__(Tile::THREADS, Tile::MINB)
 #define FHE_FUSE_LAG 16
 #endif
 constexpr int kFuseLag = FHE_FUSE_LAG;
+#ifndef FHE_FUSE_CTAS
+#define FHE_FUSE_CTAS 5
+#endif
 constexpr int kFuseSlabs = 8;
 
 struct FusePlan {
@@ -451,7 +454,7 @@ __global__ void __launch_bounds__(kSplitThreads, kSplitMinB)
 // The signal of a CTA's last first-phase tile is flushed before the CTA
 // waits on anything, so no CTA can wait on its own pending signal.
 template <class CT, class KT, bool FWD>
-__global__ void __launch_bounds__(kSplitThreads, 5)
+__global__ void __launch_bounds__(kSplitThreads, FHE_FUSE_CTAS)
     ntt_fused_tma_kernel(const DevChain ch, const __grid_constant__ CUtensorMap cs_map,
                          const __grid_constant__ CUtensorMap cd_map,
                          const __grid_constant__ CUtensorMap ks_map,
@@ -830,7 +833,7 @@ int launch_fused_tma(const DevChain& ch, u64* dst, const u64* src, const CT& ct,
   constexpr int SW = CT::SMEM_WORDS > KT::SMEM_WORDS ? CT::SMEM_WORDS : KT::SMEM_WORDS;
   constexpr int TW = CT::TWMAX > KT::TWMAX ? CT::TWMAX : KT::TWMAX;
   constexpr int smem = SW * sizeof(u64) + TW * sizeof(double2) + 16;
-  const int grid = std::min(fp.total, 5 * sm_count());
+  const int grid = std::min(fp.total, FHE_FUSE_CTAS * sm_count());
   auto go = [&](auto kern) {
     static bool attr = false;
     if (!attr) {
