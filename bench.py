@@ -427,7 +427,10 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--batch", type=int, default=8)
+    # resident ciphertext pairs per step: 16 keeps the row groups of one
+    # residue class at 32 rows for the fused NTT (batch 4/8/16/32: 4030 /
+    # 4846 / 5151 / 5230 ops/s, profiles/r1_ntt_notes.md)
+    ap.add_argument("--batch", type=int, default=16)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-pdq", action="store_true")
@@ -511,7 +514,7 @@ def main():
         "config": {"workload": "config 4: CKKS HMult+Relin, N=2^16, L=30 x 50-bit, "
                                "P=10 x 50-bit, dnum=3 (hybrid), Delta=2^49",
                    "batch_per_gpu": B, "ops_per_step": B * world,
-                   "l2": "inputs larger than L2 (8 x 60 MiB pairs + 120 MiB key)"},
+                   "l2": f"inputs larger than L2 ({B} x 60 MiB pairs + 120 MiB key)"},
         "e2e": {"value": B * world / (e2e_ms / 1000.0), "unit": "ops/s",
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "path": "host_io.hmult_relin_host_batch: ckks_multiply + ckks_relinearize per "
