@@ -568,21 +568,25 @@ __global__ void __launch_bounds__(kThreads, TENS  ? FHE_TENS_MINB
       for (int u = 0; u < FHE_INNER_BU; ++u) {
         if (b0 + u >= batch) break;
         const int b = b0 + u;
-        u64 d2 = 0;
+        double d2 = 0.0;
         if constexpr (TENS) {
-          const ModConst mc = ch.mc[p];
-          u64 h, l;
-          av[u][0] = mul_mod(tx[u][0], ty[u][0], mc);
-          mul_wide(tx[u][0], ty[u][1], h, l);
-          mac_wide(h, l, tx[u][1], ty[u][0]);
-          av[u][1] = reduce_prod(h, l, mc);
-          d2 = mul_mod(tx[u][1], ty[u][1], mc);
+          // tensor terms on the FP64 pipe (idle in this HBM-bound kernel):
+          // exact products of canonical words as in the inner product below
+          const double a0 = fp_from_u52(tx[u][0]), a1 = fp_from_u52(tx[u][1]);
+          const double c0 = fp_from_u52(ty[u][0]), c1 = fp_from_u52(ty[u][1]);
+          const double2 w0 = make_double2(c0, __dmul_rn(c0, qd.y));
+          const double2 w1 = make_double2(c1, __dmul_rn(c1, qd.y));
+          av[u][0] = fp_canon_half(fp_reduce(fp_mulmod(a0, w0, qd.x), qd), qd.x);
+          av[u][1] = fp_canon_half(
+              fp_reduce(__dadd_rn(fp_mulmod(a0, w1, qd.x), fp_mulmod(a1, w0, qd.x)), qd), qd.x);
+          const double r2 = fp_reduce(fp_mulmod(a1, w1, qd.x), qd);
+          d2 = r2 < 0.0 ? __dadd_rn(r2, qd.x) : r2;
         }
         double sb = 0.0, sa = 0.0;
 #pragma unroll
         for (int di = 0; di < kD; ++di) {
           if (di < D) {
-            const double x = fp_from_u52((TENS && di == own_di) ? d2 : v[u][di]);
+            const double x = (TENS && di == own_di) ? d2 : fp_from_u52(v[u][di]);
             sb = __dadd_rn(sb, fp_mulmod(x, kb[di], qd.x));
             sa = __dadd_rn(sa, fp_mulmod(x, ka[di], qd.x));
           }
@@ -902,9 +906,10 @@ __global__ void __launch_bounds__(kThreads)
 }
 
 // Opt-in (FHE_HMULT_TENS=1): form d0/d1/d2 inside the fused finish kernel.
-// It saves three polynomials of HBM traffic per op but moves ~40 integer
-// instructions per word into the FP64-bound finishing kernel: measured 1.4%
-// slower (profiles/r1_ntt_notes.md), so the default materialises the tensor.
+// It saves three polynomials of HBM traffic per op, but the extra operands
+// cost the HBM-bound finishing kernel a CTA per SM: measured -0.4% at batch 8
+// and +0.5% at batch 16 (profiles/r1_ntt_notes.md), so the default keeps the
+// materialised tensor.
 static bool hmult_tens_enabled() {
   static int on = -1;
   if (on < 0) {
