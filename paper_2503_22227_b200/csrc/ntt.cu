@@ -185,11 +185,14 @@ struct ColsTmaTile : ColsTile<LOG_N, LOG_N1> {
     climb = this->row % this->map.limbs;
     cbat = this->row / this->map.limbs;
   }
+  uint64_t ld_pol = 0, st_pol = 0;  // L2 cache-hint policies (0: no hint)
   __device__ __forceinline__ void tma_load(u64* sm, uint64_t* bar) const {
-    tma_load_5d(sm, smap_p, 0, ccol, 0, climb, cbat, bar);
+    if (ld_pol) tma_load_5d_hint(sm, smap_p, 0, ccol, 0, climb, cbat, bar, ld_pol);
+    else tma_load_5d(sm, smap_p, 0, ccol, 0, climb, cbat, bar);
   }
   __device__ __forceinline__ void tma_store(const u64* sm) const {
-    tma_store_5d(dmap_p, 0, ccol, 0, climb, cbat, sm);
+    if (st_pol) tma_store_5d_hint(dmap_p, 0, ccol, 0, climb, cbat, sm, st_pol);
+    else tma_store_5d(dmap_p, 0, ccol, 0, climb, cbat, sm);
   }
 };
 
@@ -212,8 +215,13 @@ struct ChunksTmaTile : ChunksTile<LOG_N, LOG_N1> {
   const CUtensorMap* dmap_p = nullptr;
   bool has_fin = false;
   NttFinish fin{};
+  uint64_t ld_pol = 0, st_pol = 0;  // L2 cache-hint policies (0: no hint)
   __device__ __forceinline__ void tma_load(u64* sm, uint64_t* bar) const {
-    tma_load_4d(sm, smap_p, 0, this->c0 << (Base::LOG_S - 4), this->cls_, this->i0_, bar);
+    if (ld_pol)
+      tma_load_4d_hint(sm, smap_p, 0, this->c0 << (Base::LOG_S - 4), this->cls_, this->i0_, bar,
+                       ld_pol);
+    else
+      tma_load_4d(sm, smap_p, 0, this->c0 << (Base::LOG_S - 4), this->cls_, this->i0_, bar);
   }
   // ModDown finish from the swizzled result tile, 16 bytes per step: every
   // element is read once from smem, accQ and the add-in once from HBM, and
@@ -249,7 +257,11 @@ struct ChunksTmaTile : ChunksTile<LOG_N, LOG_N1> {
     }
   }
   __device__ __forceinline__ void tma_store(const u64* sm) const {
-    tma_store_4d(dmap_p, 0, this->c0 << (Base::LOG_S - 4), this->cls_, this->i0_, sm);
+    if (st_pol)
+      tma_store_4d_hint(dmap_p, 0, this->c0 << (Base::LOG_S - 4), this->cls_, this->i0_, sm,
+                        st_pol);
+    else
+      tma_store_4d(dmap_p, 0, this->c0 << (Base::LOG_S - 4), this->cls_, this->i0_, sm);
   }
 };
 
@@ -338,6 +350,9 @@ __global__ void __launch_bounds__(Tile::THREADS, Tile::MINB)
 #define FHE_FUSE_LAG 16
 #endif
 constexpr int kFuseLag = FHE_FUSE_LAG;
+#ifndef FHE_FUSE_L2HINT
+#define FHE_FUSE_L2HINT 0
+#endif
 #ifndef FHE_FUSE_CTAS
 #define FHE_FUSE_CTAS 5
 #endif
@@ -479,6 +494,13 @@ __global__ void __launch_bounds__(kSplitThreads, FHE_FUSE_CTAS)
   }
   __syncthreads();
   unsigned phase = 0;
+  // L2 priorities (FHE_FUSE_L2HINT): bit 0 -> loads evict_first (inputs and
+  // the intermediate are read once), bit 1 -> first-phase stores evict_last
+  // (the intermediate is re-read by the second phase a few groups later),
+  // bit 2 -> second-phase loads (of the intermediate) evict_first
+  const uint64_t pol_ld = (FHE_FUSE_L2HINT & 1) ? l2_policy_evict_first() : 0;
+  const uint64_t pol_mid = (FHE_FUSE_L2HINT & 2) ? l2_policy_evict_last() : 0;
+  const uint64_t pol_ld2 = (FHE_FUSE_L2HINT & 4) ? l2_policy_evict_first() : pol_ld;
   for (int cur = 0;; cur ^= 1) {
     const int t = s_tk[cur];
     if (t >= fp.total) break;
@@ -513,6 +535,8 @@ __global__ void __launch_bounds__(kSplitThreads, FHE_FUSE_CTAS)
           CT c = ct;
           c.smap_p = &cs_map;
           c.dmap_p = &cd_map;
+          c.ld_pol = first ? pol_ld : pol_ld2;
+          c.st_pol = first ? pol_mid : 0;
           c.setup(row * CT::TILES + jb);
           if (threadIdx.x == 0) {
             const unsigned twb = c.tw_pairs() * sizeof(double2);
@@ -533,6 +557,8 @@ __global__ void __launch_bounds__(kSplitThreads, FHE_FUSE_CTAS)
         KT k = kt;
         k.smap_p = &ks_map;
         k.dmap_p = &kd_map;
+        k.ld_pol = first ? pol_ld : pol_ld2;
+        k.st_pol = first ? pol_mid : 0;
         k.setup(g * fp.k_per_g + idx);
         if (k.valid) {
           if (threadIdx.x == 0) {
