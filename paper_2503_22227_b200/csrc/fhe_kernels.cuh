@@ -49,8 +49,6 @@ int launch_ewise(const DevChain& ch, int op, u64* out, const u64* a, const u64* 
 int launch_tensor(const DevChain& ch, u64* out, const u64* x, const u64* y, int limbs, long batch,
                   long x_stride, long y_stride, long out_stride, int square, cudaStream_t st);
 int launch_automorph(u64* out, const u64* in, long rows, int log_n, u64 elt, cudaStream_t st);
-int launch_gather_last(u64* dst, const u64* src, int polys, int level, int log_n,
-                       cudaStream_t st);
 int launch_modswitch_expand(const DevChain& ch, u64* corr, const u64* last, int polys,
                             int new_level, int last_prime, u64 t_plain, WPair tinv_last,
                             const u64* t_mod, const u64* qlast_mod, cudaStream_t st);

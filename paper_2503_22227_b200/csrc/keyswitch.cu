@@ -990,9 +990,10 @@ int run_rescale(FheContext& ctx, u64* out, const u64* in, int polys, int level, 
     tinv = pp->tinv_last[level];
     t_mod = pp->t_mod[level];
   }
-  int rc = launch_gather_last(last, in, polys, level, ch.log_n, st);
-  if (rc) return rc;
-  rc = launch_ntt(ch, last, last, polys, RowMap{nullptr, 1, level - 1}, true, st);
+  // inverse NTT of each poly's last limb, read in place (row stride level*n)
+  int rc = launch_ntt(ch, NttArgs{last, in + (long)(level - 1) * n, polys,
+                                  RowMap{nullptr, 1, level - 1}, (long)level * n, 0},
+                      true, st);
   if (rc) return rc;
   rc = launch_modswitch_expand(ch, corr, last, polys, level - 1, level - 1, t_plain, tinv, t_mod,
                                lp.rs_qlast, st);

@@ -193,18 +193,6 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
-// gather the last limb of every poly: dst[p] = src[p][level-1]
-__global__ void gather_last_kernel(u64* __restrict__ dst, const u64* __restrict__ src, int polys,
-                                   int level, int log_n) {
-  const long n = 1L << log_n;
-  const long total = (long)polys * n;
-  for (long t = blockIdx.x * (long)blockDim.x + threadIdx.x; t < total;
-       t += (long)gridDim.x * blockDim.x) {
-    const long p = t >> log_n, i = t & (n - 1);
-    dst[t] = src[(p * level + level - 1) * n + i];
-  }
-}
-
 }  // namespace
 
 int grid_for(long work) {
@@ -238,14 +226,6 @@ int launch_automorph(u64* out, const u64* in, long rows, int log_n, u64 elt, cud
   const long work = rows << log_n;
   if (work <= 0) return 0;
   automorph_kernel<<<grid_for(work), kThreads, 0, st>>>(out, in, rows, log_n, elt);
-  FHE_LAUNCH_CHECK();
-  return 0;
-}
-
-int launch_gather_last(u64* dst, const u64* src, int polys, int level, int log_n,
-                       cudaStream_t st) {
-  gather_last_kernel<<<grid_for((long)polys << log_n), kThreads, 0, st>>>(dst, src, polys, level,
-                                                                          log_n);
   FHE_LAUNCH_CHECK();
   return 0;
 }
