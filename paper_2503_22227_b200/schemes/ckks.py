@@ -225,8 +225,8 @@ def ckks_add(ctx: Context, a: CkksCiphertext, b: CkksCiphertext) -> CkksCipherte
     lv = a.level
     out = _new_ct(ctx, p, lv)
     common = min(pa, pb)
-    _ew(ctx, _native.EW_ADD, out.view()[:common], a.data.view()[:common],
-        b.data.view()[:common], rows=common * lv, limbs=lv)
+    # the first `common` polys start at each buffer's base: rows bound the op
+    _ew(ctx, _native.EW_ADD, out._buf, a.data._buf, b.data._buf, rows=common * lv, limbs=lv)
     if p > common:
         src = a if pa > pb else b
         out.view()[common:].copy_(src.data.view()[common:])
