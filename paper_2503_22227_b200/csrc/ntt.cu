@@ -353,6 +353,9 @@ constexpr int kFuseLag = FHE_FUSE_LAG;
 #ifndef FHE_FUSE_L2HINT
 #define FHE_FUSE_L2HINT 0
 #endif
+#ifndef FHE_FUSE_LAG_ROWS
+#define FHE_FUSE_LAG_ROWS 0
+#endif
 #ifndef FHE_FUSE_CTAS
 #define FHE_FUSE_CTAS 5
 #endif
@@ -365,6 +368,7 @@ struct FusePlan {
   int c_per_g;    // column tiles per group = R * C::TILES
   int k_per_g;    // chunk tiles per group = cblocks
   int total;      // tickets
+  int lag;        // second phase trails the first by this many groups
   FastDiv blk_div;    // ticket -> block (block = c_per_g + k_per_g tickets)
   FastDiv rb_div;     // group -> (class, row block)
 };
@@ -425,7 +429,7 @@ __global__ void __launch_bounds__(kSplitThreads, kSplitMinB)
     const int blk = fp.blk_div.div(t);
     const int r = t - blk * per_block;
     const bool first = r < first_n;
-    const int g = first ? blk : blk - kFuseLag;
+    const int g = first ? blk : blk - fp.lag;
     if (g >= 0 && g < fp.groups) {
       const int cls = fp.rb_div.div(g);
       const int rb = g - cls * fp.rblocks;
@@ -516,7 +520,7 @@ __global__ void __launch_bounds__(kSplitThreads, FHE_FUSE_CTAS)
     const int blk = fp.blk_div.div(t);
     const int r = t - blk * per_block;
     const bool first = r < first_n;
-    const int g = first ? blk : blk - kFuseLag;
+    const int g = first ? blk : blk - fp.lag;
     bool work = false;
     if (g >= 0 && g < fp.groups) {
       const int cls = fp.rb_div.div(g);
@@ -678,7 +682,10 @@ FusePlan make_fuse_plan(const K& kt, int cols_tiles_per_row, int rows, int limbs
   fp.groups = std::min(limbs, rows) * kt.rblocks;
   fp.c_per_g = (1 << kt.log_r) * cols_tiles_per_row;
   fp.k_per_g = kt.cblocks;
-  fp.total = (fp.groups + kFuseLag) * (fp.c_per_g + fp.k_per_g);
+  // FHE_FUSE_LAG_ROWS > 0: the lag is a fixed number of rows (a fixed
+  // intermediate window) instead of a fixed number of groups
+  fp.lag = FHE_FUSE_LAG_ROWS > 0 ? std::max(2, FHE_FUSE_LAG_ROWS >> kt.log_r) : kFuseLag;
+  fp.total = (fp.groups + fp.lag) * (fp.c_per_g + fp.k_per_g);
   fp.blk_div.init(fp.c_per_g + fp.k_per_g);
   fp.rb_div.init(kt.rblocks);
   return fp;
