@@ -48,7 +48,11 @@ def _peaks():
 
 
 class ClockSampler:
-    """nvidia-smi SM clocks and throttle reasons sampled during the timed region."""
+    """SM clocks and throttle reasons sampled during the timed region.
+
+    In-process NVML (nvidia-ml-py) every 10 ms: no nvidia-smi child process
+    (whose NVML start-up can stall the GPU for a millisecond or more inside a
+    ~60 ms timed region).  Falls back to nvidia-smi when NVML is missing."""
 
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
@@ -58,20 +62,49 @@ class ClockSampler:
         self.index = index
         self.rows = []
         self._stop = threading.Event()
+        self.period = float(os.environ.get("BENCH_CLOCK_PERIOD", "0.02"))
+        self._nvml = None
+        try:
+            import pynvml
+            import torch
+
+            pynvml.nvmlInit()
+            props = torch.cuda.get_device_properties(index)
+            bus = f"{props.pci_domain_id:08x}:{props.pci_bus_id:02x}:{props.pci_device_id:02x}.0"
+            try:
+                h = pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+            except Exception:
+                h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self._nvml = (pynvml, h)
+        except Exception:
+            self._nvml = None
         self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _sample_nvml(self):
+        nv, h = self._nvml
+        sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+        bits = (nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
+                nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap)
+        return [str(sm), str(mx)] + ["Active" if r & b else "Not Active" for b in bits]
 
     def _run(self):
         while not self._stop.is_set():
             try:
-                out = subprocess.run(
-                    ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
-                     "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
-                vals = [v.strip() for v in out.stdout.strip().split(",")]
-                if len(vals) == 6:
-                    self.rows.append(vals)
+                if self._nvml is not None:
+                    self.rows.append(self._sample_nvml())
+                else:
+                    out = subprocess.run(
+                        ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                         "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                        timeout=5)
+                    vals = [v.strip() for v in out.stdout.strip().split(",")]
+                    if len(vals) == 6:
+                        self.rows.append(vals)
             except Exception:
                 pass
-            self._stop.wait(0.2)
+            self._stop.wait(self.period if self._nvml is not None else 0.2)
 
     def __enter__(self):
         self._t.start()
@@ -90,7 +123,8 @@ class ClockSampler:
         reasons = sorted({names[k] for r in self.rows for k in range(4) if r[2 + k] == "Active"})
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.rows)}
+                "samples": len(self.rows),
+                "source": "nvml" if self._nvml is not None else "nvidia-smi"}
 
 
 def dist_init():
@@ -498,9 +532,12 @@ def main():
     try:
         with open(os.path.join(ROOT, "profiles", "r1_ntt_traffic.json")) as f:
             tr = json.load(f)
-        per = tr.get("fused_kernel_dram_bytes") or (tr["cols_kernel_dram_bytes"]
-                                                    + tr["chunks_kernel_dram_bytes"])
-        traffic = per * rows / tr["rows"]
+        if tr.get("fused_kernel_dram_bytes"):
+            per, per_rows = tr["fused_kernel_dram_bytes"], tr.get("fused_rows", tr["rows"])
+        else:
+            per = tr["cols_kernel_dram_bytes"] + tr["chunks_kernel_dram_bytes"]
+            per_rows = tr["rows"]
+        traffic = per * rows / per_rows
     except Exception:
         pass
     inv_gbs = algo / (ntt_ms["inverse"] / 1000.0) / 1e9
@@ -522,8 +559,8 @@ def main():
         "roofline": {"bound": "hbm", "kernel": "batched NTT forward (fused four-step TMA kernel), "
                      f"N=2^16, {rows} rows", "achieved": fwd_gbs, "peak": peak,
                      "peak_kind": peak_kind, "unit": "GB/s", "frac": fwd_gbs / peak,
-                     "traffic": traffic, "traffic_source": "profiles/r1_ntt_traffic.json (ncu, "
-                     "scaled per row)", "inverse_achieved": inv_gbs,
+                     "traffic": traffic, "traffic_source": "profiles/r1_ntt_traffic.json (ncu --set full of "
+                     "the same 5120-row launch; scaled per row for other sizes)", "inverse_achieved": inv_gbs,
                      "algorithmic_bytes_per_launch": algo},
         "ntt": {"forward_ms": ntt_ms["forward"], "inverse_ms": ntt_ms["inverse"],
                 "forward_gbs": fwd_gbs, "inverse_gbs": inv_gbs, "rows": rows, "N": n},
