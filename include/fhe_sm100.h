@@ -132,8 +132,9 @@ int fhe_keyswitch(const FheContext* ctx, int level, const uint64_t* d, int64_t d
  *      (y may equal x: squaring).  out0 = d0 + b, out1 = d1 + a with
  *      (d0, d1, d2) the tensor product and (b, a) the key switch of d2;
  *      out0/out1 may alias x's polys.  The words equal those of fhe_tensor
- *      followed by fhe_keyswitch (with FHE_HMULT_TENS=1, d0/d1 are formed
- *      in the key switch's finishing kernel and never written to HBM). */
+ *      followed by fhe_keyswitch; d0/d1 are formed in the key switch's
+ *      finishing kernel and never written to HBM (FHE_HMULT_TENS=0: the
+ *      tensor is materialised instead). */
 size_t fhe_hmult_relin_workspace(const FheContext* ctx, int level, int batch);
 int fhe_hmult_relin(const FheContext* ctx, int level, const uint64_t* x, const uint64_t* y,
                     int64_t in_stride, const uint64_t* key, uint64_t* out0, uint64_t* out1,

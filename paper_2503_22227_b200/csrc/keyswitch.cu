@@ -905,16 +905,17 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
-// Opt-in (FHE_HMULT_TENS=1): form d0/d1/d2 inside the fused finish kernel.
-// It saves three polynomials of HBM traffic per op, but the extra operands
-// cost the HBM-bound finishing kernel a CTA per SM: measured -0.4% at batch 8
-// and +0.5% at batch 16 (profiles/r1_ntt_notes.md), so the default keeps the
-// materialised tensor.
+// Default (FHE_HMULT_TENS=0 turns it off): form d0/d1/d2 inside the fused
+// finish kernel.  It saves three polynomials of HBM traffic per op; the extra
+// operands cost the HBM-bound finishing kernel a CTA per SM, so in a short
+// burst it is within 0.5% (-0.4% at batch 8, +0.5% at batch 16), but under
+// sustained load the board is power-capped and the lower DRAM traffic keeps
+// the clocks higher: +2% at batch 16 (profiles/r1_ntt_notes.md).
 static bool hmult_tens_enabled() {
   static int on = -1;
   if (on < 0) {
     const char* e = getenv("FHE_HMULT_TENS");
-    on = (e && e[0] == '1') ? 1 : 0;
+    on = (e && e[0] == '0') ? 0 : 1;
   }
   return on == 1;
 }
@@ -926,9 +927,10 @@ size_t hmult_relin_workspace(const FheContext& ctx, int level, int batch) {
 
 // HMult+Relin in one call (ckks_multiply then ckks_relinearize, ckks.py):
 // x, y are batch x (2, level, n) evaluation-domain ciphertexts in_stride words
-// apart; out0/out1 receive the relinearized (c0, c1).  Default: the tensor
-// goes to the workspace and the key switch runs on it; FHE_HMULT_TENS=1 only
-// materialises d2 and forms d0/d1 in the finishing kernel.  Same words.
+// apart; out0/out1 receive the relinearized (c0, c1).  Default: only d2 is
+// materialised and d0/d1 are formed in the finishing kernel; with
+// FHE_HMULT_TENS=0 (or without the fused finish path) the full tensor goes
+// to the workspace and the plain key switch runs on it.  Same words.
 int run_hmult_relin(const FheContext& ctx, int level, const u64* x, const u64* y, long in_stride,
                     const u64* key, u64* out0, u64* out1, long out_stride, int batch, void* ws,
                     size_t ws_bytes, cudaStream_t st) {
