@@ -166,7 +166,7 @@ def max_over_ranks(x: float, world: int) -> float:
 # ---------------------------------------------------------------------------
 
 def build_workload(batch: int):
-    """Config 4: Q = 30 x 50-bit, P = 10 x 60-bit, dnum = 3, Delta = 2^49;
+    """Config 4: Q = 30 x 50-bit, P = 10 x SPECIAL_BITS (50) bit, dnum = 3, Delta = 2^49;
     keys from Rng((4).to_bytes(32)), slots ~ U(-1,1) from default_rng(9)."""
     import torch
 
@@ -193,14 +193,44 @@ def build_workload(batch: int):
     if not err < 1e-4:
         raise AssertionError(f"HMult+Relin+Rescale error {err} too large")
     L, n = LEVELS, ctx.n
+    # distinct batch items: X[b] encrypts x + b*y and Y[b] encrypts y + b*x
+    # (ckks_add chains of the two fresh ciphertexts), so a row mix-up between
+    # batch items inside the fused transforms shows in the per-item check
     X = torch.empty((batch, 2, L, n), dtype=torch.int64, device="cuda")
     Y = torch.empty_like(X)
-    X[:] = cx.data.view()
-    Y[:] = cy.data.view()
+    ax, ay = cx, cy
+    for b in range(batch):
+        X[b] = ax.data.view()
+        Y[b] = ay.data.view()
+        ax, ay = ckks.ckks_add(ctx, ax, cy), ckks.ckks_add(ctx, ay, cx)
     T3 = torch.empty((batch, 3, L, n), dtype=torch.int64, device="cuda")
     OUT = torch.empty((batch, 2, L, n), dtype=torch.int64, device="cuda")
     return {"ctx": ctx, "rlk": rlk, "X": X, "Y": Y, "T3": T3, "OUT": OUT, "err": err,
             "cx": cx, "cy": cy, "sk": sk, "x": x, "y": y}
+
+
+def item_ct(w, T, b: int):
+    """Batch item b of a resident (B, 2, L, n) block as a CkksCiphertext."""
+    from paper_2503_22227_b200.schemes import ckks
+
+    ctx = w["ctx"]
+    return ckks.CkksCiphertext(ckks.CData.wrap(T[b].reshape(-1), 2, LEVELS, ctx.n,
+                                               ckks.Domain.EVALUATION), w["cx"].scale, LEVELS)
+
+
+def check_batch_items(w, batch: int) -> list:
+    """Items of the batched step that differ from the public API's result."""
+    import torch
+
+    from paper_2503_22227_b200.schemes import ckks
+
+    ctx, bad = w["ctx"], []
+    for b in range(batch):
+        ref = ckks.ckks_relinearize(ctx, ckks.ckks_multiply(ctx, item_ct(w, w["X"], b),
+                                                            item_ct(w, w["Y"], b)), w["rlk"])
+        if not torch.equal(w["OUT"][b], ref.data.view()):
+            bad.append(b)
+    return bad
 
 
 def hmult_relin_step(w, batch: int):
@@ -279,12 +309,12 @@ def rotate_rescale_legs(w, batch: int, steps: int, warmup: int, world: int):
 
     rot_ms = max_over_ranks(time_steps(rot, steps, warmup, world), world)
     resc_ms = max_over_ranks(time_steps(resc, steps, warmup, world), world)
-    want = ckks.ckks_rotate(ctx, w["cx"], 1, gks)
-    if not torch.equal(R[0], want.data.view()):
-        raise AssertionError("batched rotate differs from ckks_rotate")
-    want = ckks.ckks_rescale(ctx, w["cx"])
-    if not torch.equal(S[0], want.data.view()):
-        raise AssertionError("batched rescale differs from ckks_rescale")
+    for b in range(batch):
+        ct = item_ct(w, X, b)
+        if not torch.equal(R[b], ckks.ckks_rotate(ctx, ct, 1, gks).data.view()):
+            raise AssertionError(f"batched rotate item {b} differs from ckks_rotate")
+        if not torch.equal(S[b], ckks.ckks_rescale(ctx, ct).data.view()):
+            raise AssertionError(f"batched rescale item {b} differs from ckks_rescale")
     peak, _ = _peaks()
     B = n * 8
     out = {}
@@ -497,12 +527,11 @@ def main():
     gpu_launches = counted["n1"] - counted["n0"]
     ms = max_over_ranks(ms, world)
     ops = B * world / (ms / 1000.0)
-    # parity of the timed path itself: batch item 0 equals the public-API result
-    from paper_2503_22227_b200.schemes import ckks
-
-    ref = ckks.ckks_relinearize(w["ctx"], ckks.ckks_multiply(w["ctx"], w["cx"], w["cy"]), w["rlk"])
-    if not torch.equal(w["OUT"][0], ref.data.view()):
-        raise AssertionError("batched step differs from the public API result")
+    # parity of the timed path itself: every batch item equals the public-API
+    # result (ckks_multiply -> ckks_relinearize) of its own distinct pair
+    bad = check_batch_items(w, B)
+    if bad:
+        raise AssertionError(f"batched step differs from the public API for items {bad}")
 
     # config-4 Rotate and Rescale throughput (same resident batch)
     legs = rotate_rescale_legs(w, B, max(4, args.steps // 2), 3, world)
@@ -510,8 +539,8 @@ def main():
     # end to end through the public API with host buffers
     L, n = LEVELS, 1 << N_LOG
     host_in = torch.empty((B, 2, 2, L, n), dtype=torch.int64).pin_memory()
-    host_in[:, 0] = w["X"][0].cpu()
-    host_in[:, 1] = w["Y"][0].cpu()
+    host_in[:, 0] = w["X"].cpu()
+    host_in[:, 1] = w["Y"].cpu()
     host_out = torch.empty((B, 2, L, n), dtype=torch.int64).pin_memory()
     from paper_2503_22227_b200.host_io import CopyStreams
 
@@ -519,7 +548,7 @@ def main():
     e2e_ms = time_steps(lambda: e2e_step(w, B, host_in, host_out, streams),
                         max(3, args.steps // 4), 3, world)
     # the pipelined public-API path returns the same bits as the resident step
-    if not torch.equal(host_out[0], w["OUT"][0].cpu()):
+    if not torch.equal(host_out, w["OUT"].cpu()):
         raise AssertionError("host pipeline result differs from the resident batched step")
     e2e_ms = max_over_ranks(e2e_ms, world)
     h2d = B * 2 * 2 * L * n * 8

@@ -59,6 +59,20 @@ const char* fhe_last_error(void);
 uint64_t fhe_launch_count(void);
 int fhe_device_sm_count(void);
 
+/* Transform launches per NTT kernel path since load (no reference
+ * counterpart: evidence for the parity tests and the bench of WHICH kernel
+ * ran a transform).  Unknown path: 0. */
+enum {
+  FHE_NTT_PATH_ROWS = 0,      /* whole-row tiles, N <= 2^12 (FP64 pipe)          */
+  FHE_NTT_PATH_SPLIT = 1,     /* four-step, two kernels (column + chunk tiles)   */
+  FHE_NTT_PATH_FUSED_TMA = 2, /* four-step, one ticketed kernel on TMA tiles      */
+  FHE_NTT_PATH_FUSED_CP = 3,  /* four-step, one ticketed kernel on cp.async tiles */
+  FHE_NTT_PATH_INT = 4,       /* 64-bit integer pipe (a prime >= 2^50)            */
+  FHE_NTT_PATH_CLUSTER = 5,   /* one pass, row held by a CTA cluster (DSMEM)      */
+  FHE_NTT_PATHS = 8
+};
+uint64_t fhe_ntt_path_count(int path);
+
 /* ---- chains: NttTables / NttChain precompute (coremath/ntt.py:52-137,
  *      240-275; primes.py:60-71 for psi; rnspoly.py:47-67) ---------------- */
 int fhe_chain_create(const uint64_t* primes, int count, int log_n, FheChain** out);

@@ -17,6 +17,8 @@ HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "fhe_sm100.h")
 # op codes / operand modes (mirror include/fhe_sm100.h)
 EW_ADD, EW_SUB, EW_NEG, EW_MUL, EW_NEG_MUL, EW_MUL_ADD, EW_MUL_SUB, EW_REDUCE = range(8)
 B_FULL, B_BCAST, B_CONST = range(3)
+# NTT kernel paths (fhe_ntt_path_count)
+NTT_PATHS = {"rows": 0, "split": 1, "fused_tma": 2, "fused_cp": 3, "int": 4, "cluster": 5}
 
 _u64p = ctypes.c_void_p
 _vp = ctypes.c_void_p
@@ -29,6 +31,7 @@ SIGNATURES = {
     "fhe_last_error": (ctypes.c_char_p, []),
     "fhe_launch_count": (ctypes.c_uint64, []),
     "fhe_device_sm_count": (_int, []),
+    "fhe_ntt_path_count": (ctypes.c_uint64, [_int]),
     "fhe_chain_create": (_int, [_vp, _int, _int, ctypes.POINTER(_vp)]),
     "fhe_chain_destroy": (_int, [_vp]),
     "fhe_chain_tables": (_int, [_vp, _int, _vp, _vp, _vp, _vp]),
@@ -96,6 +99,12 @@ def lib() -> ctypes.CDLL:
             raise NativeUnavailable("no CUDA device: the B200 path has no CPU fallback")
         _device_ok = True
     return _lib if _lib is not None else load_library()
+
+
+def ntt_path_counts() -> dict:
+    """Transform launches per NTT kernel path so far (fhe_ntt_path_count)."""
+    lb = load_library()
+    return {k: int(lb.fhe_ntt_path_count(v)) for k, v in NTT_PATHS.items()}
 
 
 def check(rc: int, what: str):

@@ -26,6 +26,8 @@ const char* fhe_last_error(void) { return g_err.c_str(); }
 
 uint64_t fhe_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 
+uint64_t fhe_ntt_path_count(int path) { return ntt_path_count(path); }
+
 int fhe_device_sm_count(void) {
   int dev = 0, n = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return -1;

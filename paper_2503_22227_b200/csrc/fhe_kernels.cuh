@@ -35,6 +35,7 @@ struct NttArgs {
   bool* fin_done = nullptr;
 };
 int launch_ntt(const DevChain& ch, const NttArgs& a, bool inverse, cudaStream_t st);
+unsigned long long ntt_path_count(int path);
 // per-chain scratch of the fused four-step NTT (tile tickets, group counters)
 void* fuse_scratch_new();
 void fuse_scratch_free(void* p);

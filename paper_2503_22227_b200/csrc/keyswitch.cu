@@ -553,10 +553,12 @@ __global__ void __launch_bounds__(kThreads, TENS  ? FHE_TENS_MINB
             if constexpr (TENS) {
               const u64* xb = add0 + bb * add_stride + w;
               const u64* yb = add1 + bb * add_stride + w;
-              tx[u][0] = __ldg(xb);
-              tx[u][1] = __ldg(xb + (long)level * n);
-              ty[u][0] = __ldg(yb);
-              ty[u][1] = __ldg(yb + (long)level * n);
+              // plain (coherent) loads: out0/out1 may alias x (fhe_sm100.h),
+              // so x is not read-only for the duration of the kernel
+              tx[u][0] = xb[0];
+              tx[u][1] = xb[(long)level * n];
+              ty[u][0] = yb[0];
+              ty[u][1] = yb[(long)level * n];
             } else {
               av[u][0] = add0 ? add0[bb * add_stride + w] : 0;
               av[u][1] = add1 ? add1[bb * add_stride + w] : 0;

@@ -35,8 +35,17 @@
 
 #include <cuda.h>
 
+#include <atomic>
 #include <cstdlib>
 #include <mutex>
+
+// Launches per transform path (fhe_ntt_path_count): evidence for the tests
+// and the bench of WHICH kernel ran (FHE_NTT_PATH_* in fhe_sm100.h).
+static std::atomic<unsigned long long> g_ntt_path[FHE_NTT_PATHS];
+static void path_hit(int p) { g_ntt_path[p].fetch_add(1, std::memory_order_relaxed); }
+unsigned long long ntt_path_count(int p) {
+  return (p >= 0 && p < FHE_NTT_PATHS) ? g_ntt_path[p].load(std::memory_order_relaxed) : 0;
+}
 
 namespace {
 #include "ntt_tiles.cuh"
@@ -937,6 +946,7 @@ int launch_rows(const DevChain& ch, const NttArgs& a, bool inverse, bool lazy, c
   tl.dst = RowAddr{a.dst_bstride, a.map.limbs, LOG_N};
   tl.fwd = !inverse;
   const int ntiles = (a.rows + T::NB - 1) / T::NB;
+  path_hit(ch.fp64_ok ? FHE_NTT_PATH_ROWS : FHE_NTT_PATH_INT);
   if (ch.fp64_ok)
     return inverse ? launch_tiles_fp<T, false, FPIN_U64, FPOUT_U64>(ch, a.dst, a.src, tl, ntiles, st)
                    : launch_tiles_fp<T, true, FPIN_U64, FPOUT_U64>(ch, a.dst, a.src, tl, ntiles, st);
@@ -991,6 +1001,7 @@ int launch_split(const DevChain& ch, const NttArgs& a, bool inverse, bool lazy,
       bool done = false;
       rc = launch_fused_tma(ch, a.dst, a.src, tc, tk, !inverse, a.src_bstride, a.dst_bstride,
                             a.rows, a.map.limbs, st, done);
+      if (done) path_hit(FHE_NTT_PATH_FUSED_TMA);
       if (rc || done) return rc;
     }
   }
@@ -999,8 +1010,10 @@ int launch_split(const DevChain& ch, const NttArgs& a, bool inverse, bool lazy,
     ct.dst = d;
     kt.src = inverse ? s : d;
     kt.dst = d;
+    path_hit(FHE_NTT_PATH_FUSED_CP);
     return launch_fused(ch, a.dst, a.src, ct, kt, !inverse, a.rows, a.map.limbs, st);
   }
+  path_hit(ch.fp64_ok ? FHE_NTT_PATH_SPLIT : FHE_NTT_PATH_INT);
   if (ch.fp64_ok) {
     if (!inverse) {
       ct.src = s;
