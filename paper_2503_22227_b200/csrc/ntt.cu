@@ -36,6 +36,7 @@
 #include <cuda.h>
 
 #include <atomic>
+#include <cstdio>
 #include <cstdlib>
 #include <mutex>
 
@@ -821,6 +822,8 @@ bool chunks_tensor_map(CUtensorMap* m, const u64* base, int log_n, int log_s, in
                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+#include "ntt_cluster.cuh"
+
 template <class Tile, bool FWD, int IN, int OUT>
 int launch_chunks_tma(const DevChain& ch, u64* dst, const u64* src, const Tile& tl, int ntiles,
                       long src_bstride, long dst_bstride, cudaStream_t st, bool& done) {
@@ -983,6 +986,13 @@ int launch_split(const DevChain& ch, const NttArgs& a, bool inverse, bool lazy,
   const bool use_ktma = (LOG_N - LOG_N1 == 8) && ch.fp64_ok && kstage && tma_enabled() &&
                         a.rows % a.map.limbs == 0 && std::getenv("FHE_NTT_KTMA") == nullptr;
   if constexpr (LOG_N1 == 8 && LOG_N - LOG_N1 == 8) {
+    // one pass, the row held by a 16-CTA cluster (DSMEM transpose)
+    if (ch.fp64_ok && !a.fin && tma_enabled()) {
+      bool done = false;
+      rc = launch_cluster_ntt(ch, a, inverse, st, done);
+      if (done) path_hit(FHE_NTT_PATH_CLUSTER);
+      if (rc || done) return rc;
+    }
     // fused for groups of >= 8 rows of one residue class: with the second
     // phase 16 groups behind the first, the key switch's 8-row groups (input
     // INTT, ModUp NTT) gain too (HMult+Relin +2.5%); at lag 8 they lost 15%
