@@ -165,19 +165,37 @@ def max_over_ranks(x: float, world: int) -> float:
 
 # ---------------------------------------------------------------------------
 
-def build_workload(batch: int):
-    """Config 4: Q = 30 x 50-bit, P = 10 x SPECIAL_BITS (50) bit, dnum = 3, Delta = 2^49;
-    keys from Rng((4).to_bytes(32)), slots ~ U(-1,1) from default_rng(9)."""
+def build_workload(batch: int, special_bits: int = SPECIAL_BITS, gadget: bool = False):
+    """Config 4: Q = 30 x 50-bit, Delta = 2^49; hybrid: P = 10 x special_bits
+    (default 50: every prime < 2^50 keeps the FP64-pipe path; 60 runs the
+    64-bit integer path), dnum = 3.  gadget=True: the reference's per-prime
+    gadget (alpha = 1, K = 0, MAX_CHAIN_LEN patched to 30 as the reference
+    needs), the apples-to-apples mode of the CPU reference.  Keys from
+    Rng((4).to_bytes(32)), slots ~ U(-1,1) from default_rng(9)."""
     import torch
 
-    from paper_2503_22227_b200.context import Context, PoolConfig, hybrid_params
+    import paper_2503_22227_b200.context as pctx
+    from paper_2503_22227_b200.context import (Context, EncryptionParams, PoolConfig, Scheme,
+                                               hybrid_params)
+    from paper_2503_22227_b200.coremath.primes import gen_ntt_prime_chain
     from paper_2503_22227_b200.coremath.sampling import Rng
     from paper_2503_22227_b200.keys import keygen, pk_gen, relin_keygen
     from paper_2503_22227_b200.schemes import ckks
 
-    params = hybrid_params(1 << N_LOG, LEVELS, bits=50, special=SPECIAL, special_bits=SPECIAL_BITS,
-                           dnum=DNUM, scale=float(2 ** 49))
-    ctx = Context(params, PoolConfig(unit_mb=200, cap_mb=4096))
+    if gadget:
+        q = tuple(m.value for m in gen_ntt_prime_chain(50, 1 << N_LOG, LEVELS))
+        old = pctx.MAX_CHAIN_LEN
+        pctx.MAX_CHAIN_LEN = LEVELS
+        try:
+            ctx = Context(EncryptionParams(Scheme.CKKS, 1 << N_LOG, q,
+                                           default_scale=float(2 ** 49)),
+                          PoolConfig(unit_mb=200, cap_mb=6144))
+        finally:
+            pctx.MAX_CHAIN_LEN = old
+    else:
+        params = hybrid_params(1 << N_LOG, LEVELS, bits=50, special=SPECIAL,
+                               special_bits=special_bits, dnum=DNUM, scale=float(2 ** 49))
+        ctx = Context(params, PoolConfig(unit_mb=200, cap_mb=4096))
     seed = lambda s: Rng(int(s).to_bytes(32, "little"))  # noqa: E731
     sk = keygen(ctx, seed(4))
     pk = pk_gen(ctx, sk, seed(41))
@@ -218,14 +236,14 @@ def item_ct(w, T, b: int):
                                                ckks.Domain.EVALUATION), w["cx"].scale, LEVELS)
 
 
-def check_batch_items(w, batch: int) -> list:
+def check_batch_items(w, batch: int, items=None) -> list:
     """Items of the batched step that differ from the public API's result."""
     import torch
 
     from paper_2503_22227_b200.schemes import ckks
 
     ctx, bad = w["ctx"], []
-    for b in range(batch):
+    for b in (range(batch) if items is None else items):
         ref = ckks.ckks_relinearize(ctx, ckks.ckks_multiply(ctx, item_ct(w, w["X"], b),
                                                             item_ct(w, w["Y"], b)), w["rlk"])
         if not torch.equal(w["OUT"][b], ref.data.view()):
@@ -433,13 +451,226 @@ def pdq_latency(reps: int = 3, world: int = 1):
             raise AssertionError("PDQ-1 mask differs from the plaintext oracle")
         out[f"q{qid}_ms"] = statistics.median(times)
     out["ranks"] = world
-    out["sharding"] = "(atom, digit) units over ranks, one NCCL exchange" if world > 1 else "none"
+    out["sharding"] = ("(atom, digit) units over ranks, one all-gather of the stacked unit results" if world > 1 else "none")
     return out
 
 
-def cpu_baseline_hmult(seconds_budget: float = 20.0):
+def host_info() -> dict:
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"cpu_model": model, "cpu_cores": os.cpu_count()}
+
+
+def config4_variant(batch: int, steps: int, warmup: int, world: int, special_bits: int = 50,
+                    gadget: bool = False) -> dict:
+    """HMult+Relin throughput of a config-4 variant over `batch` resident
+    distinct pairs: the per-prime gadget (alpha=1, K=0; the CPU reference's
+    own algorithm) or hybrid dnum=3 with 60-bit special primes (integer
+    path).  Every batch item is checked against the public API."""
+    w = build_workload(batch, special_bits=special_bits, gadget=gadget)
+    ms = max_over_ranks(time_steps(lambda: hmult_relin_step(w, batch), steps, warmup, world),
+                        world)
+    bad = check_batch_items(w, batch)
+    if bad:
+        raise AssertionError(f"config-4 variant items {bad} differ from the public API")
+    peak, _ = _peaks()
+    B = (1 << N_LOG) * 8
+    # algorithmic bytes per op (SURVEY 8(d)): 2 ct in (120 B) + key / batch + out (60 B)
+    key = (LEVELS * 2 * LEVELS if gadget else DNUM * 2 * (LEVELS + SPECIAL)) * B
+    per_op = 180 * B + key / batch
+    ops = batch * world / (ms / 1000.0)
+    del w
+    import torch
+
+    torch.cuda.empty_cache()
+    return {"ops_s": ops, "ms_per_step": ms, "batch": batch,
+            "mode": "per-prime gadget (alpha=1, K=0)" if gadget else
+                    f"hybrid dnum=3, P=10 x {special_bits}-bit",
+            "path": "FP64-pipe NTT" if (gadget or special_bits <= 50) else "64-bit integer NTT",
+            "algorithmic_bytes_per_op": per_op, "hbm_frac": ops * per_op / 1e9 / peak}
+
+
+def config2_sweep(steps: int = 5, warmup: int = 3) -> list:
+    """Config 2: batched NTT / INTT over 64 ciphertexts x 2 polys x L limbs,
+    N = 2^12 .. 2^16, 50-bit primes; GB/s against 2 * rows * N * 8 bytes."""
+    import torch
+
+    from paper_2503_22227_b200.coremath.ntt import DeviceChain
+    from paper_2503_22227_b200.coremath.primes import gen_ntt_prime_chain
+
+    peak, _ = _peaks()
+    out = []
+    for log_n in (12, 13, 14, 15, 16):
+        n = 1 << log_n
+        for L in (1, 8, 40):
+            rows = 64 * 2 * L
+            primes = [m.value for m in gen_ntt_prime_chain(50, n, L)]
+            ch = DeviceChain(primes, log_n)
+            qv = torch.tensor(primes, dtype=torch.float64, device="cuda")
+            buf = (torch.rand((rows, n), dtype=torch.float64, device="cuda")
+                   * qv.repeat(rows // L).unsqueeze(1)).to(torch.int64)
+            algo = 2.0 * rows * n * 8
+            row = {"log_n": log_n, "L": L, "rows": rows}
+            for name, inv in (("fwd", False), ("inv", True)):
+                t = time_steps(lambda: ch.transform(buf, rows, inv, limbs=L, offset=0), steps,
+                               warmup, 1)
+                row[f"{name}_ms"] = t
+                row[f"{name}_gbs"] = algo / (t / 1000.0) / 1e9
+                row[f"{name}_frac"] = row[f"{name}_gbs"] / peak
+            out.append(row)
+            del buf
+    torch.cuda.empty_cache()
+    return out
+
+
+def config3_legs(steps: int = 20, warmup: int = 3) -> dict:
+    """Config 3: BGV and BFV multiply + relinearize at N=2^14, Q = 8 x 50-bit,
+    t = 65537 through the public API (bgv_/bfv_multiply -> _relinearize; BFV
+    runs the BEHZ tensor), ops/s on the device; one decrypt checked exact."""
+    import torch
+
+    from paper_2503_22227_b200.context import Context, EncryptionParams, PoolConfig, Scheme
+    from paper_2503_22227_b200.coremath.primes import gen_ntt_prime_chain
+    from paper_2503_22227_b200.coremath.sampling import Rng
+    from paper_2503_22227_b200.keys import keygen, pk_gen, relin_keygen
+    from paper_2503_22227_b200.schemes import bfv, bgv
+    from paper_2503_22227_b200.schemes.batching import batch_decode
+
+    n, t = 1 << 14, 65537
+    primes = tuple(m.value for m in gen_ntt_prime_chain(50, n, 8))
+    out = {}
+    for name, scheme, mod in (("bgv", Scheme.BGV, bgv), ("bfv", Scheme.BFV, bfv)):
+        ctx = Context(EncryptionParams(scheme, n, primes, plain_modulus=t),
+                      PoolConfig(unit_mb=64, cap_mb=1024))
+        rng = Rng((3).to_bytes(32, "little"))
+        sk = keygen(ctx, rng)
+        pk = pk_gen(ctx, sk, rng)
+        rlk = relin_keygen(ctx, sk, rng)
+        vr = np.random.default_rng(5)
+        va, vb = vr.integers(0, t, n), vr.integers(0, t, n)
+        a = getattr(mod, f"{name}_encrypt_ints")(ctx, va, pk, rng)
+        b = getattr(mod, f"{name}_encrypt_ints")(ctx, vb, pk, rng)
+        mul, rel = getattr(mod, f"{name}_multiply"), getattr(mod, f"{name}_relinearize")
+        res = {}
+
+        def step():
+            res["ct"] = rel(ctx, mul(ctx, a, b), rlk)
+
+        ms = time_steps(step, steps, warmup, 1)
+        dec = batch_decode(ctx, getattr(mod, f"{name}_decrypt")(ctx, res["ct"], sk))
+        exact = bool(np.array_equal(np.asarray(dec) % t, (va * vb) % t))
+        out[name] = {"ops_s": 1000.0 / ms, "ms_per_op": ms, "decrypt_exact": exact}
+        del ctx
+    torch.cuda.empty_cache()
+    return out
+
+
+def reference_cpu_file() -> dict | None:
+    """The reference package itself timed in the build container
+    (tools/reference_cpu_baselines.py); the reference does not travel to
+    the GPU box, so these are reported with where they ran."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r2_reference_cpu_baselines.json")) as f:
+            return json.load(f)
+    except (OSError, ValueError):
+        return None
+
+
+def pdq_session(rows: int):
+    from paper_2503_22227_b200.context import Context, PoolConfig, Scheme, params_for_profile
+    from paper_2503_22227_b200.coremath.sampling import Rng
+    from paper_2503_22227_b200.keys import galois_keygen, keygen, pk_gen, relin_keygen
+    from paper_2503_22227_b200.pdq.config import PdqConfig
+    from paper_2503_22227_b200.pdq.evaluator import CkksEval, rotation_steps
+
+    cfg = PdqConfig(rows=rows)
+    ctx = Context(params_for_profile("pdq", Scheme.CKKS), PoolConfig(unit_mb=64, cap_mb=2048))
+    rng = Rng((1).to_bytes(32, "little"))
+    sk = keygen(ctx, rng)
+    pk = pk_gen(ctx, sk, rng)
+    ev = CkksEval(ctx, relin_keygen(ctx, sk, rng),
+                  galois_keygen(ctx, sk, rotation_steps(ctx.n), rng))
+    return cfg, ctx, sk, pk, ev, rng
+
+
+def pdq_rowblocks(world: int, rows: int = 16384, reps: int = 3) -> dict:
+    """Row-batch layout (pdq/rowblocks.py): rows / 2048 blocks, block b on
+    rank b % world, one all-reduce + mod-q fix-up of the aggregates.  Query 2
+    (sum) and query 4 (avg) latency, max over ranks."""
+    import torch
+
+    from paper_2503_22227_b200.pdq.dataset import make_dataset, oracle_result
+    from paper_2503_22227_b200.pdq.engine import LocalInverseClient, standard_query
+    from paper_2503_22227_b200.pdq.rowblocks import RowBlockEngine
+    from paper_2503_22227_b200.pdq.shard import ShardGroup
+
+    cfg, ctx, sk, pk, ev, rng = pdq_session(rows)
+    data = make_dataset(cfg)
+    group = ShardGroup.from_env() if world > 1 else ShardGroup(0, 1)
+    eng = RowBlockEngine(ev, cfg, group)
+    eng.load(data, pk, seed=100)
+    inv = LocalInverseClient(ev, cfg, sk, pk, rng=rng)
+    out = {"rows": rows, "blocks": eng.nblocks, "blocks_per_rank": len(eng.blocks_of_rank()),
+           "ranks": world}
+    for qid in (2, 4):
+        spec = standard_query(qid)
+        times = []
+        for _ in range(reps):
+            barrier(world)
+            t0 = time.perf_counter()
+            res = eng.run(spec, pk, channel=inv, rng=np.random.default_rng(5))
+            torch.cuda.synchronize()
+            times.append(max_over_ranks((time.perf_counter() - t0) * 1e3, world))
+        ms = statistics.median(times)
+        out[f"q{qid}_ms"] = ms
+        out[f"q{qid}_rows_s"] = rows / (ms / 1000.0)
+        if qid == 2:
+            got = float(ev.decrypt(res.cts["sum"], sk).real[0])
+            want = oracle_result(spec, data)
+            if abs(got - want) > 1e-3 * max(1.0, abs(want)):
+                raise AssertionError(f"row-block sum {got} vs oracle {want}")
+    return out
+
+
+def pdq_query_batch(world: int, queries: int = 16) -> dict:
+    """Throughput of a batch of independent standard queries (1..4 cycled)
+    over 1024 rows: query i runs on rank i % world, no collective."""
+    import torch
+
+    from paper_2503_22227_b200.pdq.columns import encode_column
+    from paper_2503_22227_b200.pdq.dataset import make_dataset
+    from paper_2503_22227_b200.pdq.engine import LocalInverseClient, PdqEngine, standard_query
+
+    cfg, ctx, sk, pk, ev, rng = pdq_session(1024)
+    engine = PdqEngine(ev, cfg)
+    for name, vals in make_dataset(cfg).items():
+        engine.add_column(encode_column(ev, cfg, name, vals, pk, rng))
+    inv = LocalInverseClient(ev, cfg, sk, pk, rng=rng)
+    mask_rng = np.random.default_rng(20240118)
+    rank = int(os.environ.get("RANK", "0"))
+    mine = [i for i in range(queries) if i % world == rank]
+    engine.run(standard_query(1), channel=inv, rng=mask_rng)  # warm-up
+    barrier(world)
+    t0 = time.perf_counter()
+    for i in mine:
+        engine.run(standard_query(1 + i % 4), channel=inv, rng=mask_rng)
+    torch.cuda.synchronize()
+    ms = max_over_ranks((time.perf_counter() - t0) * 1e3, world)
+    return {"queries": queries, "ranks": world, "ms": ms, "queries_s": queries / (ms / 1000.0)}
+
+
+def cpu_baseline_hmult(ops: int = 8, warmup: int = 1, seconds_budget: float = 180.0):
     """The oracle port of the reference algorithm (per-prime gadget key switch,
-    keys.py:186-237, alpha=1, K=0) at N=2^16, L=30 on all host threads."""
+    keys.py:186-237, alpha=1, K=0) at N=2^16, L=30 on all host threads:
+    `warmup` untimed ops, then up to `ops` timed ops (fewer only if the
+    budget runs out; the count is reported)."""
     from oracle import fast
     from oracle import rns_oracle as orc
 
@@ -451,36 +682,49 @@ def cpu_baseline_hmult(seconds_budget: float = 20.0):
     x, y = ct(), ct()
     # random per-prime-gadget key (L digits x (b, a) x L limbs); content does not change cost
     keys = rng.integers(0, Q[0], (LEVELS, 2, LEVELS, n), dtype=np.uint64)
-    times = []
-    t_all = time.perf_counter()
-    while True:
-        t0 = time.perf_counter()
+
+    def one():
         d0, d1, d2 = fast.tensor(x, y, Q)
         b, a = fast.key_switch(d2, keys, Q)
         fast.add(d0, b, Q)
         fast.add(d1, a, Q)
+
+    for _ in range(warmup):
+        one()
+    times = []
+    t_all = time.perf_counter()
+    while len(times) < max(1, ops):
+        t0 = time.perf_counter()
+        one()
         times.append(time.perf_counter() - t0)
-        if time.perf_counter() - t_all > seconds_budget or len(times) >= 8:
+        if time.perf_counter() - t_all > seconds_budget:
             break
     med = statistics.median(times)
+    hi = host_info()
     return {"value": 1.0 / med, "unit": "ops/s", "cores": fast.threads(), "kind": "port",
-            "sample": f"{len(times)} HMult+Relin ops (per-prime gadget, reference algorithm) "
-                      f"at N=2^16, L=30, median {med:.2f} s/op"}
+            "ops": len(times), "warmup": warmup, "cpu_model": hi["cpu_model"],
+            "sample": f"{len(times)} timed HMult+Relin ops after {warmup} warm-up (per-prime "
+                      f"gadget, the reference's algorithm) at N=2^16, L=30, median "
+                      f"{med:.2f} s/op"}
 
 
 def run_reference(args):
+    """The reference arm: the oracle port of the reference's own algorithm
+    (per-prime gadget HMult+Relin, oracle/c, all host threads), one op per
+    step: --warmup untimed ops, then --steps timed ops (median reported)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    base = cpu_baseline_hmult(seconds_budget=max(20.0, 3.0 * args.steps))
+    base = cpu_baseline_hmult(ops=args.steps, warmup=args.warmup)
     v = base["value"]
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "ops/s",
-            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "n_gpus": args.gpus, "steps": base["ops"], "warmup": base["warmup"],
             "ms_per_step": 1000.0 / v, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u64", "data": "synthetic",
             "config": {"workload": "config 4: CKKS HMult+Relin N=2^16 L=30 (reference per-prime "
-                                   "gadget on CPU)"},
-            "cpu_baseline": base,
+                                   "gadget on CPU)", "inputs": "uniform residues mod q_j per limb, "
+                                   "random key words (the content does not change the cost)"},
+            "cpu_baseline": base, "host": host_info(),
             "e2e": {"value": v, "unit": "ops/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
@@ -498,6 +742,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-pdq", action="store_true")
+    ap.add_argument("--quick", action="store_true",
+                    help="headline legs only (no config-2 sweep, config-3, config-4 variants)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
@@ -572,7 +818,21 @@ def main():
     inv_gbs = algo / (ntt_ms["inverse"] / 1000.0) / 1e9
     decrypt_err = w["err"]
     del w
+    torch.cuda.empty_cache()
+    extra = {}
+    if not args.quick and world == 1:
+        # measurement-contract legs: the reference's own
+        # algorithm on the GPU, the 60-bit special primes, the config-2 sweep, config 3
+        extra["config4_parity_mode"] = config4_variant(4, max(3, args.steps // 4), 2, world,
+                                                       gadget=True)
+        extra["config4_hybrid_p60"] = config4_variant(B, max(3, args.steps // 4), 2, world,
+                                                      special_bits=60)
+        extra["config2_sweep"] = config2_sweep()
+        extra["config3"] = config3_legs()
     pdq = pdq_latency(world=world) if not args.no_pdq else None
+    if not args.no_pdq:
+        extra["pdq_rowblocks"] = pdq_rowblocks(world)
+        extra["pdq_query_batch"] = pdq_query_batch(world)
     line = {
         "metric": METRIC, "value": ops, "unit": "ops/s", "n_gpus": world, "steps": args.steps,
         "warmup": max(args.warmup, 3), "ms_per_step": ms, "higher_is_better": True,
@@ -600,7 +860,12 @@ def main():
         "pdq_1024_rows": pdq,
         "config4_rotate": legs["rotate"],
         "config4_rescale": legs["rescale"],
+        "host": host_info(),
     }
+    line.update(extra)
+    ref = reference_cpu_file()
+    if ref is not None:
+        line["reference_cpu_measured"] = ref
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline_hmult()
     if rank == 0:
