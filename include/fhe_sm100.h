@@ -69,6 +69,7 @@ enum {
   FHE_NTT_PATH_FUSED_CP = 3,  /* four-step, one ticketed kernel on cp.async tiles */
   FHE_NTT_PATH_INT = 4,       /* 64-bit integer pipe (a prime >= 2^50)            */
   FHE_NTT_PATH_CLUSTER = 5,   /* one pass, row held by a CTA cluster (DSMEM)      */
+  FHE_NTT_PATH_MM = 6,        /* matrix-product variant (fhe_ntt_mm)              */
   FHE_NTT_PATHS = 8
 };
 uint64_t fhe_ntt_path_count(int path);
@@ -92,6 +93,14 @@ int fhe_ntt_fwd(const FheChain* ch, uint64_t* data, int64_t rows, const int32_t*
                 int limbs, int offset, void* stream);
 int fhe_ntt_inv(const FheChain* ch, uint64_t* data, int64_t rows, const int32_t* mod_idx,
                 int limbs, int offset, void* stream);
+
+/* ---- matrix-product NTT variant: ntt_mm / intt_mm (coremath/ntt.py:201-233),
+ *      the NttVariant.FORCE_MM path of NttChain (ntt.py:266-275) and the
+ *      AUTO rule of ntt_dispatch below degree 1024 (ntt.py:354-364).
+ *      Same canonical words as fhe_ntt_fwd/inv; out must not alias in;
+ *      N <= 2^13. */
+int fhe_ntt_mm(const FheChain* ch, uint64_t* out, const uint64_t* in, int64_t rows,
+               const int32_t* mod_idx, int limbs, int offset, int inverse, void* stream);
 
 /* ---- element-wise family: _kernels.mul_batch/neg_mul_batch/mul_add_batch
  *      (_kernels.py:141-173), fused_neg_multiply / fused_mul_add

@@ -18,7 +18,8 @@ HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "fhe_sm100.h")
 EW_ADD, EW_SUB, EW_NEG, EW_MUL, EW_NEG_MUL, EW_MUL_ADD, EW_MUL_SUB, EW_REDUCE = range(8)
 B_FULL, B_BCAST, B_CONST = range(3)
 # NTT kernel paths (fhe_ntt_path_count)
-NTT_PATHS = {"rows": 0, "split": 1, "fused_tma": 2, "fused_cp": 3, "int": 4, "cluster": 5}
+NTT_PATHS = {"rows": 0, "split": 1, "fused_tma": 2, "fused_cp": 3, "int": 4, "cluster": 5,
+             "mm": 6}
 
 _u64p = ctypes.c_void_p
 _vp = ctypes.c_void_p
@@ -37,6 +38,7 @@ SIGNATURES = {
     "fhe_chain_tables": (_int, [_vp, _int, _vp, _vp, _vp, _vp]),
     "fhe_ntt_fwd": (_int, [_vp, _u64p, _i64, _vp, _int, _int, _vp]),
     "fhe_ntt_inv": (_int, [_vp, _u64p, _i64, _vp, _int, _int, _vp]),
+    "fhe_ntt_mm": (_int, [_vp, _u64p, _u64p, _i64, _vp, _int, _int, _int, _vp]),
     "fhe_ewise": (_int, [_vp, _int, _u64p, _u64p, _u64p, _u64p, _i64, _vp, _int, _int, _int,
                          _vp]),
     "fhe_tensor": (_int, [_vp, _u64p, _u64p, _u64p, _int, _i64, _i64, _i64, _i64, _int, _vp]),

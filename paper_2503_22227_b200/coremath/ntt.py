@@ -25,6 +25,11 @@ class ShapeError(ValueError):
     pass
 
 
+class ConfigurationError(RuntimeError):
+    """The matrix variant was requested without materialize_matrix()
+    (reference ntt.py:34-35)."""
+
+
 class NttVariant(str, Enum):
     AUTO = "auto"
     FORCE_BM = "force_bm"
@@ -133,6 +138,15 @@ class DeviceChain:
         _native.check(fn(self.handle, _native.ptr(data), rows, idx, limbs, offset,
                          _native.stream_handle(stream)), "fhe_ntt")
 
+    def transform_mm(self, out, data, rows: int, inverse: bool, mod_idx=None, stream=None):
+        """Matrix-product variant (fhe_ntt_mm) of ``rows`` device rows into
+        ``out`` (must not alias ``data``)."""
+        lib = _native.lib()
+        idx, limbs, offset = self._rowmap(rows, mod_idx)
+        _native.check(lib.fhe_ntt_mm(self.handle, _native.ptr(out), _native.ptr(data), rows, idx,
+                                     limbs, offset, int(bool(inverse)),
+                                     _native.stream_handle(stream)), "fhe_ntt_mm")
+
 
 class NttTables:
     """Per-(degree, modulus) tables, read back from the device chain
@@ -148,9 +162,21 @@ class NttTables:
         self.modulus = m
         self._chain = DeviceChain([m.value], degree.bit_length() - 1)
         self.psi, self.psi_powers, self.inv_psi_powers, self.n_inv = self._chain.tables(0)
+        self.dft_matrix = None
+        self.inv_dft_matrix = None
 
     def exponent_map(self) -> np.ndarray:
         return exponent_map(self.degree)
+
+    def materialize_matrix(self):
+        """Enable the matrix variant (reference ntt.py:101-124).  The device
+        kernel reads every entry psi^(exp_j * i) from the psi table, so the
+        n x n matrices are not stored: the attributes only record that the
+        variant was set up (ntt_mm raises ConfigurationError before)."""
+        if self.degree > 1 << 13:
+            raise ParameterError("matrix NTT variant supports degree <= 2^13")
+        self.dft_matrix = "device"
+        self.inv_dft_matrix = "device"
 
 
 class NttChain:
@@ -178,17 +204,80 @@ class NttChain:
         rows = a.shape[0]
         if mod_idx is None:
             mod_idx = np.arange(rows) % len(self.dev.primes)
+        mm = self.variant is NttVariant.FORCE_MM
         if isinstance(a, torch.Tensor):
-            out = a.contiguous().clone()
+            src = a.contiguous()
+        else:
+            host = np.ascontiguousarray(a, dtype=np.uint64)
+            src = torch.from_numpy(host.view(np.int64)).cuda()
+        if mm:
+            # forced matrix variant (reference NttChain._per_row -> ntt_dispatch,
+            # ntt.py:266-275): same words as the butterflies
+            out = torch.empty_like(src)
+            self.dev.transform_mm(out, src, rows, inverse, mod_idx)
+        else:
+            out = src.clone() if isinstance(a, torch.Tensor) else src
             self.dev.transform(out, rows, inverse, mod_idx)
-            return out
-        host = np.ascontiguousarray(a, dtype=np.uint64)
-        dev = torch.from_numpy(host.view(np.int64)).cuda()
-        self.dev.transform(dev, rows, inverse, mod_idx)
-        return dev.cpu().numpy().view(np.uint64)
+        return out if isinstance(a, torch.Tensor) else out.cpu().numpy().view(np.uint64)
 
     def forward(self, a, mod_idx=None):
         return self._run(a, mod_idx, inverse=False)
 
     def inverse(self, a, mod_idx=None):
         return self._run(a, mod_idx, inverse=True)
+
+
+# -- single-row transforms and the variant dispatch (reference ntt.py:145-233,
+#    354-364); every variant runs on the device and returns canonical words.
+
+
+def _single(vec, tables: NttTables, inverse: bool, mm: bool):
+    import torch
+
+    v = np.asarray(vec)
+    if v.shape != (tables.degree,):
+        raise ShapeError(f"expected length {tables.degree}, got {v.shape}")
+    if mm and tables.dft_matrix is None:
+        raise ConfigurationError("dft matrix not materialized; call materialize_matrix()")
+    src = torch.from_numpy(np.ascontiguousarray(v, dtype=np.uint64).view(np.int64)).cuda()
+    src = src.reshape(1, -1)
+    if mm:
+        out = torch.empty_like(src)
+        tables._chain.transform_mm(out, src, 1, inverse)
+    else:
+        out = src
+        tables._chain.transform(out, 1, inverse)
+    return out.cpu().numpy().view(np.uint64).reshape(-1)
+
+
+def ntt_bm(coeffs, tables: NttTables) -> np.ndarray:
+    """Forward negacyclic NTT, butterflies (reference ntt.py:145-169)."""
+    return _single(coeffs, tables, False, False)
+
+
+def intt_bm(evals, tables: NttTables) -> np.ndarray:
+    """Inverse of ntt_bm (reference ntt.py:172-198)."""
+    return _single(evals, tables, True, False)
+
+
+def ntt_mm(coeffs, tables: NttTables) -> np.ndarray:
+    """Forward NTT as an n x n matrix-vector product (reference ntt.py:220-225)."""
+    return _single(coeffs, tables, False, True)
+
+
+def intt_mm(evals, tables: NttTables) -> np.ndarray:
+    """Inverse matrix variant (reference ntt.py:228-233)."""
+    return _single(evals, tables, True, True)
+
+
+def ntt_dispatch(coeffs, tables: NttTables, policy=NttVariant.AUTO,
+                 inverse: bool = False) -> np.ndarray:
+    """Matrix product below degree 1024, butterflies above (reference
+    ntt.py:354-364)."""
+    policy = NttVariant(policy)
+    if policy is NttVariant.FORCE_MM or (policy is NttVariant.AUTO
+                                         and tables.degree < MATRIX_DEGREE_LIMIT):
+        if tables.dft_matrix is None:
+            tables.materialize_matrix()
+        return intt_mm(coeffs, tables) if inverse else ntt_mm(coeffs, tables)
+    return intt_bm(coeffs, tables) if inverse else ntt_bm(coeffs, tables)

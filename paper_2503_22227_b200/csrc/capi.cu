@@ -120,6 +120,18 @@ int fhe_ntt_inv(const FheChain* ch, uint64_t* data, int64_t rows, const int32_t*
                     (cudaStream_t)stream);
 }
 
+int fhe_ntt_mm(const FheChain* ch, uint64_t* out, const uint64_t* in, int64_t rows,
+               const int32_t* mod_idx, int limbs, int offset, int inverse, void* stream) {
+  int rc = check_map(ch, rows, mod_idx, limbs, offset);
+  if (rc) return rc;
+  if (out == in && rows > 0) {
+    fhe_set_error("fhe_ntt_mm: out must not alias in");
+    return -1;
+  }
+  return launch_ntt_mm(ch->dev, out, in, (int)rows, RowMap{mod_idx, limbs, offset}, inverse != 0,
+                       (cudaStream_t)stream);
+}
+
 int fhe_ewise(const FheChain* ch, int op, uint64_t* out, const uint64_t* a, const uint64_t* b,
               const uint64_t* c, int64_t rows, const int32_t* mod_idx, int limbs, int offset,
               int b_mode, void* stream) {

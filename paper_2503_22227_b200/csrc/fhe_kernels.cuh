@@ -36,6 +36,10 @@ struct NttArgs {
 };
 int launch_ntt(const DevChain& ch, const NttArgs& a, bool inverse, cudaStream_t st);
 unsigned long long ntt_path_count(int path);
+void ntt_path_hit(int path);
+// ntt_mm.cu: matrix-product variant (reference ntt_mm / intt_mm), out != in
+int launch_ntt_mm(const DevChain& ch, u64* out, const u64* in, int rows, RowMap map, bool inverse,
+                  cudaStream_t st);
 // per-chain scratch of the fused four-step NTT (tile tickets, group counters)
 void* fuse_scratch_new();
 void fuse_scratch_free(void* p);

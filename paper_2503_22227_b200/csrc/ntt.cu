@@ -44,6 +44,9 @@
 // and the bench of WHICH kernel ran (FHE_NTT_PATH_* in fhe_sm100.h).
 static std::atomic<unsigned long long> g_ntt_path[FHE_NTT_PATHS];
 static void path_hit(int p) { g_ntt_path[p].fetch_add(1, std::memory_order_relaxed); }
+void ntt_path_hit(int p) {
+  if (p >= 0 && p < FHE_NTT_PATHS) path_hit(p);
+}
 unsigned long long ntt_path_count(int p) {
   return (p >= 0 && p < FHE_NTT_PATHS) ? g_ntt_path[p].load(std::memory_order_relaxed) : 0;
 }

@@ -169,3 +169,21 @@ def test_pdq_plaintext_oracle_matches_reference_index(golden):
     mask = oracle_result(standard_query(1), data)
     assert mask.astype(int).tolist() == golden["pdq"]["queries"]["1"]["value"]
     assert oracle_result(standard_query(2), data) == golden["pdq"]["queries"]["2"]["oracle"]
+
+
+def test_kernel_seam_signatures_match_reference():
+    """The seam module mirrors rnsfhe.coremath._kernels (_kernels.py:86-173):
+    same names and positional parameters (it imports without a GPU)."""
+    import inspect
+
+    from paper_2503_22227_b200.coremath import _kernels
+
+    want = {
+        "ntt_batch": ["a", "psi", "psi_sh", "q", "mod_idx"],
+        "intt_batch": ["a", "ipsi", "ipsi_sh", "n_inv", "n_inv_sh", "q", "mod_idx"],
+        "mul_batch": ["a", "b", "out", "q", "qinv", "r2", "mod_idx"],
+        "neg_mul_batch": ["a", "b", "out", "q", "qinv", "r2", "mod_idx"],
+        "mul_add_batch": ["a", "b", "c", "out", "q", "qinv", "r2", "mod_idx"],
+    }
+    for name, params in want.items():
+        assert list(inspect.signature(getattr(_kernels, name)).parameters) == params, name

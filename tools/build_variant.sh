@@ -9,5 +9,5 @@ nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler
   --expt-relaxed-constexpr -cudart static -Xptxas -v $* -c ntt.cu -o build/ntt_$NAME.o \
   2> build/ntt_$NAME.ptxas.log
 nvcc -gencode arch=compute_100a,code=sm_100a -shared -cudart static -o ../lib/libfhe_$NAME.so \
-  build/context.o build/ntt_$NAME.o build/poly.o build/keyswitch.o build/behz.o build/capi.o
+  build/context.o build/ntt_$NAME.o build/ntt_mm.o build/poly.o build/keyswitch.o build/behz.o build/capi.o
 echo built lib/libfhe_$NAME.so
