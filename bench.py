@@ -450,6 +450,22 @@ def pdq_latency(reps: int = 3, world: int = 1):
         if spec.agg == "index" and not (np.asarray(got) == want).all():
             raise AssertionError("PDQ-1 mask differs from the plaintext oracle")
         out[f"q{qid}_ms"] = statistics.median(times)
+    if world == 1:
+        # the same queries with the device part replayed as one CUDA graph
+        # (pdq/graphs.py); the two-party inverse stays eager
+        from paper_2503_22227_b200.pdq.graphs import CapturedQuery
+
+        for qid in (1, 2, 3, 4):
+            cq = CapturedQuery(engine, standard_query(qid))
+            times = []
+            for _ in range(max(reps, 5)):
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                cq.run(channel=inv, rng=mask_rng)
+                torch.cuda.synchronize()
+                times.append((time.perf_counter() - t0) * 1e3)
+            out[f"q{qid}_graph_ms"] = statistics.median(times)
+            del cq
     out["ranks"] = world
     out["sharding"] = ("(atom, digit) units over ranks, one all-gather of the stacked unit results" if world > 1 else "none")
     return out

@@ -127,6 +127,10 @@ int fhe_automorph(uint64_t* out, const uint64_t* in, int64_t rows, int log_n, ui
  *      is exactly the reference gadget (keys.py:1-7, 128-141, 186-237). */
 int fhe_context_create(const uint64_t* q_primes, int L, const uint64_t* p_primes, int K,
                        int alpha, int log_n, FheContext** out);
+/* Build the BGV modulus-switch constants of plain modulus t (bgv.py:215-260)
+ * now, so fhe_rescale(t_plain = t) never allocates; Context creation calls it
+ * for its plain modulus.  Idempotent. */
+int fhe_context_prepare_plain(FheContext* ctx, uint64_t t);
 int fhe_context_destroy(FheContext* ctx);
 const FheChain* fhe_context_chain(const FheContext* ctx);
 

@@ -45,6 +45,7 @@ SIGNATURES = {
     "fhe_automorph": (_int, [_u64p, _u64p, _i64, _int, ctypes.c_uint64, _vp]),
     "fhe_context_create": (_int, [_vp, _int, _vp, _int, _int, _int, ctypes.POINTER(_vp)]),
     "fhe_context_destroy": (_int, [_vp]),
+    "fhe_context_prepare_plain": (_int, [_vp, ctypes.c_uint64]),
     "fhe_context_chain": (_vp, [_vp]),
     "fhe_rescale_workspace": (_sz, [_vp, _int, _int]),
     "fhe_rescale": (_int, [_vp, _u64p, _u64p, _int, _int, ctypes.c_uint64, _vp, _sz, _vp]),

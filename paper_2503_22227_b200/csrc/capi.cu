@@ -209,6 +209,20 @@ int fhe_context_create(const uint64_t* q_primes, int L, const uint64_t* p_primes
   })
 }
 
+int fhe_context_prepare_plain(FheContext* ctx, uint64_t t) {
+  FHE_TRY({
+    if (!ctx || t < 2) {
+      fhe_set_error("fhe_context_prepare_plain: bad arguments");
+      return -1;
+    }
+    if (!get_plain_plan(ctx, t)) {
+      fhe_set_error("fhe_context_prepare_plain: device allocation failed");
+      return -2;
+    }
+    return 0;
+  })
+}
+
 int fhe_context_destroy(FheContext* ctx) {
   if (!ctx) return 0;
   for (auto& lp : ctx->levels)

@@ -213,7 +213,11 @@ int build_chain(const u64* primes, int count, int log_n, FheChain* ch) {
   ch->dev.ninv_w1_d = fp64 ? (const double2*)(b + o_nwd) : nullptr;
   ch->dev.tws = (fp64 && log_n >= 13) ? (const double2*)(b + o_tws) : nullptr;
   ch->dev.tws_dir = (long)tws_dir;
-  ch->dev.fuse = fuse_scratch_new();
+  ch->dev.fuse = fuse_scratch_new(log_n);
+  if (!ch->dev.fuse) {
+    fhe_set_error("fused NTT scratch allocation failed");
+    return -2;
+  }
   return 0;
 }
 
@@ -224,6 +228,40 @@ void free_chain(FheChain* ch) {
   }
   if (ch && ch->dmem) cudaFree(ch->dmem);
   if (ch) ch->dmem = nullptr;
+}
+
+// Packed mma.sync m16n8k32 B fragments of the byte-split conversion matrix
+// W'[(s, a)][(t, b)] = byte b of [w(s, t) 2^(8a)]_{p(t)} (bconv_imma.cuh):
+// per target t and k-step, lane (gr = lane / 4 = byte b, gq = lane % 4) holds
+// rows k = 32 ks + 4 gq + i (b0) and + 16 (b1), byte i = row k's byte.
+template <class W, class P>
+static void pack_bfrag(std::vector<uint2>& out, int ns, int nt, int ks, W w, P p) {
+  std::vector<u64> v((size_t)ns * 7 * nt);
+  for (int s = 0; s < ns; ++s)
+    for (int t = 0; t < nt; ++t) {
+      const u64 pt = p(t);
+      u64 x = w(s, t) % pt;
+      for (int a = 0; a < 7; ++a) {
+        v[((size_t)s * 7 + a) * nt + t] = x;
+        x = mulmod_h(x, 256 % pt, pt);
+      }
+    }
+  auto byte = [&](int k, int t, int b) -> unsigned {
+    if (k >= 7 * ns || b >= 7) return 0;
+    return (unsigned)((v[(size_t)k * nt + t] >> (8 * b)) & 0xff);
+  };
+  for (int t = 0; t < nt; ++t)
+    for (int kk = 0; kk < ks; ++kk)
+      for (int lane = 0; lane < 32; ++lane) {
+        const int gq = lane & 3, gr = lane >> 2;
+        unsigned b0 = 0, b1 = 0;
+        for (int i = 0; i < 4; ++i) {
+          const int k0 = 32 * kk + 4 * gq + i;
+          b0 |= byte(k0, t, gr) << (8 * i);
+          b1 |= byte(k0 + 16, t, gr) << (8 * i);
+        }
+        out.push_back(make_uint2(b0, b1));
+      }
 }
 
 // Product of primes[idx] for idx in [lo, hi) except `skip`, reduced mod m.
@@ -314,7 +352,33 @@ int build_levels(FheContext* ctx) {
           down_w_d.push_back(make_double2((double)w, (double)w / (double)pr[j]));
         }
     }
+    // tensor-core base conversion tables (every chain prime < 2^56)
+    bool bf_ok = K <= 16;
+    for (u64 q : pr) bf_ok &= q < ((u64)1 << 56) && q >= ((u64)1 << 39);  // bc_reduce71 domain
+    std::vector<uint2> up_bf, down_bf;
+    std::vector<int> up_bf_off;
+    if (bf_ok) {
+      int max_na = 0;
+      for (int di = 0; di < D; ++di) max_na = std::max(max_na, lp.dig_na[di]);
+      bf_ok = max_na <= 16;
+      lp.max_na = max_na;
+      lp.up_ks = (7 * max_na + 31) / 32;
+      lp.down_ks = (7 * K + 31) / 32;
+      for (int di = 0; bf_ok && di < D; ++di) {
+        const int s0 = lp.dig_s0[di], na = lp.dig_na[di], nt = l + K - na;
+        up_bf_off.push_back((int)up_bf.size());
+        pack_bfrag(up_bf, na, nt, lp.up_ks,
+                   [&](int s, int t) { return up_w[lp.dig_w_off[di] + s * nt + t]; },
+                   [&](int t) { return pr[cp(t < s0 ? t : t + na)]; });
+      }
+      if (K > 0)
+        pack_bfrag(down_bf, K, l, lp.down_ks,
+                   [&](int k, int j) { return down_w[(size_t)k * l + j]; },
+                   [&](int j) { return pr[j]; });
+    }
+    lp.bf_ok = bf_ok;
     Packer pk;
+    const size_t o14 = pk.addv(up_bf), o15 = pk.addv(up_bf_off), o16 = pk.addv(down_bf);
     const size_t o1 = pk.addv(up_inv), o2 = pk.addv(up_w), o3 = pk.addv(ext_prime),
                  o4 = pk.addv(info), o5 = pk.addv(down_inv), o6 = pk.addv(down_w),
                  o7 = pk.addv(p_inv), o8 = pk.addv(rs_inv), o9 = pk.addv(rs_qlast);
@@ -334,6 +398,11 @@ int build_levels(FheContext* ctx) {
     lp.p_inv = (const WPair*)(b + o7);
     lp.rs_inv = (const WPair*)(b + o8);
     lp.rs_qlast = (const u64*)(b + o9);
+    if (bf_ok) {
+      lp.up_bf = (const uint2*)(b + o14);
+      lp.up_bf_off = (const int*)(b + o15);
+      lp.down_bf = K > 0 ? (const uint2*)(b + o16) : nullptr;
+    }
     if (fp64) {
       lp.up_inv_d = (const double2*)(b + o10);
       lp.up_w_d = (const double2*)(b + o11);
@@ -353,16 +422,27 @@ const PlainPlan* get_plain_plan(FheContext* ctx, u64 t) {
   pp->dmem.assign(ctx->L + 1, nullptr);
   pp->t_mod.assign(ctx->L + 1, nullptr);
   pp->tinv_last.assign(ctx->L + 1, WPair{0, 0});
+  // every level's (t mod q_j) table in one allocation: level l at offset
+  // (l - 2)(l - 1) / 2 words
+  std::vector<u64> all;
   for (int l = 2; l <= ctx->L; ++l) {
-    std::vector<u64> tm(l - 1);
-    for (int j = 0; j + 1 < l; ++j) tm[j] = t % pr[j];
+    for (int j = 0; j + 1 < l; ++j) all.push_back(t % pr[j]);
     const u64 ql = pr[l - 1];
     pp->tinv_last[l] = wpair(invmod_h(t % ql, ql), ql);
-    void* d = nullptr;
-    if (cudaMalloc(&d, tm.size() * 8) != cudaSuccess) return nullptr;
-    cudaMemcpy(d, tm.data(), tm.size() * 8, cudaMemcpyHostToDevice);
-    pp->dmem[l] = d;
-    pp->t_mod[l] = (const u64*)d;
+  }
+  void* d = nullptr;
+  if (!all.empty()) {
+    if (cudaMalloc(&d, all.size() * 8) != cudaSuccess) return nullptr;
+    if (cudaMemcpy(d, all.data(), all.size() * 8, cudaMemcpyHostToDevice) != cudaSuccess) {
+      cudaFree(d);
+      return nullptr;
+    }
+  }
+  pp->dmem[0] = d;
+  size_t off = 0;
+  for (int l = 2; l <= ctx->L; ++l) {
+    pp->t_mod[l] = (const u64*)d + off;
+    off += l - 1;
   }
   PlainPlan* raw = pp.get();
   ctx->plain[t] = std::move(pp);

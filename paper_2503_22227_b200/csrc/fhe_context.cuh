@@ -38,6 +38,14 @@ struct LevelPlan {
   const double2* up_w_d = nullptr;
   const double2* down_inv_d = nullptr;
   const double2* down_w_d = nullptr;
+  // tensor-core base conversion (bconv_imma.cuh), every chain prime < 2^56:
+  // packed byte-split W' fragments, ModUp per digit ([nt][up_ks][32] each,
+  // offsets in up_bf_off) and ModDown ([level][down_ks][32])
+  bool bf_ok = false;
+  int up_ks = 0, down_ks = 0, max_na = 0;
+  const uint2* up_bf = nullptr;
+  const int* up_bf_off = nullptr;
+  const uint2* down_bf = nullptr;
   void* dmem = nullptr;
 };
 

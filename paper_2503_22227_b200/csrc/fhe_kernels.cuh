@@ -41,7 +41,7 @@ void ntt_path_hit(int path);
 int launch_ntt_mm(const DevChain& ch, u64* out, const u64* in, int rows, RowMap map, bool inverse,
                   cudaStream_t st);
 // per-chain scratch of the fused four-step NTT (tile tickets, group counters)
-void* fuse_scratch_new();
+void* fuse_scratch_new(int log_n);
 void fuse_scratch_free(void* p);
 inline int launch_ntt(const DevChain& ch, u64* data, const u64* in, int rows, RowMap map,
                       bool inverse, cudaStream_t st) {

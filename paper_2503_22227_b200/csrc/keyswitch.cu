@@ -702,6 +702,19 @@ bool fuse_finish_enabled() {
   return on == 1;
 }
 
+#include "bconv_imma.cuh"
+
+// tensor-core base conversions (default when the level has the tables and a
+// digit of >= 4 limbs; FHE_BCONV_IMMA=0 keeps the FP64 / integer kernels)
+bool bconv_imma_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("FHE_BCONV_IMMA");
+    on = (e && e[0] == '0') ? 0 : 1;
+  }
+  return on == 1;
+}
+
 int mac_chunk(const std::vector<u64>& primes) {
   u64 mx = 0;
   for (u64 p : primes) mx = p > mx ? p : mx;
@@ -766,7 +779,16 @@ int run_keyswitch(const FheContext& ctx, int level, const u64* d, long d_stride,
       max_w = std::max(max_w, lp.dig_na[di] * (level + K - lp.dig_na[di]));
     const size_t smem = (size_t)max_w * sizeof(u64);
     dim3 grid((unsigned)std::max<long>(1, std::min<long>(n / kThreads, 1024)), lp.digits, batch);
-    if (ch.fp64_ok && lp.up_w_d) {
+    if (lp.bf_ok && lp.max_na >= 4 && bconv_imma_enabled()) {
+      BconvArgs ba{c, (long)level * n, ext, (long)lp.ext_rows * n, lp.dig_info, lp.up_bf_off,
+                   lp.up_bf, lp.up_inv, lp.up_inv_d, lp.ext_prime, 0, 0, 0, level, K};
+      int max_nt = 0;
+      for (int di = 0; di < lp.digits; ++di) max_nt = std::max(max_nt, level + K - lp.dig_na[di]);
+      dim3 g((unsigned)std::max<long>(1, std::min<long>(n / (32 * kBcWarps), 64)), lp.digits,
+             batch);
+      rc = launch_bconv(ch, ba, lp.max_na, max_nt, g, st);
+      if (rc) return rc;
+    } else if (ch.fp64_ok && lp.up_w_d) {
       int max_na = 0;
       for (int di = 0; di < lp.digits; ++di) max_na = std::max(max_na, lp.dig_na[di]);
       const size_t smem_d = ((size_t)max_w + level + K) * sizeof(double2);
@@ -779,6 +801,7 @@ int run_keyswitch(const FheContext& ctx, int level, const u64* d, long d_stride,
       if (max_na <= 4) go(modup_fp_kernel<4, FHE_MODUP_U>);
       else if (max_na <= 12) go(modup_fp_kernel<12, FHE_MODUP_U>);
       else go(modup_fp_kernel<16, FHE_MODUP_U>);
+      FHE_LAUNCH_CHECK();
     } else {
       if (smem > 48 * 1024)
         cudaFuncSetAttribute(modup_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -786,8 +809,8 @@ int run_keyswitch(const FheContext& ctx, int level, const u64* d, long d_stride,
       modup_kernel<<<grid, kThreads, smem, st>>>(ch, c, (long)level * n, ext,
                                                  (long)lp.ext_rows * n, lp.dig_info, lp.up_inv,
                                                  lp.up_w, level, K, L, chunk);
+      FHE_LAUNCH_CHECK();
     }
-    FHE_LAUNCH_CHECK();
     if (lp.ext_rows > 0) {
       rc = launch_ntt(ch, ext, ext, batch * lp.ext_rows,
                       RowMap{lp.ext_prime, lp.ext_rows, 0}, false, st);
@@ -842,13 +865,24 @@ int run_keyswitch(const FheContext& ctx, int level, const u64* d, long d_stride,
         kern<<<grid, kThreads, smem_d, st>>>(ch, accP, conv, lp.down_inv_d, lp.down_w_d, level,
                                              K, L);
       };
-      if (K <= 4) go(moddown_conv_fp_kernel<4, FHE_MODUP_U>);
-      else if (K <= 12) go(moddown_conv_fp_kernel<12, FHE_MODUP_U>);
-      else go(moddown_conv_fp_kernel<16, FHE_MODUP_U>);
-    } else
+      if (lp.bf_ok && lp.down_bf && K >= 4 && bconv_imma_enabled()) {
+        BconvArgs ba{accP, (long)K * n, conv, (long)level * n, nullptr, nullptr, lp.down_bf,
+                     lp.down_inv, lp.down_inv_d, nullptr, K, level, L, level, K};
+        dim3 g((unsigned)std::max<long>(1, std::min<long>(n / (32 * kBcWarps), 64)), 1,
+               batch * 2);
+        rc = launch_bconv(ch, ba, K, level, g, st);
+        if (rc) return rc;
+      } else {
+        if (K <= 4) go(moddown_conv_fp_kernel<4, FHE_MODUP_U>);
+        else if (K <= 12) go(moddown_conv_fp_kernel<12, FHE_MODUP_U>);
+        else go(moddown_conv_fp_kernel<16, FHE_MODUP_U>);
+        FHE_LAUNCH_CHECK();
+      }
+    } else {
       moddown_conv_kernel<<<grid, kThreads, smem, st>>>(ch, accP, conv, lp.down_inv, lp.down_w,
                                                         level, K, L, chunk);
-    FHE_LAUNCH_CHECK();
+      FHE_LAUNCH_CHECK();
+    }
   }
   // forward NTT of the conversion with the ModDown finish fused into its
   // last pass when the TMA chunk path runs it; otherwise a separate pass

@@ -1131,7 +1131,22 @@ int launch_ntt(const DevChain& ch, const NttArgs& a, bool inverse, cudaStream_t 
   }
 }
 
-void* fuse_scratch_new() { return new FuseScratch(); }
+// The counter slabs are allocated with the chain (log N >= 13, where the fused
+// transforms run): 64K groups per launch covers every transform that fits in
+// HBM (a group is >= 8 rows of 2^13+ words), so fuse_slab never has to grow
+// (and synchronise the device) on a first-use path.
+void* fuse_scratch_new(int log_n) {
+  FuseScratch* fs = new FuseScratch();
+  if (log_n >= 13) {
+    const size_t ints = 1 << 16;
+    if (cudaMalloc(&fs->dev, ints * kFuseSlabs * sizeof(int)) != cudaSuccess) {
+      delete fs;
+      return nullptr;
+    }
+    fs->slab_ints = ints;
+  }
+  return fs;
+}
 
 void fuse_scratch_free(void* p) {
   FuseScratch* fs = static_cast<FuseScratch*>(p);

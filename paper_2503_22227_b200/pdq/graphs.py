@@ -1,0 +1,65 @@
+"""CUDA-graph replay of a private-dataset query.
+
+A query is ~300 operator calls and ~800 small kernels at N = 4096; in eager
+mode the host (Python operator dispatch, 13-35 us per call) dominates the
+latency.  Everything before the two-party inverse is pure device work with a
+fixed shape for a given (engine, query), so it is recorded ONCE into a CUDA
+graph and replayed per query with one launch:
+
+* the device part runs once eagerly first, so every cached plaintext constant,
+  workspace and table the circuit touches already lives in HBM (nothing is
+  uploaded or allocated on the device while capturing);
+* during capture the context's memory pool is swapped for a private arena
+  that belongs to the graph: the capture's temporaries reuse each other's
+  blocks exactly as they will on every replay, and no block the graph
+  writes can be handed to anyone else afterwards;
+* inputs are the engine's resident column ciphertexts and the query's
+  constant columns (passed at capture and kept alive here); the outputs are
+  the captured ciphertexts, overwritten by every replay -- a result is valid
+  until the next replay of the same CapturedQuery;
+* the host part (two-party inverse: decrypt, reciprocal, re-encrypt) and the
+  one or two products after it run eagerly (PdqEngine.finish).
+
+Every replay computes the same words as the eager path (same kernels, same
+order); tests/test_gpu_pdq_graph.py checks them against the reference goldens.
+Single-GPU only (the sharded layouts exchange through collectives).
+"""
+
+from __future__ import annotations
+
+from ..pools import MemoryPool
+from .engine import PdqEngine, QueryResult, QuerySpec
+
+
+class CapturedQuery:
+    def __init__(self, engine: PdqEngine, spec: QuerySpec, temps: dict | None = None,
+                 arena_mb: int = 512):
+        import torch
+
+        if engine.group is not None and engine.group.world > 1:
+            raise ValueError("CUDA-graph capture is single-GPU (the sharded query exchanges "
+                             "through collectives)")
+        self.engine, self.spec, self.temps = engine, spec, temps or {}
+        ctx = engine.ev.ctx
+        # 1. eager warm-up of the device part (no inverse: consumes no randomness)
+        engine.device_part(spec, self.temps)
+        torch.cuda.synchronize()
+        # 2. capture the device part with a private pool arena
+        self.pool = MemoryPool(1, unit_mb=arena_mb, cap_mb=arena_mb)
+        self.graph = torch.cuda.CUDAGraph()
+        saved = ctx.pool
+        ctx.pool = self.pool
+        try:
+            with torch.cuda.graph(self.graph):
+                self.parts = engine.device_part(spec, self.temps)
+        finally:
+            ctx.pool = saved
+        torch.cuda.synchronize()
+
+    def replay(self) -> dict:
+        """The device part: one graph launch on the current stream."""
+        self.graph.replay()
+        return self.parts
+
+    def run(self, channel=None, rng=None) -> QueryResult:
+        return self.engine.finish(self.spec, self.replay(), channel, rng)

@@ -229,3 +229,23 @@ print(h(a), h(c))
         assert out.returncode == 0, out.stderr[-2000:]
         digests.add(out.stdout.strip().splitlines()[-1])
     assert len(digests) == 1, digests
+
+
+def test_tensor_core_bconv_equals_fp64_bconv():
+    """The tensor-core base conversion (csrc/bconv_imma.cuh, the default)
+    and the FP64-pipe conversion give the same words for HMult+Relin (batch
+    3, ragged last digit) and rotate."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    script = os.path.join(os.path.dirname(os.path.abspath(__file__)), "helpers", "bconv_paths.py")
+    res = {}
+    for flag in ("1", "0"):
+        r = subprocess.run([sys.executable, script], capture_output=True, text=True, timeout=600,
+                           env=dict(os.environ, FHE_BCONV_IMMA=flag))
+        assert r.returncode == 0, r.stderr[-2000:]
+        res[flag] = json.loads(r.stdout.strip().splitlines()[-1])
+    assert res["1"]["hmult"] == res["0"]["hmult"]
+    assert res["1"]["rotate"] == res["0"]["rotate"]

@@ -10,7 +10,9 @@ rep = sys.argv[1]
 n = int(sys.argv[2]) if len(sys.argv) > 2 else 25
 txt = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv"], capture_output=True,
                      text=True).stdout
-rows = list(csv.reader(io.StringIO(txt)))
+kidx = int(sys.argv[3]) if len(sys.argv) > 3 else 0
+blk = txt.split('"Kernel Name"')[1 + kidx]
+rows = list(csv.reader(io.StringIO('"Kernel Name"' + blk)))
 h = rows[1]
 data = [r for r in rows[2:] if len(r) == len(h)]
 ia, isrc = h.index("Address"), h.index("Source")
