@@ -130,6 +130,21 @@ int fhe_context_create(const uint64_t* q_primes, int L, const uint64_t* p_primes
 /* Build the BGV modulus-switch constants of plain modulus t (bgv.py:215-260)
  * now, so fhe_rescale(t_plain = t) never allocates; Context creation calls it
  * for its plain modulus.  Idempotent. */
+/* ---- exact CRT lift of decrypted residues (the step after the path,
+ *      SURVEY 8(f)2): replaces crt_reconstruct_poly (crt.py:84-100) in
+ *        FHE_CRT_FLOAT  ckks_decode (ckks.py:157-166): double out[n] =
+ *                       float(centred v) / scale (scale 0: no division)
+ *        FHE_CRT_MOD_T  bgv_decrypt (bgv.py:89-101): u64 out[n] =
+ *                       (centred v % t) * inv_f % t
+ *        FHE_CRT_BFV    bfv_decrypt (bfv.py:106-117): u64 out[n] =
+ *                       ((t * centred v + Q // 2) // Q) % t
+ *      rows: the level coefficient-domain residue rows; Python integer
+ *      semantics exactly (float() rounds to nearest even; +-inf where
+ *      Python raises OverflowError). */
+enum { FHE_CRT_FLOAT = 0, FHE_CRT_MOD_T = 1, FHE_CRT_BFV = 2 };
+int fhe_crt_lift(const FheContext* ctx, int mode, void* out, const uint64_t* rows, int level,
+                 double scale, uint64_t t, uint64_t inv_f, void* stream);
+
 int fhe_context_prepare_plain(FheContext* ctx, uint64_t t);
 int fhe_context_destroy(FheContext* ctx);
 const FheChain* fhe_context_chain(const FheContext* ctx);

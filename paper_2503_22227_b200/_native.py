@@ -15,6 +15,7 @@ LIB_PATH = os.environ.get("FHE_SM100_LIB") or os.path.join(_HERE, "lib", "libfhe
 HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "fhe_sm100.h")
 
 # op codes / operand modes (mirror include/fhe_sm100.h)
+CRT_FLOAT, CRT_MOD_T, CRT_BFV = range(3)
 EW_ADD, EW_SUB, EW_NEG, EW_MUL, EW_NEG_MUL, EW_MUL_ADD, EW_MUL_SUB, EW_REDUCE = range(8)
 B_FULL, B_BCAST, B_CONST = range(3)
 # NTT kernel paths (fhe_ntt_path_count)
@@ -46,6 +47,8 @@ SIGNATURES = {
     "fhe_context_create": (_int, [_vp, _int, _vp, _int, _int, _int, ctypes.POINTER(_vp)]),
     "fhe_context_destroy": (_int, [_vp]),
     "fhe_context_prepare_plain": (_int, [_vp, ctypes.c_uint64]),
+    "fhe_crt_lift": (_int, [_vp, _int, _vp, _vp, _int, ctypes.c_double, ctypes.c_uint64,
+                            ctypes.c_uint64, _vp]),
     "fhe_context_chain": (_vp, [_vp]),
     "fhe_rescale_workspace": (_sz, [_vp, _int, _int]),
     "fhe_rescale": (_int, [_vp, _u64p, _u64p, _int, _int, ctypes.c_uint64, _vp, _sz, _vp]),

@@ -209,6 +209,17 @@ int fhe_context_create(const uint64_t* q_primes, int L, const uint64_t* p_primes
   })
 }
 
+int fhe_crt_lift(const FheContext* ctx, int mode, void* out, const uint64_t* rows, int level,
+                 double scale, uint64_t t, uint64_t inv_f, void* stream) {
+  FHE_TRY({
+    if (!ctx || !out || !rows) {
+      fhe_set_error("fhe_crt_lift: null argument");
+      return -1;
+    }
+    return run_crt_lift(*ctx, mode, out, rows, level, scale, t, inv_f, (cudaStream_t)stream);
+  })
+}
+
 int fhe_context_prepare_plain(FheContext* ctx, uint64_t t) {
   FHE_TRY({
     if (!ctx || t < 2) {

@@ -377,8 +377,45 @@ int build_levels(FheContext* ctx) {
                    [&](int j) { return pr[j]; });
     }
     lp.bf_ok = bf_ok;
+    // exact CRT lift constants of Q_l = q_0 ... q_{l-1} (multi-limb, little endian)
+    int qbits = 0;
+    for (int j = 0; j < l; ++j) qbits += 64 - __builtin_clzll(pr[j]);
+    const int W = (qbits + 6 + 63) / 64 + 1;  // sum_i y_i Q/q_i < l Q max q / min q, plus a sign bit
+    auto mul_word = [&](std::vector<u64>& a, u64 w) {
+      u128 carry = 0;
+      for (auto& x : a) {
+        const u128 v = (u128)x * w + carry;
+        x = (u64)v;
+        carry = v >> 64;
+      }
+    };
+    std::vector<u64> crt_Q(W, 0), crt_Qh(W, 0), crt_M((size_t)l * W, 0);
+    crt_Q[0] = 1;
+    for (int j = 0; j < l; ++j) mul_word(crt_Q, pr[j]);
+    for (int k = 0; k < W; ++k) crt_Qh[k] = (crt_Q[k] >> 1) | (k + 1 < W ? crt_Q[k + 1] << 63 : 0);
+    std::vector<WPair> crt_inv(l);
+    std::vector<double> crt_qinv(l);
+    for (int i = 0; i < l; ++i) {
+      std::vector<u64> m(W, 0);
+      m[0] = 1;
+      for (int j = 0; j < l; ++j)
+        if (j != i) mul_word(m, pr[j]);
+      std::copy(m.begin(), m.end(), crt_M.begin() + (size_t)i * W);
+      crt_inv[i] = wpair(invmod_h(punct_mod(pr, 0, l, i, pr[i]), pr[i]), pr[i]);
+      crt_qinv[i] = 1.0 / (double)pr[i];
+    }
+    int hq = W - 1;
+    while (hq > 0 && crt_Q[hq] == 0) --hq;
+    const int qdrop = std::max(0, hq - 1);
+    double qd = 0.0;
+    for (int k = hq; k >= qdrop; --k) qd = qd * 18446744073709551616.0 + (double)crt_Q[k];
+    lp.crt_W = W;
+    lp.crt_Qd = qd;
+    lp.crt_qdrop = qdrop;
     Packer pk;
     const size_t o14 = pk.addv(up_bf), o15 = pk.addv(up_bf_off), o16 = pk.addv(down_bf);
+    const size_t o17 = pk.addv(crt_M), o18 = pk.addv(crt_Q), o19 = pk.addv(crt_Qh),
+                 o20 = pk.addv(crt_inv), o21 = pk.addv(crt_qinv);
     const size_t o1 = pk.addv(up_inv), o2 = pk.addv(up_w), o3 = pk.addv(ext_prime),
                  o4 = pk.addv(info), o5 = pk.addv(down_inv), o6 = pk.addv(down_w),
                  o7 = pk.addv(p_inv), o8 = pk.addv(rs_inv), o9 = pk.addv(rs_qlast);
@@ -398,6 +435,11 @@ int build_levels(FheContext* ctx) {
     lp.p_inv = (const WPair*)(b + o7);
     lp.rs_inv = (const WPair*)(b + o8);
     lp.rs_qlast = (const u64*)(b + o9);
+    lp.crt_M = (const u64*)(b + o17);
+    lp.crt_Q = (const u64*)(b + o18);
+    lp.crt_Qh = (const u64*)(b + o19);
+    lp.crt_inv = (const WPair*)(b + o20);
+    lp.crt_qinv = (const double*)(b + o21);
     if (bf_ok) {
       lp.up_bf = (const uint2*)(b + o14);
       lp.up_bf_off = (const int*)(b + o15);

@@ -41,6 +41,17 @@ struct LevelPlan {
   // tensor-core base conversion (bconv_imma.cuh), every chain prime < 2^56:
   // packed byte-split W' fragments, ModUp per digit ([nt][up_ks][32] each,
   // offsets in up_bf_off) and ModDown ([level][down_ks][32])
+  // exact CRT lift of the level's Q (crt.cu): W limbs per big integer;
+  // crt_M[i] = Q / q_i ([level][W]), crt_Q, crt_Qh = floor(Q / 2) ([W]),
+  // crt_inv[i] = (Q / q_i)^-1 mod q_i, crt_qinv[i] = 1 / q_i (quotient estimate)
+  int crt_W = 0;
+  const u64* crt_M = nullptr;
+  const u64* crt_Q = nullptr;
+  const u64* crt_Qh = nullptr;
+  const WPair* crt_inv = nullptr;
+  const double* crt_qinv = nullptr;
+  double crt_Qd = 0.0;   // Q * 2^(-64 crt_qdrop) as a double (BFV quotient estimate)
+  int crt_qdrop = 0;
   bool bf_ok = false;
   int up_ks = 0, down_ks = 0, max_na = 0;
   const uint2* up_bf = nullptr;
@@ -80,5 +91,8 @@ int run_hmult_relin(const FheContext& ctx, int level, const u64* x, const u64* y
                     const u64* key, u64* out0, u64* out1, long out_stride, int batch, void* ws,
                     size_t ws_bytes, cudaStream_t st);
 size_t rescale_workspace(const FheContext& ctx, int polys, int level);
+// crt.cu
+int run_crt_lift(const FheContext& ctx, int mode, void* out, const u64* rows, int level,
+                 double scale, u64 t, u64 inv_f, cudaStream_t st);
 int run_rescale(FheContext& ctx, u64* out, const u64* in, int polys, int level, u64 t_plain,
                 void* ws, size_t ws_bytes, cudaStream_t st);

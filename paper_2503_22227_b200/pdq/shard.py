@@ -53,21 +53,30 @@ class ShardGroup:
             return results
         return self._exchange(results)
 
-    def map_units_batched(self, units: list, fn, batch_fn, key):
+    def map_units_batched(self, units: list, fn, batch_fn, key, lanes=None):
         """map_units, but the units a rank owns are grouped by key(unit) and
         each group goes to batch_fn(list of units) (one lockstep batch);
-        batch_fn may return None to fall back to fn per unit."""
+        batch_fn may return None to fall back to fn per unit.  With a
+        StreamPool (``lanes``, the context's worker pool) the independent
+        groups run on separate CUDA streams and join on the caller's stream."""
         mine = [i for i in range(len(units)) if self.owner(i) == self.rank]
         groups: dict = {}
         for i in mine:
             groups.setdefault(key(units[i]), []).append(i)
         results: list = [None] * len(units)
-        for idx in groups.values():
+
+        def run_group(idx):
             res = batch_fn([units[i] for i in idx]) if len(idx) > 1 else None
             if res is None:
                 res = [fn(units[i]) for i in idx]
             for i, r in zip(idx, res):
                 results[i] = r
+
+        if lanes is not None and len(groups) > 1:
+            lanes.run([lambda idx=idx: run_group(idx) for idx in groups.values()])
+        else:
+            for idx in groups.values():
+                run_group(idx)
         if self.world == 1:
             return results
         return self._exchange(results)

@@ -162,9 +162,19 @@ def _coeff_rows(ctx: Context, cd: CData, level: int) -> np.ndarray:
 
 
 def ckks_decode(ctx: Context, pt: CkksPlaintext) -> np.ndarray:
-    rows = _coeff_rows(ctx, pt.data, pt.level)
-    centered = crt_centered_floats(rows, ctx.bases[pt.level])
-    return embed_forward(centered / pt.scale, ctx.n)
+    """ckks.py:157-166: INTT, centred CRT lift to float64 and the division by
+    the scale on the device (exact Python-integer float() rounding, same IEEE
+    division: fhe_crt_lift), then the canonical-embedding FFT on the host
+    (numpy, as the reference: bit-identical slots)."""
+    from .. import _native
+    from ..coremath.crt import device_lift
+
+    t = pt.data.view()[0].clone()
+    ctx.chain.transform(t, pt.level, True, limbs=pt.level, offset=0)
+    vals = device_lift(ctx, t, pt.level, _native.CRT_FLOAT, scale=pt.scale).cpu().numpy()
+    if not np.isfinite(vals).all():
+        raise OverflowError("int too large to convert to float")
+    return embed_forward(vals, ctx.n)
 
 
 # -- encrypt / decrypt ----------------------------------------------------------------
