@@ -141,6 +141,36 @@ int fhe_context_create(const uint64_t* q_primes, int L, const uint64_t* p_primes
  *      rows: the level coefficient-domain residue rows; Python integer
  *      semantics exactly (float() rounds to nearest even; +-inf where
  *      Python raises OverflowError). */
+/* ---- device sampler: numpy Generator(Philox(SeedSequence)) replay
+ *      (sampling.py:27-63, SURVEY 8(f)1 phase 2).  The state is numpy's
+ *      Philox state (bit_generator.state: counter, key, buffer, buffer_pos,
+ *      has_uint32, uinteger) and lives in DEVICE memory, so draws chain on
+ *      the stream.  fhe_philox_integers writes Generator.integers(low,
+ *      low + rng + 1, count) (endpoint excluded; 64-bit Lemire for
+ *      rng > 2^32 - 1, else the buffered 32-bit path) as 64-bit words to out
+ *      and advances the state exactly as numpy would.  A call whose
+ *      candidate draws held too few accepted values (only possible for
+ *      ranges with heavy Lemire rejection) leaves the state untouched and
+ *      sets shortfall = 1. */
+typedef struct FhePhilox {
+  uint64_t counter[4];
+  uint64_t key[2];
+  uint64_t buffer[4];
+  int32_t buffer_pos;
+  int32_t has_uint32;
+  uint32_t uinteger;
+  int32_t shortfall;
+} FhePhilox;
+size_t fhe_philox_workspace(int64_t count, uint64_t rng);
+int fhe_philox_integers(FhePhilox* dev_state, int64_t low, uint64_t rng, int64_t count,
+                        uint64_t* out, void* workspace, size_t ws_bytes, void* stream);
+/* cbd_error's combine (sampling.py:48-52): out[i] = sum of flip rows
+ * 0..pairs-1 minus rows pairs..2 pairs-1 (flips: (2 pairs, n) words) */
+int fhe_cbd_combine(int64_t* out, const uint64_t* flips, int pairs, int64_t n, void* stream);
+/* signed_to_residues (sampling.py:60-65): out row j = coeffs mod q_(offset+j) */
+int fhe_signed_lift(const FheChain* ch, uint64_t* out, const int64_t* coeffs, int64_t n, int limbs,
+                    int offset, void* stream);
+
 enum { FHE_CRT_FLOAT = 0, FHE_CRT_MOD_T = 1, FHE_CRT_BFV = 2 };
 int fhe_crt_lift(const FheContext* ctx, int mode, void* out, const uint64_t* rows, int level,
                  double scale, uint64_t t, uint64_t inv_f, void* stream);

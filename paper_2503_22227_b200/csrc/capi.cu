@@ -209,6 +209,45 @@ int fhe_context_create(const uint64_t* q_primes, int L, const uint64_t* p_primes
   })
 }
 
+size_t fhe_philox_workspace(int64_t count, uint64_t rng) {
+  return count > 0 ? philox_workspace((long)count, rng) : 0;
+}
+
+int fhe_philox_integers(FhePhilox* dev_state, int64_t low, uint64_t rng, int64_t count,
+                        uint64_t* out, void* workspace, size_t ws_bytes, void* stream) {
+  FHE_TRY({
+    if (!dev_state || (count > 0 && (!out || !workspace))) {
+      fhe_set_error("fhe_philox_integers: null argument");
+      return -1;
+    }
+    return run_philox_integers(dev_state, (long long)low, rng, (long)count, out, workspace,
+                               ws_bytes, (cudaStream_t)stream);
+  })
+}
+
+int fhe_cbd_combine(int64_t* out, const uint64_t* flips, int pairs, int64_t n, void* stream) {
+  FHE_TRY({
+    if (!out || !flips || pairs < 1) {
+      fhe_set_error("fhe_cbd_combine: bad arguments");
+      return -1;
+    }
+    return run_cbd_combine((long long*)out, flips, pairs, (long)n, (cudaStream_t)stream);
+  })
+}
+
+int fhe_signed_lift(const FheChain* ch, uint64_t* out, const int64_t* coeffs, int64_t n, int limbs,
+                    int offset, void* stream) {
+  FHE_TRY({
+    if (!ch || !out || !coeffs || limbs < 1 || offset < 0 ||
+        offset + limbs > (int)ch->primes.size()) {
+      fhe_set_error("fhe_signed_lift: bad arguments");
+      return -1;
+    }
+    return run_signed_lift(ch->dev, out, (const long long*)coeffs, (long)n, limbs, offset,
+                           (cudaStream_t)stream);
+  })
+}
+
 int fhe_crt_lift(const FheContext* ctx, int mode, void* out, const uint64_t* rows, int level,
                  double scale, uint64_t t, uint64_t inv_f, void* stream) {
   FHE_TRY({

@@ -85,10 +85,29 @@ def ntt_rows(ctx: Context, t, limbs: int, offset: int = 0, inverse: bool = False
     return t
 
 
-def signed_eval(ctx: Context, coeffs: np.ndarray, primes) -> object:
-    """Small signed polynomial -> evaluation-domain rows over `primes`
-    (which must be a prefix of the context chain)."""
-    t = upload_rows(signed_to_residues(coeffs, primes))
+# Ring degree from which keys and noise are sampled on the device (the same
+# Philox stream as the host sampler, coremath/sampling.py *_device): below it
+# the numpy draws are cheaper than the launches.
+DEVICE_SAMPLING_MIN_N = 1 << 13
+
+
+def device_sampling(ctx: Context) -> bool:
+    return ctx.n >= DEVICE_SAMPLING_MIN_N
+
+
+def signed_eval(ctx: Context, coeffs, primes) -> object:
+    """Small signed polynomial (host numpy, or an int64 device tensor from a
+    device sampler) -> evaluation-domain rows over `primes` (a prefix of the
+    context chain)."""
+    import torch
+
+    if isinstance(coeffs, torch.Tensor):
+        t = torch.empty((len(primes), ctx.n), dtype=torch.int64, device="cuda")
+        _native.check(_native.lib().fhe_signed_lift(ctx.chain.handle, t.data_ptr(),
+                                                    coeffs.data_ptr(), ctx.n, len(primes), 0,
+                                                    _native.stream_handle()), "fhe_signed_lift")
+    else:
+        t = upload_rows(signed_to_residues(coeffs, primes))
     return ntt_rows(ctx, t, len(primes))
 
 
@@ -115,9 +134,11 @@ def _rlwe_pair(ctx: Context, sk: SecretKey, rng: Rng, extra=None, a_rows=None,
     limbs = limbs or ctx.L
     n = ctx.n
     primes = _chain_primes(ctx, limbs)
+    dev = device_sampling(ctx) and ctx.params.scheme is not Scheme.BGV
     if a_rows is None:
-        a_rows = ntt_rows(ctx, upload_rows(rng.uniform_residues(primes, n)), limbs)
-    e = rng.cbd_error(n)
+        a_rows = ntt_rows(ctx, rng.uniform_residues_device(primes, n) if dev
+                          else upload_rows(rng.uniform_residues(primes, n)), limbs)
+    e = rng.cbd_error_device(n) if dev else rng.cbd_error(n)
     if ctx.params.scheme is Scheme.BGV:
         e = e * ctx.plain_modulus.value
     e_rows = signed_eval(ctx, e, primes)
@@ -136,7 +157,9 @@ def _rlwe_pair(ctx: Context, sk: SecretKey, rng: Rng, extra=None, a_rows=None,
 def pk_gen(ctx: Context, sk: SecretKey, rng: Rng | None = None) -> PublicKey:
     rng = rng or Rng(fresh_seed())
     a_seed = rng.uniform_bytes(SEED_BYTES)
-    a_rows = ntt_rows(ctx, upload_rows(Rng(a_seed).uniform_residues(ctx.q_arr(), ctx.n)), ctx.L)
+    ar = Rng(a_seed)
+    a_rows = ntt_rows(ctx, ar.uniform_residues_device(ctx.q_arr(), ctx.n) if device_sampling(ctx)
+                      else upload_rows(ar.uniform_residues(ctx.q_arr(), ctx.n)), ctx.L)
     return PublicKey(data=_rlwe_pair(ctx, sk, rng, a_rows=a_rows, limbs=ctx.L), a_seed=a_seed)
 
 

@@ -47,13 +47,24 @@ class CapturedQuery:
         # 2. capture the device part with a private pool arena
         self.pool = MemoryPool(1, unit_mb=arena_mb, cap_mb=arena_mb)
         self.graph = torch.cuda.CUDAGraph()
-        saved = ctx.pool
-        ctx.pool = self.pool
+        # the capture runs on one stream: the worker lanes (StreamPool) are
+        # off while capturing.  The garbage collector is off too: a collected
+        # Context / DeviceChain frees its native tables (cudaFree), which is
+        # illegal while a stream captures and would invalidate the graph.
+        import gc
+
+        gc.collect()
+        gc_was_on = gc.isenabled()
+        gc.disable()
+        saved, saved_worker = ctx.pool, ctx.worker
+        ctx.pool, ctx.worker = self.pool, None
         try:
             with torch.cuda.graph(self.graph):
                 self.parts = engine.device_part(spec, self.temps)
         finally:
-            ctx.pool = saved
+            ctx.pool, ctx.worker = saved, saved_worker
+            if gc_was_on:
+                gc.enable()
         torch.cuda.synchronize()
 
     def replay(self) -> dict:

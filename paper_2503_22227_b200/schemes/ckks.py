@@ -25,7 +25,8 @@ from ..context import Context
 from ..coremath.crt import crt_centered_floats
 from ..coremath.modmath import ParameterError
 from ..coremath.sampling import Rng, fresh_seed, signed_to_residues
-from ..keys import (KSwitchKey, PublicKey, SecretKey, automorph_rows, hmult_relin_into,
+from ..keys import (KSwitchKey, PublicKey, SecretKey, automorph_rows, device_sampling,
+                    hmult_relin_into,
                     key_switch_into, signed_eval, upload_rows)
 from ..rnspoly import CData, Domain, cdata_new, ew
 
@@ -184,9 +185,14 @@ def ckks_encrypt(ctx: Context, pt: CkksPlaintext, pk: PublicKey,
     rng = rng or Rng(fresh_seed())
     level, n = pt.level, ctx.n
     primes = ctx.q_arr(level)
-    u = signed_eval(ctx, rng.ternary(n), primes)
-    e0 = signed_eval(ctx, rng.cbd_error(n), primes)
-    e1 = signed_eval(ctx, rng.cbd_error(n), primes)
+    if device_sampling(ctx):  # the same Philox stream, drawn on the device
+        u = signed_eval(ctx, rng.ternary_device(n), primes)
+        e0 = signed_eval(ctx, rng.cbd_error_device(n), primes)
+        e1 = signed_eval(ctx, rng.cbd_error_device(n), primes)
+    else:
+        u = signed_eval(ctx, rng.ternary(n), primes)
+        e0 = signed_eval(ctx, rng.cbd_error(n), primes)
+        e1 = signed_eval(ctx, rng.cbd_error(n), primes)
     out = _new_ct(ctx, 2, level)
     v = out.view()
     pkv = pk.data.view()
