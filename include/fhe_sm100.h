@@ -171,6 +171,14 @@ int fhe_cbd_combine(int64_t* out, const uint64_t* flips, int pairs, int64_t n, v
 int fhe_signed_lift(const FheChain* ch, uint64_t* out, const int64_t* coeffs, int64_t n, int limbs,
                     int offset, void* stream);
 
+/* ---- zlib CRC-32 of a device buffer (the CATF record checksum, serial.py:
+ *      67-78), written to the device word *out: chunked on the device and
+ *      merged with zlib's crc32_combine rule.  Lets a record body go from HBM
+ *      into a pinned wire buffer without a host pass over it. */
+size_t fhe_crc32_workspace(int64_t nbytes);
+int fhe_crc32(const void* data, int64_t nbytes, uint32_t* out, void* workspace, size_t ws_bytes,
+              void* stream);
+
 enum { FHE_CRT_FLOAT = 0, FHE_CRT_MOD_T = 1, FHE_CRT_BFV = 2 };
 int fhe_crt_lift(const FheContext* ctx, int mode, void* out, const uint64_t* rows, int level,
                  double scale, uint64_t t, uint64_t inv_f, void* stream);

@@ -248,6 +248,19 @@ int fhe_signed_lift(const FheChain* ch, uint64_t* out, const int64_t* coeffs, in
   })
 }
 
+size_t fhe_crc32_workspace(int64_t nbytes) { return crc32_workspace((long)nbytes); }
+
+int fhe_crc32(const void* data, int64_t nbytes, uint32_t* out, void* workspace, size_t ws_bytes,
+              void* stream) {
+  FHE_TRY({
+    if (!out || (nbytes > 0 && (!data || !workspace))) {
+      fhe_set_error("fhe_crc32: null argument");
+      return -1;
+    }
+    return run_crc32(data, (long)nbytes, out, workspace, ws_bytes, (cudaStream_t)stream);
+  })
+}
+
 int fhe_crt_lift(const FheContext* ctx, int mode, void* out, const uint64_t* rows, int level,
                  double scale, uint64_t t, uint64_t inv_f, void* stream) {
   FHE_TRY({

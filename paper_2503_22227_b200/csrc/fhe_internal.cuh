@@ -63,6 +63,10 @@ size_t philox_workspace(long count, unsigned long long rng);
 int run_philox_integers(FhePhilox* dev_state, long long low, unsigned long long rng, long count,
                         uint64_t* out, void* ws, size_t ws_bytes, cudaStream_t st);
 int run_cbd_combine(long long* out, const uint64_t* flips, int pairs, long n, cudaStream_t st);
+// crc32.cu
+size_t crc32_workspace(long nbytes);
+int run_crc32(const void* data, long nbytes, unsigned* out, void* ws, size_t ws_bytes,
+              cudaStream_t st);
 
 // thread-local error text for fhe_last_error()
 void fhe_set_error(const std::string& msg);
