@@ -167,6 +167,12 @@ int fhe_philox_integers(FhePhilox* dev_state, int64_t low, uint64_t rng, int64_t
 /* cbd_error's combine (sampling.py:48-52): out[i] = sum of flip rows
  * 0..pairs-1 minus rows pairs..2 pairs-1 (flips: (2 pairs, n) words) */
 int fhe_cbd_combine(int64_t* out, const uint64_t* flips, int pairs, int64_t n, void* stream);
+/* CKKS encode's residue lift (ckks.py:104-136): values are the rounded
+ * scaled coefficients (integer-valued doubles of any magnitude); out row j =
+ * the exact integer mod q_(offset+j) (what the reference computes with
+ * Python integers beyond 2^62) */
+int fhe_real_lift(const FheChain* ch, uint64_t* out, const double* values, int64_t n, int limbs,
+                  int offset, void* stream);
 /* signed_to_residues (sampling.py:60-65): out row j = coeffs mod q_(offset+j) */
 int fhe_signed_lift(const FheChain* ch, uint64_t* out, const int64_t* coeffs, int64_t n, int limbs,
                     int offset, void* stream);

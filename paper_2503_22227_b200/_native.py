@@ -51,6 +51,7 @@ SIGNATURES = {
     "fhe_philox_integers": (_int, [_vp, ctypes.c_int64, ctypes.c_uint64, ctypes.c_int64, _vp, _vp,
                                    _sz, _vp]),
     "fhe_cbd_combine": (_int, [_vp, _vp, _int, ctypes.c_int64, _vp]),
+    "fhe_real_lift": (_int, [_vp, _vp, _vp, ctypes.c_int64, _int, _int, _vp]),
     "fhe_signed_lift": (_int, [_vp, _vp, _vp, ctypes.c_int64, _int, _int, _vp]),
     "fhe_crc32_workspace": (ctypes.c_size_t, [ctypes.c_int64]),
     "fhe_crc32": (_int, [_vp, ctypes.c_int64, _vp, _vp, _sz, _vp]),

@@ -261,6 +261,18 @@ int fhe_crc32(const void* data, int64_t nbytes, uint32_t* out, void* workspace, 
   })
 }
 
+int fhe_real_lift(const FheChain* ch, uint64_t* out, const double* values, int64_t n, int limbs,
+                  int offset, void* stream) {
+  FHE_TRY({
+    if (!ch || !out || !values || limbs < 1 || offset < 0 ||
+        offset + limbs > (int)ch->primes.size()) {
+      fhe_set_error("fhe_real_lift: bad arguments");
+      return -1;
+    }
+    return run_real_lift(ch->dev, out, values, (long)n, limbs, offset, (cudaStream_t)stream);
+  })
+}
+
 int fhe_crt_lift(const FheContext* ctx, int mode, void* out, const uint64_t* rows, int level,
                  double scale, uint64_t t, uint64_t inv_f, void* stream) {
   FHE_TRY({

@@ -51,6 +51,9 @@ inline int launch_ntt(const DevChain& ch, u64* data, const u64* in, int rows, Ro
 // philox.cu: small signed coefficients -> residue rows (canonical)
 int run_signed_lift(const DevChain& ch, u64* out, const long long* c, long n, int limbs,
                     int offset, cudaStream_t st);
+// integer-valued doubles (any magnitude) -> residue rows (CKKS encode)
+int run_real_lift(const DevChain& ch, u64* out, const double* v, long n, int limbs, int offset,
+                  cudaStream_t st);
 
 // poly.cu
 int launch_ewise(const DevChain& ch, int op, u64* out, const u64* a, const u64* b, const u64* c,

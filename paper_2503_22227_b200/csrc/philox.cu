@@ -234,7 +234,54 @@ __global__ void signed_lift_kernel(const DevChain ch, u64* __restrict__ out,
   }
 }
 
+// Integer-valued doubles (CKKS encode: the rounded scaled coefficients,
+// any magnitude up to the modulus budget) -> residue rows: v = m 2^e exactly
+// (m the 53-bit significand), so [v]_q = [m]_q [2^e]_q, negated for v < 0 --
+// the residues the reference computes with Python integers
+// (ckks.py:104-136) without leaving the device.
+__global__ void real_lift_kernel(const DevChain ch, u64* __restrict__ out,
+                                 const double* __restrict__ v, long n, int limbs, int offset) {
+  const long total = n * limbs;
+  for (long t = blockIdx.x * (long)blockDim.x + threadIdx.x; t < total;
+       t += (long)gridDim.x * blockDim.x) {
+    const int j = (int)(t / n);
+    const long i = t - (long)j * n;
+    const ModConst mc = ch.mc[offset + j];
+    const u64 q = mc.q;
+    const double x = v[i];
+    const u64 bits = (u64)__double_as_longlong(x);
+    const bool neg = bits >> 63;
+    const int be = (int)((bits >> 52) & 0x7ff);
+    u64 r;
+    if (be == 0) {
+      r = 0;  // +-0 (subnormals cannot be integer-valued)
+    } else {
+      const u64 m = (bits & 0xfffffffffffffull) | (1ull << 52);
+      const int e = be - 1075;  // x = m 2^e
+      if (e <= 0) {
+        r = (m >> (-e)) % q;  // an integer below 2^53
+      } else {
+        u64 p = 1 % q, b = 2 % q;
+        for (int k = e; k; k >>= 1) {  // 2^e mod q
+          if (k & 1) p = mul_mod(p, b, mc);
+          b = mul_mod(b, b, mc);
+        }
+        r = mul_mod(m % q, p, mc);
+      }
+    }
+    out[t] = (neg && r) ? q - r : r;
+  }
+}
+
 }  // namespace
+
+int run_real_lift(const DevChain& ch, u64* out, const double* v, long n, int limbs, int offset,
+                  cudaStream_t st) {
+  if (n <= 0 || limbs <= 0) return 0;
+  real_lift_kernel<<<grid_for(n * limbs), kPxThreads, 0, st>>>(ch, out, v, n, limbs, offset);
+  FHE_LAUNCH_CHECK();
+  return 0;
+}
 
 int run_cbd_combine(long long* out, const u64* flips, int pairs, long n, cudaStream_t st) {
   if (n <= 0) return 0;

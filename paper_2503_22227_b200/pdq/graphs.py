@@ -33,7 +33,7 @@ from .engine import PdqEngine, QueryResult, QuerySpec
 
 class CapturedQuery:
     def __init__(self, engine: PdqEngine, spec: QuerySpec, temps: dict | None = None,
-                 arena_mb: int = 512):
+                 arena_mb: int = 512, lanes: bool = True):
         import torch
 
         if engine.group is not None and engine.group.world > 1:
@@ -47,22 +47,24 @@ class CapturedQuery:
         # 2. capture the device part with a private pool arena
         self.pool = MemoryPool(1, unit_mb=arena_mb, cap_mb=arena_mb)
         self.graph = torch.cuda.CUDAGraph()
-        # the capture runs on one stream: the worker lanes (StreamPool) are
-        # off while capturing.  The garbage collector is off too: a collected
-        # Context / DeviceChain frees its native tables (cudaFree), which is
-        # illegal while a stream captures and would invalidate the graph.
+        # lanes: the independent unit groups are captured on the context's
+        # StreamPool streams (fork / join inside the capture), so the graph
+        # runs them as concurrent branches.  The garbage collector is off
+        # while capturing: a collected Context / DeviceChain frees its native
+        # tables (cudaFree), which is illegal while a stream captures.
         import gc
 
         gc.collect()
         gc_was_on = gc.isenabled()
         gc.disable()
-        saved, saved_worker = ctx.pool, ctx.worker
-        ctx.pool, ctx.worker = self.pool, None
+        saved, saved_lanes = ctx.pool, engine.use_lanes
+        ctx.pool = self.pool
+        engine.use_lanes = lanes and ctx.worker is not None
         try:
             with torch.cuda.graph(self.graph):
                 self.parts = engine.device_part(spec, self.temps)
         finally:
-            ctx.pool, ctx.worker = saved, saved_worker
+            ctx.pool, engine.use_lanes = saved, saved_lanes
             if gc_was_on:
                 gc.enable()
         torch.cuda.synchronize()

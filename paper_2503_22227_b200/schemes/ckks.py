@@ -145,13 +145,19 @@ def ckks_encode(ctx: Context, values, scale: float | None = None,
         raise EncodeRangeError(f"scaled magnitude 2^{np.log2(max(peak, 1)):.1f} exceeds the "
                                f"2^{budget.bit_length() - 1} modulus budget at level {level}")
     rounded = _round_half_away(coeffs)
-    if peak < 2.0 ** 62:
-        rows = signed_to_residues(rounded.astype(np.int64), ctx.q_arr(level))
-    else:
-        big = [int(x) for x in rounded]
-        rows = np.stack([np.array([x % int(q) for x in big], dtype=np.uint64)
-                         for q in ctx.q_arr(level)])
-    return CkksPlaintext(_poly_from_rows(ctx, rows, level), float(scale), level)
+    # the exact residues of the rounded coefficients (Python-integer results of
+    # the reference at any magnitude) are lifted on the device from the
+    # doubles themselves (fhe_real_lift): N words go up instead of L x N
+    import torch
+
+    vals = torch.from_numpy(np.ascontiguousarray(rounded, dtype=np.float64)).cuda()
+    cd = cdata_new(ctx.pool, 1, level, n, zero=False)
+    _native.check(_native.lib().fhe_real_lift(ctx.chain.handle, cd.view().data_ptr(),
+                                              vals.data_ptr(), n, level, 0,
+                                              _native.stream_handle()), "fhe_real_lift")
+    ctx.chain.transform(cd.view()[0], level, False, limbs=level, offset=0)
+    cd.domains = [Domain.EVALUATION]
+    return CkksPlaintext(cd, float(scale), level)
 
 
 def _coeff_rows(ctx: Context, cd: CData, level: int) -> np.ndarray:
