@@ -33,6 +33,18 @@ struct NttArgs {
   long dst_bstride;
   const NttFinish* fin = nullptr;  // forward only; *fin_done tells if it was applied
   bool* fin_done = nullptr;
+  // Broadcast input (forward, N = 2^16 TMA column path only): input row r is
+  // bcast_src + (r / map.limbs) * bcast_stride -- one row per batch item,
+  // shared by its map.limbs target rows -- read as the centred integer
+  // (v > center_q / 2 ? v - center_q : v).  Rescale's correction (ckks.py:
+  // 382-410) is the centred last limb mod every q_j; the transform takes the
+  // centred value itself as the representative, so no expanded rows are
+  // materialised.  A launch that cannot take this path returns *bcast_done
+  // = false and leaves dst untouched.
+  const u64* bcast_src = nullptr;
+  long bcast_stride = 0;
+  u64 center_q = 0;
+  bool* bcast_done = nullptr;
 };
 int launch_ntt(const DevChain& ch, const NttArgs& a, bool inverse, cudaStream_t st);
 unsigned long long ntt_path_count(int path);

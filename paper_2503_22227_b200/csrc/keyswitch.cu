@@ -997,6 +997,19 @@ int run_hmult_relin(const FheContext& ctx, int level, const u64* x, const u64* y
                        out1, out_stride, batch, ws, ks_bytes, st, false);
 }
 
+static u64 ch_prime(const FheContext& ctx, int i) { return ctx.chain->primes[i]; }
+
+// broadcast correction input in rescale (FHE_RESCALE_BCAST=0 keeps the
+// materialised expand + NTT)
+static bool bcast_rescale_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("FHE_RESCALE_BCAST");
+    on = (e && e[0] == '0') ? 0 : 1;
+  }
+  return on == 1;
+}
+
 size_t rescale_workspace(const FheContext& ctx, int polys, int level) {
   const size_t n = (size_t)1 << ctx.chain->log_n;
   return (size_t)polys * level * n * sizeof(u64);
@@ -1033,10 +1046,26 @@ int run_rescale(FheContext& ctx, u64* out, const u64* in, int polys, int level, 
                                   RowMap{nullptr, 1, level - 1}, (long)level * n, 0},
                       true, st);
   if (rc) return rc;
-  rc = launch_modswitch_expand(ch, corr, last, polys, level - 1, level - 1, t_plain, tinv, t_mod,
-                               lp.rs_qlast, st);
-  if (rc) return rc;
-  rc = launch_ntt(ch, corr, corr, polys * (level - 1), RowMap{nullptr, level - 1, 0}, false, st);
-  if (rc) return rc;
+  // CKKS: the correction rows are the centred last limb mod every q_j, which
+  // the forward NTT reads straight from `last` (broadcast, centred input):
+  // the expanded rows are never written.  Otherwise (BGV, or a shape the
+  // broadcast path does not take) the expand kernel materialises them.
+  bool bcast = false;
+  if (t_plain == 0 && bcast_rescale_enabled()) {
+    NttArgs na{corr, corr, polys * (level - 1), RowMap{nullptr, level - 1, 0}, 0, 0};
+    na.bcast_src = last;
+    na.bcast_stride = n;
+    na.center_q = ch_prime(ctx, level - 1);
+    na.bcast_done = &bcast;
+    rc = launch_ntt(ch, na, false, st);
+    if (rc) return rc;
+  }
+  if (!bcast) {
+    rc = launch_modswitch_expand(ch, corr, last, polys, level - 1, level - 1, t_plain, tinv,
+                                 t_mod, lp.rs_qlast, st);
+    if (rc) return rc;
+    rc = launch_ntt(ch, corr, corr, polys * (level - 1), RowMap{nullptr, level - 1, 0}, false, st);
+    if (rc) return rc;
+  }
   return launch_modswitch_finish(ch, out, in, corr, polys, level, lp.rs_inv, st);
 }

@@ -192,6 +192,7 @@ struct ColsTmaTile : ColsTile<LOG_N, LOG_N1> {
   const CUtensorMap* smap_p = nullptr;  // the kernel's __grid_constant__ maps
   const CUtensorMap* dmap_p = nullptr;
   int ccol = 0, climb = 0, cbat = 0;  // box coordinates of the tile
+  bool bcast = false;  // source map holds one row per batch item (NttArgs::bcast_src)
   __device__ __forceinline__ void setup(int t) {
     Base::setup(t);
     ccol = this->j0 >> 4;
@@ -200,8 +201,9 @@ struct ColsTmaTile : ColsTile<LOG_N, LOG_N1> {
   }
   uint64_t ld_pol = 0, st_pol = 0;  // L2 cache-hint policies (0: no hint)
   __device__ __forceinline__ void tma_load(u64* sm, uint64_t* bar) const {
-    if (ld_pol) tma_load_5d_hint(sm, smap_p, 0, ccol, 0, climb, cbat, bar, ld_pol);
-    else tma_load_5d(sm, smap_p, 0, ccol, 0, climb, cbat, bar);
+    const int sl = bcast ? 0 : climb;
+    if (ld_pol) tma_load_5d_hint(sm, smap_p, 0, ccol, 0, sl, cbat, bar, ld_pol);
+    else tma_load_5d(sm, smap_p, 0, ccol, 0, sl, cbat, bar);
   }
   __device__ __forceinline__ void tma_store(const u64* sm) const {
     if (st_pol) tma_store_5d_hint(dmap_p, 0, ccol, 0, climb, cbat, sm, st_pol);
@@ -857,16 +859,20 @@ int launch_chunks_tma(const DevChain& ch, u64* dst, const u64* src, const Tile& 
 template <class CT, class KT>
 int launch_fused_tma(const DevChain& ch, u64* dst, const u64* src, const CT& ct, const KT& kt,
                      bool fwd, long src_bstride, long dst_bstride, int rows, int limbs,
-                     cudaStream_t st, bool& done) {
+                     cudaStream_t st, bool& done, bool bcast = false) {
   done = false;
   const int log_c = kChunkLogTile - KT::LOG_S - kt.log_r;
   // forward: columns read src, chunks work in place on dst; inverse: chunks
-  // read src, columns work in place on dst
+  // read src, columns work in place on dst.  bcast (forward): src holds one
+  // row per batch item (src_bstride apart), read by every limb of the item
   CUtensorMap cs, cd, ks, kd;
   const u64* col_src = fwd ? src : dst;
   const u64* chk_src = fwd ? dst : src;
   const long col_sb = fwd ? src_bstride : dst_bstride, chk_sb = fwd ? dst_bstride : src_bstride;
-  if (!cols_tensor_map(&cs, col_src, ch.log_n, CT::LOG_S, limbs, col_sb, rows) ||
+  const bool col_ok = bcast ? cols_tensor_map(&cs, col_src, ch.log_n, CT::LOG_S, 1, col_sb,
+                                              (rows + limbs - 1) / limbs)
+                            : cols_tensor_map(&cs, col_src, ch.log_n, CT::LOG_S, limbs, col_sb, rows);
+  if (!col_ok ||
       !cols_tensor_map(&cd, dst, ch.log_n, CT::LOG_S, limbs, dst_bstride, rows) ||
       !chunks_tensor_map(&ks, chk_src, ch.log_n, KT::LOG_S, limbs, chk_sb, rows, kt.log_r, log_c) ||
       !chunks_tensor_map(&kd, dst, ch.log_n, KT::LOG_S, limbs, dst_bstride, rows, kt.log_r, log_c))
@@ -923,7 +929,12 @@ int launch_cols_tma(const DevChain& ch, u64* dst, const u64* src, const Tile& tl
                     long src_bstride, long dst_bstride, cudaStream_t st, bool& done) {
   done = false;
   CUtensorMap smap, dmap;
-  if (!cols_tensor_map(&smap, src, ch.log_n, Tile::LOG_S, tl.map.limbs, src_bstride, tl.rows) ||
+  const bool src_ok =
+      tl.bcast ? cols_tensor_map(&smap, src, ch.log_n, Tile::LOG_S, 1, src_bstride,
+                                 (tl.rows + tl.map.limbs - 1) / tl.map.limbs)
+               : cols_tensor_map(&smap, src, ch.log_n, Tile::LOG_S, tl.map.limbs, src_bstride,
+                                 tl.rows);
+  if (!src_ok ||
       !cols_tensor_map(&dmap, dst, ch.log_n, Tile::LOG_S, tl.map.limbs, dst_bstride, tl.rows))
     return 0;  // fall back to the cp.async path
   constexpr int smem =
@@ -988,6 +999,60 @@ int launch_split(const DevChain& ch, const NttArgs& a, bool inverse, bool lazy,
   // rows (rows % limbs == 0: no box row can fall past the buffer's end)
   const bool use_ktma = (LOG_N - LOG_N1 == 8) && ch.fp64_ok && kstage && tma_enabled() &&
                         a.rows % a.map.limbs == 0 && std::getenv("FHE_NTT_KTMA") == nullptr;
+  if (a.bcast_src) {
+    // centred broadcast input (rescale): TMA column tiles only
+    if (a.bcast_done) *a.bcast_done = false;
+    if constexpr (kTmaShape) {
+      if (inverse || !use_tma || a.fin) return 0;
+      const double center = (double)a.center_q;
+      bool done = false;
+      if constexpr (LOG_N - LOG_N1 == 8) {
+        if (use_ktma && ch.fuse && fused_tma_enabled() && kt.log_r >= FHE_FUSE_MIN_LOG_R) {
+          ColsTmaTile<LOG_N, LOG_N1> tc;
+          static_cast<C&>(tc) = ct;
+          tc.bcast = true;
+          tc.center = center;
+          tc.src = d;
+          tc.dst = d;
+          ChunksTmaTile<LOG_N, LOG_N1> tk;
+          static_cast<K&>(tk) = kt;
+          if (tk.log_r > FHE_FUSE_MAX_LOG_R) tk.plan(a.rows, a.map.limbs, FHE_FUSE_MAX_LOG_R);
+          tk.src = d;
+          tk.dst = d;
+          rc = launch_fused_tma(ch, a.dst, a.bcast_src, tc, tk, true, a.bcast_stride,
+                                a.dst_bstride, a.rows, a.map.limbs, st, done, true);
+          if (done) path_hit(FHE_NTT_PATH_FUSED_TMA);
+          if (rc || done) {
+            if (done && a.bcast_done) *a.bcast_done = true;
+            return rc;
+          }
+        }
+      }
+      // two passes: the column pass reads the broadcast rows, the chunk pass
+      // runs in place on dst
+      CT tt;
+      static_cast<C&>(tt) = ct;
+      tt.bcast = true;
+      tt.center = center;
+      rc = launch_cols_tma<CT, true, FPIN_U64, FPOUT_DOUBLE>(ch, a.dst, a.bcast_src, tt, nc,
+                                                            a.bcast_stride, a.dst_bstride, st,
+                                                            done);
+      if (rc || !done) return rc;
+      path_hit(FHE_NTT_PATH_SPLIT);
+      kt.src = d;
+      kt.dst = d;
+      bool kdone = false;
+      if (use_ktma)
+        rc = maybe_chunks_tma<LOG_N, LOG_N1, true, FPIN_DOUBLE, FPOUT_U64>(
+            ch, a.dst, a.dst, kt, nk, a.dst_bstride, a.dst_bstride, st, kdone);
+      if (!rc && !kdone)
+        rc = kstage ? launch_tiles_fp<K, true, FPIN_DOUBLE, FPOUT_U64, true>(ch, a.dst, a.dst, kt, nk, st)
+                    : launch_tiles_fp<K, true, FPIN_DOUBLE, FPOUT_U64>(ch, a.dst, a.dst, kt, nk, st);
+      if (!rc && a.bcast_done) *a.bcast_done = true;
+      return rc;
+    }
+    return 0;
+  }
   if constexpr (LOG_N1 == 8 && LOG_N - LOG_N1 == 8) {
     // one pass, the row held by a 16-CTA cluster (DSMEM transpose)
     if (ch.fp64_ok && !a.fin && tma_enabled()) {

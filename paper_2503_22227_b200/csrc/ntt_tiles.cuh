@@ -150,6 +150,7 @@ struct RowsTile {
   static constexpr bool TMA = false;
   static constexpr bool SWZ = false;   // 128B-swizzled rows (TMA chunk tiles)
   static constexpr int THREADS = kRowThreads;
+  static constexpr double center = 0.0;  // (column tiles only: centred broadcast input)
   static constexpr int MINB = 2;
   static constexpr int NBUF = 2;
   static constexpr int SMEM_WORDS = padded_words(NB * S);
@@ -211,6 +212,7 @@ struct ColsTile {
   static constexpr int TILES = N2 / CN;
   static constexpr int THREADS = kColsThreads;
   static constexpr int MINB = kColsMinB;
+  double center = 0.0;  // != 0: input values are centred about this modulus (NttArgs::center_q)
   static constexpr int NBUF = kSplitNBuf;
   static constexpr int TILE = 1 << kColsLogTile;
   // >= 16 columns: lanes run across the columns of a k-row (conflict-free
@@ -298,6 +300,7 @@ struct ChunksTile {
   static constexpr int TILE = 1 << kChunkLogTile;
   static constexpr int NB = TILE / S;
   static constexpr int THREADS = kSplitThreads;
+  static constexpr double center = 0.0;
   static constexpr int MINB = kChunkMinB;
   static constexpr int NBUF = kChunkNBuf;
   static constexpr int SMEM_WORDS = padded_words(TILE);
@@ -726,6 +729,14 @@ __device__ __forceinline__ void run_pass_fp(u64* sm, const double2* tws, const T
 #pragma unroll
     for (int i = 0; i < E; ++i)
       x[i] = (FIRST && IN == FPIN_U64) ? fp_from_u52(raw[i]) : __longlong_as_double((long long)raw[i]);
+    if constexpr (FIRST && IN == FPIN_U64 && Tile::COLS) {
+      // centred broadcast input (rescale): the signed representative itself
+      if (tl.center != 0.0) {
+        const double hq = 0.5 * tl.center;
+#pragma unroll
+        for (int i = 0; i < E; ++i) x[i] = x[i] > hq ? __dadd_rn(x[i], -tl.center) : x[i];
+      }
+    }
 #ifdef FHE_NTT_NOCOMPUTE
     if (false) {
 #else
