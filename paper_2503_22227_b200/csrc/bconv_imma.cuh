@@ -67,6 +67,7 @@ struct BconvArgs {
   int ns, nt;               // ModDown: K, level (ModUp: from dig_info, nt = level + K - na)
   int src_prime0;           // ModDown: L (first P prime); ModUp: 0 (+ s0)
   int level, K;
+  bool layout2 = false;     // bfrag packed for bconv_imma2_kernel (pack_bfrag2)
 };
 
 // Per-target reduction constants of the epilogue: V < 2^71 is reduced by one
@@ -242,6 +243,147 @@ __global__ void __launch_bounds__(kBcThreads, FHE_BCONV_MINB)
   }
 }
 
+// Register-resident epilogue (default): the n8 tiles are (8 targets, one byte
+// position b), so after the 7 byte tiles of a target group every lane holds
+// all 7 partials of its 2 targets x 4 rows in registers -- no shared-memory
+// transpose and no warp syncs per target (C fragment: lane (gr, gq) holds
+// columns 2 gq, 2 gq + 1 of rows gr, gr + 8).  B is packed per (group,
+// byte, k-step) on the host (pack_bfrag2, context.cu).
+template <int KS, bool FPPRO>
+__global__ void __launch_bounds__(kBcThreads, FHE_BCONV_MINB)
+    bconv_imma2_kernel(const DevChain ch, const BconvArgs a) {
+  constexpr int SMAX = (32 * KS) / 7;
+  constexpr int AST = bc_astride(KS);
+  extern __shared__ __align__(16) unsigned char bc_smem[];
+  int ns = a.ns, nt = a.nt, s0 = 0, row_off = 0, bfo = 0;
+  if (a.dig_info) {
+    const int di = blockIdx.y;
+    s0 = a.dig_info[4 * di];
+    ns = a.dig_info[4 * di + 1];
+    row_off = a.dig_info[4 * di + 2];
+    nt = a.level + a.K - ns;
+    bfo = a.bf_off[di];
+  }
+  const int ng = (nt + 7) >> 3;  // target groups of 8
+  uint2* sb = reinterpret_cast<uint2*>(bc_smem);                      // [ng][7][KS][32]
+  BcTarget* tgs = reinterpret_cast<BcTarget*>(sb + ng * 7 * KS * 32);  // [8 ng]
+  double2* sinv = reinterpret_cast<double2*>(tgs + 8 * ng);
+  double2* sqd = sinv + SMAX;
+  WPair* sinvi = reinterpret_cast<WPair*>(sqd + SMAX);
+  u64* sqi = reinterpret_cast<u64*>(sinvi + SMAX);
+  unsigned* atile = reinterpret_cast<unsigned*>(sqi + ((SMAX + 1) & ~1)) +
+                    (threadIdx.x >> 5) * (32 * AST);
+  for (int i = threadIdx.x; i < ng * 7 * KS * 32; i += blockDim.x) sb[i] = a.bfrag[bfo + i];
+  for (int t = threadIdx.x; t < 8 * ng; t += blockDim.x) {
+    if (t < nt) {
+      const ModConst m = ch.mc[a.tgt_prime ? a.tgt_prime[row_off + t] : t];
+      tgs[t] = BcTarget{m.q, m.mu >> (m.s - 7), m.s, {0, 0, 0}};
+    } else {
+      tgs[t] = BcTarget{1, 0, 39, {0, 0, 0}};  // padding target (never stored)
+    }
+  }
+  for (int s = threadIdx.x; s < SMAX; s += blockDim.x) {
+    if (s < ns) {
+      const int cp = a.src_prime0 + s0 + s;
+      if (FPPRO) {
+        sinv[s] = a.inv_d[s0 + s];
+        sqd[s] = ch.qd[cp];
+      } else {
+        sinvi[s] = a.inv[s0 + s];
+        sqi[s] = ch.mc[cp].q;
+      }
+    }
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int gr = lane >> 2, gq = lane & 3;
+  const long n = 1L << ch.log_n;
+  const u64* src = a.src + blockIdx.z * a.src_bstride + (long)s0 * n;
+  u64* dst = a.dst + blockIdx.z * a.dst_bstride + (long)row_off * n;
+  const int warps_total = gridDim.x * kBcWarps;
+  for (long c0 = ((long)blockIdx.x * kBcWarps + (threadIdx.x >> 5)) * 32; c0 < n;
+       c0 += (long)warps_total * 32) {
+    const long c = c0 + lane;
+    u64 xs[SMAX];
+#pragma unroll
+    for (int s = 0; s < SMAX; ++s) xs[s] = s < ns ? src[(long)s * n + c] : 0;
+    unsigned w[8 * KS];
+#pragma unroll
+    for (int i = 0; i < 8 * KS; ++i) w[i] = 0;
+#pragma unroll
+    for (int s = 0; s < SMAX; ++s) {
+      if (s < ns) {
+        u64 y;
+        if (FPPRO) {
+          const double2 qd = sqd[s];
+          y = fp_to_u52(fp_pos(fp_mulmod(fp_from_u52(xs[s]), sinv[s], qd.x), qd.x));
+        } else {
+          const WPair iv = sinvi[s];
+          y = shoup_mul(xs[s], iv.w, iv.sh, sqi[s]);
+        }
+        const int bit = 56 * s, wi = bit >> 5, sh = bit & 31;
+        const u64 lo64 = y << sh;
+        w[wi] |= (unsigned)lo64;
+        w[wi + 1] |= (unsigned)(lo64 >> 32);
+        if (sh > 8) w[wi + 2] |= (unsigned)(y >> (64 - sh));
+      }
+    }
+    __syncwarp();  // the previous iteration's fragment loads are done
+#pragma unroll
+    for (int i = 0; i < 8 * KS; i += 4)
+      *reinterpret_cast<uint4*>(&atile[lane * AST + i]) = make_uint4(w[i], w[i + 1], w[i + 2], w[i + 3]);
+    __syncwarp();
+    unsigned af[2][KS][4];
+#pragma unroll
+    for (int m = 0; m < 2; ++m)
+#pragma unroll
+      for (int ks = 0; ks < KS; ++ks) {
+        const unsigned* r0 = &atile[(16 * m + gr) * AST + 8 * ks + gq];
+        const unsigned* r1 = r0 + 8 * AST;
+        af[m][ks][0] = r0[0];
+        af[m][ks][1] = r1[0];
+        af[m][ks][2] = r0[4];
+        af[m][ks][3] = r1[4];
+      }
+    for (int g = 0; g < ng; ++g) {
+      int acc[7][2][4];
+#pragma unroll
+      for (int b = 0; b < 7; ++b)
+#pragma unroll
+        for (int m = 0; m < 2; ++m)
+#pragma unroll
+          for (int i = 0; i < 4; ++i) acc[b][m][i] = 0;
+#pragma unroll
+      for (int b = 0; b < 7; ++b)
+#pragma unroll
+        for (int ks = 0; ks < KS; ++ks) {
+          const uint2 bf = sb[((g * 7 + b) * KS + ks) * 32 + lane];
+          imma_u8(acc[b][0], af[0][ks], bf);
+          imma_u8(acc[b][1], af[1][ks], bf);
+        }
+      // lane: targets 8 g + 2 gq + e, rows 16 m + gr + 8 h  (c index 2 h + e)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int t = 8 * g + 2 * gq + e;
+        const BcTarget tg = tgs[t];
+#pragma unroll
+        for (int m = 0; m < 2; ++m)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int ci = 2 * h + e;
+            u64 lo = (u64)(unsigned)acc[0][m][ci] + ((u64)(unsigned)acc[1][m][ci] << 8) +
+                     ((u64)(unsigned)acc[2][m][ci] << 16) + ((u64)(unsigned)acc[3][m][ci] << 24) +
+                     ((u64)(unsigned)acc[4][m][ci] << 32) + ((u64)(unsigned)acc[5][m][ci] << 40);
+            u64 hi = 0;
+            const u64 p6 = (u64)(unsigned)acc[6][m][ci];
+            add_wide(hi, lo, p6 >> 16, p6 << 48);
+            if (t < nt) dst[(long)t * n + c0 + 16 * m + 8 * h + gr] = bc_reduce71(hi, lo, tg);
+          }
+      }
+    }
+  }
+}
+
 // Shared memory of one CTA: the B fragments, the target and source
 // constants, and per warp an A tile and TB C tiles.
 inline size_t bconv_smem(int nt, int ks, int tb) {
@@ -253,12 +395,32 @@ inline size_t bconv_smem(int nt, int ks, int tb) {
 
 inline int bconv_ks(int ns) { return (7 * ns + 31) / 32; }
 
+inline size_t bconv2_smem(int nt, int ks) {
+  const int smax = (32 * ks) / 7, ng = (nt + 7) / 8;
+  return (size_t)ng * 7 * ks * 32 * sizeof(uint2) + (size_t)8 * ng * sizeof(BcTarget) +
+         (size_t)smax * (2 * sizeof(double2) + sizeof(WPair)) + (size_t)((smax + 1) & ~1) * 8 +
+         (size_t)kBcWarps * 32 * bc_astride(ks) * sizeof(unsigned);
+}
+
 #ifndef FHE_BCONV_TB
 #define FHE_BCONV_TB 2
 #endif
 
 template <int KS>
 int launch_bconv_ks(const DevChain& ch, const BconvArgs& a, int max_nt, dim3 grid, cudaStream_t st) {
+  if (a.layout2) {
+    const size_t smem2 = bconv2_smem(max_nt, KS);
+    auto go2 = [&](auto kern) -> int {
+      if (smem2 > 48 * 1024)
+        FHE_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)smem2));
+      kern<<<grid, kBcThreads, smem2, st>>>(ch, a);
+      FHE_LAUNCH_CHECK();
+      return 0;
+    };
+    return (ch.fp64_ok && a.inv_d) ? go2(bconv_imma2_kernel<KS, true>)
+                                   : go2(bconv_imma2_kernel<KS, false>);
+  }
   constexpr int TB = FHE_BCONV_TB;
   const size_t smem = bconv_smem(max_nt, KS, TB);
   auto go = [&](auto kern) -> int {

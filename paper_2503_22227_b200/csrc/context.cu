@@ -264,6 +264,41 @@ static void pack_bfrag(std::vector<uint2>& out, int ns, int nt, int ks, W w, P p
       }
 }
 
+// The same matrix packed for bconv_imma2_kernel: n8 tile (group g, byte b)
+// holds columns (target 8 g + n, byte b), n = lane / 4; tiles ordered
+// [g][b][ks][lane].
+template <class W, class P>
+static void pack_bfrag2(std::vector<uint2>& out, int ns, int nt, int ks, W w, P p) {
+  std::vector<u64> v((size_t)ns * 7 * nt);
+  for (int s = 0; s < ns; ++s)
+    for (int t = 0; t < nt; ++t) {
+      const u64 pt = p(t);
+      u64 x = w(s, t) % pt;
+      for (int a = 0; a < 7; ++a) {
+        v[((size_t)s * 7 + a) * nt + t] = x;
+        x = mulmod_h(x, 256 % pt, pt);
+      }
+    }
+  auto byte = [&](int k, int t, int b) -> unsigned {
+    if (k >= 7 * ns || t >= nt) return 0;
+    return (unsigned)((v[(size_t)k * nt + t] >> (8 * b)) & 0xff);
+  };
+  const int ng = (nt + 7) / 8;
+  for (int g = 0; g < ng; ++g)
+    for (int b = 0; b < 7; ++b)
+      for (int kk = 0; kk < ks; ++kk)
+        for (int lane = 0; lane < 32; ++lane) {
+          const int gq = lane & 3, t = 8 * g + (lane >> 2);
+          unsigned b0 = 0, b1 = 0;
+          for (int i = 0; i < 4; ++i) {
+            const int k0 = 32 * kk + 4 * gq + i;
+            b0 |= byte(k0, t, b) << (8 * i);
+            b1 |= byte(k0 + 16, t, b) << (8 * i);
+          }
+          out.push_back(make_uint2(b0, b1));
+        }
+}
+
 // Product of primes[idx] for idx in [lo, hi) except `skip`, reduced mod m.
 static u64 punct_mod(const std::vector<u64>& primes, int lo, int hi, int skip, u64 m) {
   u64 r = 1 % m;
@@ -355,8 +390,8 @@ int build_levels(FheContext* ctx) {
     // tensor-core base conversion tables (every chain prime < 2^56)
     bool bf_ok = K <= 16;
     for (u64 q : pr) bf_ok &= q < ((u64)1 << 56) && q >= ((u64)1 << 39);  // bc_reduce71 domain
-    std::vector<uint2> up_bf, down_bf;
-    std::vector<int> up_bf_off;
+    std::vector<uint2> up_bf, down_bf, up_bf2, down_bf2;
+    std::vector<int> up_bf_off, up_bf2_off;
     if (bf_ok) {
       int max_na = 0;
       for (int di = 0; di < D; ++di) max_na = std::max(max_na, lp.dig_na[di]);
@@ -367,14 +402,18 @@ int build_levels(FheContext* ctx) {
       for (int di = 0; bf_ok && di < D; ++di) {
         const int s0 = lp.dig_s0[di], na = lp.dig_na[di], nt = l + K - na;
         up_bf_off.push_back((int)up_bf.size());
-        pack_bfrag(up_bf, na, nt, lp.up_ks,
-                   [&](int s, int t) { return up_w[lp.dig_w_off[di] + s * nt + t]; },
-                   [&](int t) { return pr[cp(t < s0 ? t : t + na)]; });
+        up_bf2_off.push_back((int)up_bf2.size());
+        auto wf = [&](int s, int t) { return up_w[lp.dig_w_off[di] + s * nt + t]; };
+        auto pf = [&](int t) { return pr[cp(t < s0 ? t : t + na)]; };
+        pack_bfrag(up_bf, na, nt, lp.up_ks, wf, pf);
+        pack_bfrag2(up_bf2, na, nt, lp.up_ks, wf, pf);
       }
-      if (K > 0)
-        pack_bfrag(down_bf, K, l, lp.down_ks,
-                   [&](int k, int j) { return down_w[(size_t)k * l + j]; },
-                   [&](int j) { return pr[j]; });
+      if (K > 0) {
+        auto wf = [&](int k, int j) { return down_w[(size_t)k * l + j]; };
+        auto pf = [&](int j) { return pr[j]; };
+        pack_bfrag(down_bf, K, l, lp.down_ks, wf, pf);
+        pack_bfrag2(down_bf2, K, l, lp.down_ks, wf, pf);
+      }
     }
     lp.bf_ok = bf_ok;
     // exact CRT lift constants of Q_l = q_0 ... q_{l-1} (multi-limb, little endian)
@@ -414,6 +453,7 @@ int build_levels(FheContext* ctx) {
     lp.crt_qdrop = qdrop;
     Packer pk;
     const size_t o14 = pk.addv(up_bf), o15 = pk.addv(up_bf_off), o16 = pk.addv(down_bf);
+    const size_t o22 = pk.addv(up_bf2), o23 = pk.addv(up_bf2_off), o24 = pk.addv(down_bf2);
     const size_t o17 = pk.addv(crt_M), o18 = pk.addv(crt_Q), o19 = pk.addv(crt_Qh),
                  o20 = pk.addv(crt_inv), o21 = pk.addv(crt_qinv);
     const size_t o1 = pk.addv(up_inv), o2 = pk.addv(up_w), o3 = pk.addv(ext_prime),
@@ -444,6 +484,9 @@ int build_levels(FheContext* ctx) {
       lp.up_bf = (const uint2*)(b + o14);
       lp.up_bf_off = (const int*)(b + o15);
       lp.down_bf = K > 0 ? (const uint2*)(b + o16) : nullptr;
+      lp.up_bf2 = (const uint2*)(b + o22);
+      lp.up_bf2_off = (const int*)(b + o23);
+      lp.down_bf2 = K > 0 ? (const uint2*)(b + o24) : nullptr;
     }
     if (fp64) {
       lp.up_inv_d = (const double2*)(b + o10);

@@ -57,6 +57,9 @@ struct LevelPlan {
   const uint2* up_bf = nullptr;
   const int* up_bf_off = nullptr;
   const uint2* down_bf = nullptr;
+  const uint2* up_bf2 = nullptr;     // the same, packed for bconv_imma2_kernel
+  const int* up_bf2_off = nullptr;
+  const uint2* down_bf2 = nullptr;
   void* dmem = nullptr;
 };
 

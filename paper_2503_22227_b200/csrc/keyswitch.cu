@@ -715,6 +715,17 @@ bool bconv_imma_enabled() {
   return on == 1;
 }
 
+// register-resident epilogue of the tensor-core conversion (default;
+// FHE_BCONV_LAYOUT=1 takes the shared-memory transpose variant)
+bool bconv_layout2() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("FHE_BCONV_LAYOUT");
+    on = (e && e[0] == '1') ? 0 : 1;
+  }
+  return on == 1;
+}
+
 int mac_chunk(const std::vector<u64>& primes) {
   u64 mx = 0;
   for (u64 p : primes) mx = p > mx ? p : mx;
@@ -780,8 +791,10 @@ int run_keyswitch(const FheContext& ctx, int level, const u64* d, long d_stride,
     const size_t smem = (size_t)max_w * sizeof(u64);
     dim3 grid((unsigned)std::max<long>(1, std::min<long>(n / kThreads, 1024)), lp.digits, batch);
     if (lp.bf_ok && lp.max_na >= 4 && bconv_imma_enabled()) {
-      BconvArgs ba{c, (long)level * n, ext, (long)lp.ext_rows * n, lp.dig_info, lp.up_bf_off,
-                   lp.up_bf, lp.up_inv, lp.up_inv_d, lp.ext_prime, 0, 0, 0, level, K};
+      const bool l2 = bconv_layout2();
+      BconvArgs ba{c, (long)level * n, ext, (long)lp.ext_rows * n, lp.dig_info,
+                   l2 ? lp.up_bf2_off : lp.up_bf_off, l2 ? lp.up_bf2 : lp.up_bf, lp.up_inv,
+                   lp.up_inv_d, lp.ext_prime, 0, 0, 0, level, K, l2};
       int max_nt = 0;
       for (int di = 0; di < lp.digits; ++di) max_nt = std::max(max_nt, level + K - lp.dig_na[di]);
       dim3 g((unsigned)std::max<long>(1, std::min<long>(n / (32 * kBcWarps), 64)), lp.digits,
@@ -866,8 +879,10 @@ int run_keyswitch(const FheContext& ctx, int level, const u64* d, long d_stride,
                                              K, L);
       };
       if (lp.bf_ok && lp.down_bf && K >= 4 && bconv_imma_enabled()) {
-        BconvArgs ba{accP, (long)K * n, conv, (long)level * n, nullptr, nullptr, lp.down_bf,
-                     lp.down_inv, lp.down_inv_d, nullptr, K, level, L, level, K};
+        const bool l2 = bconv_layout2();
+        BconvArgs ba{accP, (long)K * n, conv, (long)level * n, nullptr, nullptr,
+                     l2 ? lp.down_bf2 : lp.down_bf, lp.down_inv, lp.down_inv_d, nullptr, K, level,
+                     L, level, K, l2};
         dim3 g((unsigned)std::max<long>(1, std::min<long>(n / (32 * kBcWarps), 64)), 1,
                batch * 2);
         rc = launch_bconv(ch, ba, K, level, g, st);

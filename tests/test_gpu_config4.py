@@ -242,10 +242,14 @@ def test_tensor_core_bconv_equals_fp64_bconv():
 
     script = os.path.join(os.path.dirname(os.path.abspath(__file__)), "helpers", "bconv_paths.py")
     res = {}
-    for flag in ("1", "0"):
+    # tensor cores (register epilogue, the default), tensor cores (shared-memory
+    # transpose epilogue), FP64 pipe
+    for tag, env in (("imma2", {}), ("imma1", {"FHE_BCONV_LAYOUT": "1"}),
+                     ("fp64", {"FHE_BCONV_IMMA": "0"})):
         r = subprocess.run([sys.executable, script], capture_output=True, text=True, timeout=600,
-                           env=dict(os.environ, FHE_BCONV_IMMA=flag))
+                           env=dict(os.environ, **env))
         assert r.returncode == 0, r.stderr[-2000:]
-        res[flag] = json.loads(r.stdout.strip().splitlines()[-1])
-    assert res["1"]["hmult"] == res["0"]["hmult"]
-    assert res["1"]["rotate"] == res["0"]["rotate"]
+        res[tag] = json.loads(r.stdout.strip().splitlines()[-1])
+    for tag in ("imma1", "fp64"):
+        assert res["imma2"]["hmult"] == res[tag]["hmult"], tag
+        assert res["imma2"]["rotate"] == res[tag]["rotate"], tag

@@ -11,7 +11,7 @@ nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler
   --expt-relaxed-constexpr -cudart static -Xptxas -v "$@" -c $SRC.cu -o build/${SRC}_$NAME.o \
   2> build/${SRC}_$NAME.ptxas.log
 OBJS=""
-for f in context ntt ntt_mm poly keyswitch behz capi; do
+for f in context ntt ntt_mm poly keyswitch behz crt philox crc32 capi; do
   if [ "$f" = "$SRC" ]; then OBJS="$OBJS build/${SRC}_$NAME.o"; else OBJS="$OBJS build/$f.o"; fi
 done
 nvcc -gencode arch=compute_100a,code=sm_100a -shared -cudart static -o ../lib/libfhe_$NAME.so $OBJS
