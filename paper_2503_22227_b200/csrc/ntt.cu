@@ -861,6 +861,20 @@ int launch_fused_tma(const DevChain& ch, u64* dst, const u64* src, const CT& ct,
                      bool fwd, long src_bstride, long dst_bstride, int rows, int limbs,
                      cudaStream_t st, bool& done, bool bcast = false) {
   done = false;
+#if FHE_FUSE_L2HINT & 8
+  // experiment: a persisting L2 carve-out, so the evict_last policy of the
+  // intermediate stores has lines to keep
+  static bool l2set = false;
+  if (!l2set) {
+    int dev = 0, mx = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&mx, cudaDevAttrMaxPersistingL2CacheSize, dev);
+    cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)mx);
+    if (getenv("FHE_NTT_CLUSTER_DEBUG")) fprintf(stderr, "persisting L2 %d bytes\n", mx);
+    cudaGetLastError();
+    l2set = true;
+  }
+#endif
   const int log_c = kChunkLogTile - KT::LOG_S - kt.log_r;
   // forward: columns read src, chunks work in place on dst; inverse: chunks
   // read src, columns work in place on dst.  bcast (forward): src holds one
