@@ -76,5 +76,7 @@ int launch_automorph(u64* out, const u64* in, long rows, int log_n, u64 elt, cud
 int launch_modswitch_expand(const DevChain& ch, u64* corr, const u64* last, int polys,
                             int new_level, int last_prime, u64 t_plain, WPair tinv_last,
                             const u64* t_mod, const u64* qlast_mod, cudaStream_t st);
+int launch_rescale_small(const DevChain& ch, u64* out, const u64* in, const u64* last, int polys,
+                         int level, const WPair* inv, const u64* qlast_mod, cudaStream_t st);
 int launch_modswitch_finish(const DevChain& ch, u64* out, const u64* in, const u64* corr,
                             int polys, int level, const WPair* inv, cudaStream_t st);

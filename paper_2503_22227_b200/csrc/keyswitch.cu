@@ -1025,6 +1025,19 @@ static bool bcast_rescale_enabled() {
   return on == 1;
 }
 
+// one-kernel rescale for N <= 2^12 (rescale_small_kernel): opt-in
+// (FHE_RESCALE_SMALL=1) -- its radix-2 shared-memory NTT is slower than the
+// broadcast-input tile NTT + finish it would replace (PDQ query 1: 7.7 vs
+// 5.8 ms graph-replayed)
+static bool small_rescale_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("FHE_RESCALE_SMALL");
+    on = (e && e[0] == '1') ? 1 : 0;
+  }
+  return on == 1;
+}
+
 size_t rescale_workspace(const FheContext& ctx, int polys, int level) {
   const size_t n = (size_t)1 << ctx.chain->log_n;
   return (size_t)polys * level * n * sizeof(u64);
@@ -1061,6 +1074,9 @@ int run_rescale(FheContext& ctx, u64* out, const u64* in, int polys, int level, 
                                   RowMap{nullptr, 1, level - 1}, (long)level * n, 0},
                       true, st);
   if (rc) return rc;
+  // N <= 2^12 (CKKS): expand, NTT and finish in one kernel per (limb, poly)
+  if (t_plain == 0 && ch.log_n <= 12 && small_rescale_enabled())
+    return launch_rescale_small(ch, out, in, last, polys, level, lp.rs_inv, lp.rs_qlast, st);
   // CKKS: the correction rows are the centred last limb mod every q_j, which
   // the forward NTT reads straight from `last` (broadcast, centred input):
   // the expanded rows are never written.  Otherwise (BGV, or a shape the

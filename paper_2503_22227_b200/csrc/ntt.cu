@@ -977,6 +977,18 @@ int launch_rows(const DevChain& ch, const NttArgs& a, bool inverse, bool lazy, c
   tl.dst = RowAddr{a.dst_bstride, a.map.limbs, LOG_N};
   tl.fwd = !inverse;
   const int ntiles = (a.rows + T::NB - 1) / T::NB;
+  if (a.bcast_src) {
+    // centred broadcast input (rescale correction), FP64 path
+    if (a.bcast_done) *a.bcast_done = false;
+    if (inverse || !ch.fp64_ok) return 0;
+    tl.bcast_limbs = a.map.limbs;
+    tl.bcast_stride = a.bcast_stride;
+    tl.center = (double)a.center_q;
+    path_hit(FHE_NTT_PATH_ROWS);
+    const int rc = launch_tiles_fp<T, true, FPIN_U64, FPOUT_U64>(ch, a.dst, a.bcast_src, tl, ntiles, st);
+    if (!rc && a.bcast_done) *a.bcast_done = true;
+    return rc;
+  }
   path_hit(ch.fp64_ok ? FHE_NTT_PATH_ROWS : FHE_NTT_PATH_INT);
   if (ch.fp64_ok)
     return inverse ? launch_tiles_fp<T, false, FPIN_U64, FPOUT_U64>(ch, a.dst, a.src, tl, ntiles, st)

@@ -150,7 +150,9 @@ struct RowsTile {
   static constexpr bool TMA = false;
   static constexpr bool SWZ = false;   // 128B-swizzled rows (TMA chunk tiles)
   static constexpr int THREADS = kRowThreads;
-  static constexpr double center = 0.0;  // (column tiles only: centred broadcast input)
+  double center = 0.0;    // != 0: centred broadcast input (NttArgs::center_q)
+  int bcast_limbs = 0;    // != 0: input row r is row r / bcast_limbs of src
+  long bcast_stride = 0;  //        (bcast_stride words apart)
   static constexpr int MINB = 2;
   static constexpr int NBUF = 2;
   static constexpr int SMEM_WORDS = padded_words(NB * S);
@@ -178,6 +180,7 @@ struct RowsTile {
     g = G & ((1 << gpa_log) - 1);
   }
   __device__ __forceinline__ const u64* gsrc(const u64* base, int b, int k) const {
+    if (bcast_limbs) return base + (long)((row0 + b) / bcast_limbs) * bcast_stride + k;
     return base + src(row0 + b) + k;
   }
   __device__ __forceinline__ u64* gdst(u64* base, int b, int k) const {
@@ -729,7 +732,7 @@ __device__ __forceinline__ void run_pass_fp(u64* sm, const double2* tws, const T
 #pragma unroll
     for (int i = 0; i < E; ++i)
       x[i] = (FIRST && IN == FPIN_U64) ? fp_from_u52(raw[i]) : __longlong_as_double((long long)raw[i]);
-    if constexpr (FIRST && IN == FPIN_U64 && Tile::COLS) {
+    if constexpr (FIRST && IN == FPIN_U64) {
       // centred broadcast input (rescale): the signed representative itself
       if (tl.center != 0.0) {
         const double hq = 0.5 * tl.center;

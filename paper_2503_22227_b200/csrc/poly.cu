@@ -193,7 +193,66 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
+// One-kernel rescale body for rows that fit one CTA (N <= 2^12): CTA (j, p)
+// expands the centred last limb of poly p mod q_j (modswitch_expand_kernel's
+// formula), runs the forward NTT mod q_j in shared memory (Cooley-Tukey with
+// psi_br[m + i], ntt.py:145-169, canonical butterflies) and applies the
+// finish (in_j - corr_j) q_last^-1 -- the expanded and transformed
+// correction never touches HBM, and the rescale is 2 launches instead of 4.
+__global__ void __launch_bounds__(kThreads)
+    rescale_small_kernel(const DevChain ch, u64* __restrict__ out, const u64* __restrict__ in,
+                         const u64* __restrict__ last, int level, const WPair* __restrict__ inv,
+                         const u64* __restrict__ qlast_mod) {
+  extern __shared__ u64 rs_row[];
+  const int j = blockIdx.x, p = blockIdx.y;
+  const int new_level = level - 1;
+  const int log_n = ch.log_n;
+  const int n = 1 << log_n;
+  const ModConst m = ch.mc[j];
+  const u64 q = m.q;
+  const u64 half = ch.mc[level - 1].q >> 1;
+  const u64 qlm = qlast_mod[j];
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const u64 c = last[(long)p * n + i];
+    u64 r = reduce_word(c, m);
+    if (c > half) r = sub_mod(r, qlm, q);
+    rs_row[i] = r;
+  }
+  __syncthreads();
+  const WPair* tw = ch.tw + ((size_t)j << log_n);
+  for (int mm = 1, t = n >> 1; mm < n; mm <<= 1, t >>= 1) {
+    for (int k = threadIdx.x; k < (n >> 1); k += blockDim.x) {
+      const int i = k / t, jj = 2 * i * t + (k - i * t);
+      const WPair w = tw[mm + i];
+      const u64 u = rs_row[jj];
+      const u64 v = shoup_mul(rs_row[jj + t], w.w, w.sh, q);
+      rs_row[jj] = add_mod(u, v, q);
+      rs_row[jj + t] = sub_mod(u, v, q);
+    }
+    __syncthreads();
+  }
+  const WPair w = inv[j];
+  const u64* src = in + ((long)p * level + j) * n;
+  u64* dst = out + ((long)p * new_level + j) * n;
+  for (int i = threadIdx.x; i < n; i += blockDim.x)
+    dst[i] = shoup_mul(sub_mod(src[i], rs_row[i], q), w.w, w.sh, q);
+}
+
 }  // namespace
+
+int launch_rescale_small(const DevChain& ch, u64* out, const u64* in, const u64* last, int polys,
+                         int level, const WPair* inv, const u64* qlast_mod, cudaStream_t st) {
+  if (ch.log_n > 12) {
+    fhe_set_error("rescale_small: N > 2^12");
+    return -1;
+  }
+  if (polys <= 0 || level < 2) return 0;
+  dim3 grid(level - 1, polys);
+  rescale_small_kernel<<<grid, kThreads, ((size_t)1 << ch.log_n) * sizeof(u64), st>>>(
+      ch, out, in, last, level, inv, qlast_mod);
+  FHE_LAUNCH_CHECK();
+  return 0;
+}
 
 int grid_for(long work) {
   // enough CTAs for 8 resident per SM on 148 SMs, no more than the work needs
