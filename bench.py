@@ -821,7 +821,7 @@ def main():
     fwd_gbs = algo / (ntt_ms["forward"] / 1000.0) / 1e9
     traffic = None
     try:
-        with open(os.path.join(ROOT, "profiles", "r1_ntt_traffic.json")) as f:
+        with open(os.path.join(ROOT, "profiles", "r2_ntt_traffic.json")) as f:
             tr = json.load(f)
         if tr.get("fused_kernel_dram_bytes"):
             per, per_rows = tr["fused_kernel_dram_bytes"], tr.get("fused_rows", tr["rows"])
@@ -864,8 +864,8 @@ def main():
         "roofline": {"bound": "hbm", "kernel": "batched NTT forward (fused four-step TMA kernel), "
                      f"N=2^16, {rows} rows", "achieved": fwd_gbs, "peak": peak,
                      "peak_kind": peak_kind, "unit": "GB/s", "frac": fwd_gbs / peak,
-                     "traffic": traffic, "traffic_source": "profiles/r1_ntt_traffic.json (ncu --set full of "
-                     "the same 5120-row launch; scaled per row for other sizes)", "inverse_achieved": inv_gbs,
+                     "traffic": traffic, "traffic_source": "profiles/r2_ntt_traffic.json (ncu --set full of "
+                     "the same 5120-row launch, round 2; scaled per row for other sizes)", "inverse_achieved": inv_gbs,
                      "algorithmic_bytes_per_launch": algo},
         "ntt": {"forward_ms": ntt_ms["forward"], "inverse_ms": ntt_ms["inverse"],
                 "forward_gbs": fwd_gbs, "inverse_gbs": inv_gbs, "rows": rows, "N": n},
