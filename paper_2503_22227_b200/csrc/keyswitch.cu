@@ -639,15 +639,23 @@ __global__ void __launch_bounds__(kThreads)
   __syncthreads();
   const int log_n = ch.log_n;
   const long n = 1L << log_n;
-  const long total = (long)(level + K) << log_n;
-  for (long t = blockIdx.x * (long)blockDim.x + threadIdx.x; t < total;
-       t += (long)gridDim.x * blockDim.x) {
+  // one thread per (batch item, output limb, coefficient): at the small
+  // ring degrees this kernel serves (the per-prime gadget of the PDQ
+  // profile, N = 4096) a thread per (limb, coefficient) looping over the
+  // batch left most of the GPU idle; the key words are re-read per item
+  // from L2
+  const long per_b = (long)(level + K) << log_n;
+  const long total = per_b * batch;
+  for (long tt = blockIdx.x * (long)blockDim.x + threadIdx.x; tt < total;
+       tt += (long)gridDim.x * blockDim.x) {
+    const int b = (int)(tt / per_b);
+    const long t = tt - (long)b * per_b;
     const int m = (int)(t >> log_n);
     const long i = t & (n - 1);
     const int p = m < level ? m : L + (m - level);
     const double2 qd = ch.qd[p];
     const u64 q = ch.mc[p].q;
-    for (int b = 0; b < batch; ++b) {
+    {
       double sb = 0.0, sa = 0.0;
 #pragma unroll 4
       for (int di = 0; di < D; ++di) {
@@ -854,7 +862,7 @@ int run_keyswitch(const FheContext& ctx, int level, const u64* d, long d_stride,
     else if (ch.fp64_ok && lp.digits == 4)
       go(ks_inner_fp_kernel<4>);
     else if (ch.fp64_ok)
-      ks_inner_fp_many_kernel<<<grid_for(work), kThreads, 4 * lp.digits * sizeof(int), st>>>(
+      ks_inner_fp_many_kernel<<<grid_for(work * batch), kThreads, 4 * lp.digits * sizeof(int), st>>>(
           ch, d, d_stride, ext, (long)lp.ext_rows * n, key, L + K, lp.dig_info, lp.digits, level,
           K, L, accQ, accP, add0, add1, add_stride, out0, out1, out_stride, batch);
     else
