@@ -688,7 +688,19 @@ def pdq_query_batch(world: int, queries: int = 16) -> dict:
         engine.run(standard_query(1 + i % 4), channel=inv, rng=mask_rng)
     torch.cuda.synchronize()
     ms = max_over_ranks((time.perf_counter() - t0) * 1e3, world)
-    return {"queries": queries, "ranks": world, "ms": ms, "queries_s": queries / (ms / 1000.0)}
+    out = {"queries": queries, "ranks": world, "ms": ms, "queries_s": queries / (ms / 1000.0)}
+    # the same batch with each query's device part replayed from its CUDA graph
+    from paper_2503_22227_b200.pdq.graphs import CapturedQuery
+
+    graphs = {q: CapturedQuery(engine, standard_query(q)) for q in (1, 2, 3, 4)}
+    barrier(world)
+    t0 = time.perf_counter()
+    for i in mine:
+        graphs[1 + i % 4].run(channel=inv, rng=mask_rng)
+    torch.cuda.synchronize()
+    gms = max_over_ranks((time.perf_counter() - t0) * 1e3, world)
+    out.update({"graph_ms": gms, "graph_queries_s": queries / (gms / 1000.0)})
+    return out
 
 
 def cpu_baseline_hmult(ops: int = 8, warmup: int = 1, seconds_budget: float = 180.0):
