@@ -91,8 +91,38 @@ __device__ __forceinline__ u64 bc_reduce71(u64 hi, u64 lo, const BcTarget& tg) {
   return csub(r, tg.p);
 }
 
+// V = sum_b P_b 2^(8b) from the 7 byte partials and its canonical residue,
+// in 32-bit pieces (the value is that of bc_reduce71 on the 128-bit sum):
+//   v = P0 + P1 2^8 + P2 2^16 + P3 2^24 < 2^48,  H = P4 + P5 2^8 + P6 2^16 < 2^40,
+//   V = v + H 2^32 = (hi : lo) with hi < 2^7;
+//   x = V >> sh < 2^32 (sh >= 39), mu < 2^32, qe = (x mu) >> (71 - sh) < 2^32.
+// Each partial product is one IMAD.WIDE.U32 instead of 64-bit shift/add pairs.
+__device__ __forceinline__ u64 bc_combine71(unsigned a0, unsigned a1, unsigned a2, unsigned a3,
+                                            unsigned a4, unsigned a5, unsigned a6,
+                                            const BcTarget& tg) {
+  u64 v = (u64)a1 * 256u + a0;
+  v = (u64)a2 * 65536u + v;
+  v = (u64)a3 * 16777216u + v;
+  u64 h = (u64)a5 * 256u + a4;
+  h = (u64)a6 * 65536u + h;
+  unsigned lo_hi, hi;
+  asm("add.cc.u32 %0, %2, %3;\n\taddc.u32 %1, %4, 0;"
+      : "=r"(lo_hi), "=r"(hi)
+      : "r"((unsigned)(v >> 32)), "r"((unsigned)h), "r"((unsigned)(h >> 32)));
+  const unsigned x = __funnelshift_r(lo_hi, hi, tg.sh - 32);
+  const u64 prod = (u64)x * (unsigned)tg.mu;
+  const unsigned qe = __funnelshift_rc((unsigned)prod, (unsigned)(prod >> 32), 71 - tg.sh);
+  const u64 lo = ((u64)lo_hi << 32) | (unsigned)v;
+  u64 r = lo - (u64)qe * tg.p;
+  r = csub(r, tg.p);
+  return csub(r, tg.p);
+}
+
 // FPPRO: the prologue product y = [x inv]_q on the FP64 pipe (fp_mulmod; the
 // pipe is otherwise idle here), else the integer Shoup product.
+#ifndef FHE_BCONV_COMBINE32
+#define FHE_BCONV_COMBINE32 1
+#endif
 #ifndef FHE_BCONV_MINB
 #define FHE_BCONV_MINB 2
 #endif
@@ -371,13 +401,19 @@ __global__ void __launch_bounds__(kBcThreads, FHE_BCONV_MINB)
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             const int ci = 2 * h + e;
+#if FHE_BCONV_COMBINE32
+            const u64 r = bc_combine71(acc[0][m][ci], acc[1][m][ci], acc[2][m][ci], acc[3][m][ci],
+                                       acc[4][m][ci], acc[5][m][ci], acc[6][m][ci], tg);
+#else
             u64 lo = (u64)(unsigned)acc[0][m][ci] + ((u64)(unsigned)acc[1][m][ci] << 8) +
                      ((u64)(unsigned)acc[2][m][ci] << 16) + ((u64)(unsigned)acc[3][m][ci] << 24) +
                      ((u64)(unsigned)acc[4][m][ci] << 32) + ((u64)(unsigned)acc[5][m][ci] << 40);
             u64 hi = 0;
             const u64 p6 = (u64)(unsigned)acc[6][m][ci];
             add_wide(hi, lo, p6 >> 16, p6 << 48);
-            if (t < nt) dst[(long)t * n + c0 + 16 * m + 8 * h + gr] = bc_reduce71(hi, lo, tg);
+            const u64 r = bc_reduce71(hi, lo, tg);
+#endif
+            if (t < nt) dst[(long)t * n + c0 + 16 * m + 8 * h + gr] = r;
           }
       }
     }

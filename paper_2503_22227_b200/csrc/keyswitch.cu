@@ -623,6 +623,175 @@ __global__ void __launch_bounds__(kThreads, TENS  ? FHE_TENS_MINB
   }
 }
 
+// Staged variant of ks_inner_fp_kernel<kD, true, TENS> (the fused Q-limb
+// inner product + ModDown finish, the largest single HBM stream of HMult+Relin).
+// The register-blocked kernel keeps FHE_INNER_BU batch items of loads in
+// flight and then computes with none in flight, so at 2 CTAs/SM it ran
+// latency-bound (ncu: 49% of DRAM peak, 54% long-scoreboard stalls on the
+// first use of each word).  Here every operand word of batch item b + ST - 1
+// is copied into this thread's shared-memory slots with cp.async (8-byte
+// .ca copies, no registers held) while item b computes, so ST - 1 items per
+// thread are always in flight.  Each thread reads back only the slots it
+// filled itself, so wait_group alone orders the pipeline (no CTA barrier).
+// Arithmetic and results are those of ks_inner_fp_kernel word for word.
+__device__ __forceinline__ void ks_cp8(u64* s, const u64* g) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(s);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(a), "l"(g) : "memory");
+}
+__device__ __forceinline__ void ks_cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void ks_cp_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+#ifndef FHE_FIN_STAGES
+#define FHE_FIN_STAGES 4
+#endif
+#ifndef FHE_FINS_MINB
+#define FHE_FINS_MINB 3
+#endif
+
+template <int kD, bool TENS>
+constexpr int fin_words() {
+  return TENS ? (kD - 1) + 2 + 4 : kD + 2 + 2;
+}
+
+template <int kD, bool TENS>
+size_t fin_staged_smem() {
+  return 64 + (size_t)FHE_FIN_STAGES * fin_words<kD, TENS>() * kThreads * sizeof(u64);
+}
+
+template <int kD, bool TENS>
+__global__ void __launch_bounds__(kThreads, FHE_FINS_MINB)
+    ks_fin_staged_kernel(const DevChain ch, const u64* __restrict__ d, long d_stride,
+                         const u64* __restrict__ ext, long ext_stride, const u64* __restrict__ key,
+                         int keyL, const int* __restrict__ dig_info, int D, int level,
+                         const u64* add0, const u64* add1, long add_stride, u64* out0, u64* out1,
+                         long out_stride, int batch, const u64* __restrict__ conv,
+                         const WPair* __restrict__ p_inv) {
+  constexpr int W = fin_words<kD, TENS>();
+  constexpr int ST = FHE_FIN_STAGES;
+  extern __shared__ __align__(16) unsigned char fsm[];
+  int* sinfo = reinterpret_cast<int*>(fsm);
+  u64* stage = reinterpret_cast<u64*>(fsm + 64);
+  if (threadIdx.x < 4 * D) sinfo[threadIdx.x] = dig_info[threadIdx.x];
+  __syncthreads();
+  const int log_n = ch.log_n;
+  const long n = 1L << log_n;
+  const long total = (long)level << log_n;
+  // slot (s, w) of this thread
+  auto slot = [&](int s, int w) { return stage + ((long)(s * W + w) * kThreads + threadIdx.x); };
+  for (long t = blockIdx.x * (long)blockDim.x + threadIdx.x; t < total;
+       t += (long)gridDim.x * blockDim.x) {
+    const int m = (int)(t >> log_n);
+    const long i = t & (n - 1);
+    const long w = (long)m * n + i;
+    const double2 qd = ch.qd[m];
+    const u64 q = ch.mc[m].q;
+    const u64* src[kD];
+    long sstr[kD];
+    int own_di = -1;
+#pragma unroll
+    for (int di = 0; di < kD; ++di) {
+      if (di < D) {
+        const int s0 = sinfo[4 * di], na = sinfo[4 * di + 1], ro = sinfo[4 * di + 2];
+        const bool own = m >= s0 && m < s0 + na;
+        if (own) own_di = di;
+        src[di] = own ? d + w : ext + (long)(ro + (m < s0 ? m : m - na)) * n + i;
+        sstr[di] = own ? d_stride : ext_stride;
+      }
+    }
+    // word order in a stage: digits (own digit skipped under TENS), conv b/a,
+    // then x0 x1 y0 y1 (TENS) or add0 add1
+    auto issue = [&](int b) {
+      if (b < batch) {
+        const int s = b % ST;
+        int k = 0;
+#pragma unroll
+        for (int di = 0; di < kD; ++di) {
+          if (di < D && !(TENS && di == own_di)) ks_cp8(slot(s, k), src[di] + b * sstr[di]);
+          if (di < D && !(TENS && di == own_di)) ++k;
+        }
+        k = TENS ? kD - 1 : kD;
+        ks_cp8(slot(s, k), conv + ((long)(b * 2 + 0) * level) * n + w);
+        ks_cp8(slot(s, k + 1), conv + ((long)(b * 2 + 1) * level) * n + w);
+        if constexpr (TENS) {
+          const u64* xb = add0 + b * add_stride + w;
+          const u64* yb = add1 + b * add_stride + w;
+          ks_cp8(slot(s, k + 2), xb);
+          ks_cp8(slot(s, k + 3), xb + (long)level * n);
+          ks_cp8(slot(s, k + 4), yb);
+          ks_cp8(slot(s, k + 5), yb + (long)level * n);
+        } else {
+          if (add0) ks_cp8(slot(s, k + 2), add0 + b * add_stride + w);
+          if (add1) ks_cp8(slot(s, k + 3), add1 + b * add_stride + w);
+        }
+      }
+      ks_cp_commit();  // always one group per step (empty past the end)
+    };
+#pragma unroll
+    for (int s = 0; s < ST - 1; ++s) issue(s);
+    double2 kb[kD], ka[kD];
+#pragma unroll
+    for (int di = 0; di < kD; ++di) {
+      if (di < D) {
+        const double b = fp_from_u52(__ldg(key + ((long)(2 * di) * keyL + m) * n + i));
+        const double a = fp_from_u52(__ldg(key + ((long)(2 * di + 1) * keyL + m) * n + i));
+        kb[di] = make_double2(b, __dmul_rn(b, qd.y));
+        ka[di] = make_double2(a, __dmul_rn(a, qd.y));
+      }
+    }
+    const WPair pi = p_inv[m];
+    for (int b = 0; b < batch; ++b) {
+      issue(b + ST - 1);
+      ks_cp_wait<ST - 1>();
+      const int s = b % ST;
+      const int k0 = TENS ? kD - 1 : kD;
+      double d2 = 0.0;
+      u64 av0 = 0, av1 = 0;
+      if constexpr (TENS) {
+        const double a0 = fp_from_u52(*slot(s, k0 + 2)), a1 = fp_from_u52(*slot(s, k0 + 3));
+        const double c0 = fp_from_u52(*slot(s, k0 + 4)), c1 = fp_from_u52(*slot(s, k0 + 5));
+        const double2 w0 = make_double2(c0, __dmul_rn(c0, qd.y));
+        const double2 w1 = make_double2(c1, __dmul_rn(c1, qd.y));
+        av0 = fp_canon_half(fp_reduce(fp_mulmod(a0, w0, qd.x), qd), qd.x);
+        av1 = fp_canon_half(
+            fp_reduce(__dadd_rn(fp_mulmod(a0, w1, qd.x), fp_mulmod(a1, w0, qd.x)), qd), qd.x);
+        const double r2 = fp_reduce(fp_mulmod(a1, w1, qd.x), qd);
+        d2 = r2 < 0.0 ? __dadd_rn(r2, qd.x) : r2;
+      } else {
+        if (add0) av0 = *slot(s, k0 + 2);
+        if (add1) av1 = *slot(s, k0 + 3);
+      }
+      double sb = 0.0, sa = 0.0;
+      int k = 0;
+#pragma unroll
+      for (int di = 0; di < kD; ++di) {
+        if (di < D) {
+          double x;
+          if (TENS && di == own_di) {
+            x = d2;
+          } else {
+            x = fp_from_u52(*slot(s, k));
+            ++k;
+          }
+          sb = __dadd_rn(sb, fp_mulmod(x, kb[di], qd.x));
+          sa = __dadd_rn(sa, fp_mulmod(x, ka[di], qd.x));
+        }
+      }
+      const u64 rb = fp_canon_half(fp_reduce(sb, qd), qd.x);
+      const u64 ra = fp_canon_half(fp_reduce(sa, qd), qd.x);
+      u64 v0 = shoup_mul(sub_mod(rb, *slot(s, k0), q), pi.w, pi.sh, q);
+      u64 v1 = shoup_mul(sub_mod(ra, *slot(s, k0 + 1), q), pi.w, pi.sh, q);
+      if (TENS || add0) v0 = add_mod(av0, v0, q);
+      if (TENS || add1) v1 = add_mod(av1, v1, q);
+      out0[b * out_stride + w] = v0;
+      out1[b * out_stride + w] = v1;
+    }
+    ks_cp_wait<0>();
+  }
+}
+
 // FP64 key inner product for many digits (the reference's per-prime gadget,
 // alpha = 1, D = level digits): digits stream through one accumulator pair
 // per output, reduced every 8 terms (|sum| <= 8 * 0.75p + p < 2^53).
@@ -689,6 +858,16 @@ __global__ void __launch_bounds__(kThreads)
       }
     }
   }
+}
+
+// FHE_FIN_STAGED=0 selects the register-blocked finish kernel
+static bool fin_staged_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("FHE_FIN_STAGED");
+    on = (e && e[0] == '0') ? 0 : 1;
+  }
+  return on == 1;
 }
 
 bool fin_inner_enabled() {
@@ -919,6 +1098,26 @@ int run_keyswitch(const FheContext& ctx, int level, const u64* d, long d_stride,
   rc = launch_ntt(ch, na, false, st);
   if (rc) return rc;
   if (fin_done) return 0;
+  if (fin_inner && fin_staged_enabled()) {
+    auto go = [&](auto kern, size_t smem_b) {
+      if (smem_b > 48 * 1024)
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_b);
+      kern<<<grid_for((long)level << log_n), kThreads, smem_b, st>>>(
+          ch, d, d_stride, ext, (long)lp.ext_rows * n, key, L + K, lp.dig_info, lp.digits, level,
+          add0, add1, add_stride, out0, out1, out_stride, batch, conv, lp.p_inv);
+    };
+    if (tens) {
+      if (lp.digits <= 2) go(ks_fin_staged_kernel<2, true>, fin_staged_smem<2, true>());
+      else if (lp.digits == 3) go(ks_fin_staged_kernel<3, true>, fin_staged_smem<3, true>());
+      else go(ks_fin_staged_kernel<4, true>, fin_staged_smem<4, true>());
+    } else {
+      if (lp.digits <= 2) go(ks_fin_staged_kernel<2, false>, fin_staged_smem<2, false>());
+      else if (lp.digits == 3) go(ks_fin_staged_kernel<3, false>, fin_staged_smem<3, false>());
+      else go(ks_fin_staged_kernel<4, false>, fin_staged_smem<4, false>());
+    }
+    FHE_LAUNCH_CHECK();
+    return 0;
+  }
   if (fin_inner) {
     // Q-limb inner product + ModDown finish in one pass
     auto go = [&](auto kern) {
