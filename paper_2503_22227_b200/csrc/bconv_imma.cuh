@@ -68,6 +68,8 @@ struct BconvArgs {
   int src_prime0;           // ModDown: L (first P prime); ModUp: 0 (+ s0)
   int level, K;
   bool layout2 = false;     // bfrag packed for bconv_imma2_kernel (pack_bfrag2)
+  const uint4* bumma = nullptr;  // W' in the tcgen05 operand layout (bconv_umma.cuh)
+  const int* bu_off = nullptr;   // ModUp: per digit offset (uint4 units) into bumma
 };
 
 // Per-target reduction constants of the epilogue: V < 2^71 is reduced by one

@@ -299,6 +299,36 @@ static void pack_bfrag2(std::vector<uint2>& out, int ns, int nt, int ks, W w, P 
         }
 }
 
+// The same matrix as B operand of the tcgen05 u8 MMA (bconv_umma.cuh): row
+// (target t, byte b) = t * 8 + b (b = 7 and t >= nt zero), K-major over
+// k = 7 s + a, in the canonical no-swizzle layout [k16 chunk][t][b][16 B]
+// with the target count padded to a multiple of 8 (whole MMA chunks).
+template <class W, class P>
+static void pack_bumma(std::vector<uint4>& out, int ns, int nt, int ks, W w, P p) {
+  std::vector<u64> v((size_t)ns * 7 * nt);
+  for (int s = 0; s < ns; ++s)
+    for (int t = 0; t < nt; ++t) {
+      const u64 pt = p(t);
+      u64 x = w(s, t) % pt;
+      for (int a = 0; a < 7; ++a) {
+        v[((size_t)s * 7 + a) * nt + t] = x;
+        x = mulmod_h(x, 256 % pt, pt);
+      }
+    }
+  auto byte = [&](int k, int t, int b) -> unsigned {
+    if (k >= 7 * ns || t >= nt || b >= 7) return 0;
+    return (unsigned)((v[(size_t)k * nt + t] >> (8 * b)) & 0xff);
+  };
+  const int ng = (nt + 7) & ~7;
+  for (int kc = 0; kc < 2 * ks; ++kc)
+    for (int t = 0; t < ng; ++t)
+      for (int b = 0; b < 8; ++b) {
+        unsigned wd[4] = {0, 0, 0, 0};
+        for (int i = 0; i < 16; ++i) wd[i / 4] |= byte(16 * kc + i, t, b) << (8 * (i % 4));
+        out.push_back(make_uint4(wd[0], wd[1], wd[2], wd[3]));
+      }
+}
+
 // Product of primes[idx] for idx in [lo, hi) except `skip`, reduced mod m.
 static u64 punct_mod(const std::vector<u64>& primes, int lo, int hi, int skip, u64 m) {
   u64 r = 1 % m;
@@ -391,7 +421,8 @@ int build_levels(FheContext* ctx) {
     bool bf_ok = K <= 16;
     for (u64 q : pr) bf_ok &= q < ((u64)1 << 56) && q >= ((u64)1 << 39);  // bc_reduce71 domain
     std::vector<uint2> up_bf, down_bf, up_bf2, down_bf2;
-    std::vector<int> up_bf_off, up_bf2_off;
+    std::vector<int> up_bf_off, up_bf2_off, up_bu_off;
+    std::vector<uint4> up_bu, down_bu;
     if (bf_ok) {
       int max_na = 0;
       for (int di = 0; di < D; ++di) max_na = std::max(max_na, lp.dig_na[di]);
@@ -407,12 +438,15 @@ int build_levels(FheContext* ctx) {
         auto pf = [&](int t) { return pr[cp(t < s0 ? t : t + na)]; };
         pack_bfrag(up_bf, na, nt, lp.up_ks, wf, pf);
         pack_bfrag2(up_bf2, na, nt, lp.up_ks, wf, pf);
+        up_bu_off.push_back((int)up_bu.size());
+        pack_bumma(up_bu, na, nt, lp.up_ks, wf, pf);
       }
       if (K > 0) {
         auto wf = [&](int k, int j) { return down_w[(size_t)k * l + j]; };
         auto pf = [&](int j) { return pr[j]; };
         pack_bfrag(down_bf, K, l, lp.down_ks, wf, pf);
         pack_bfrag2(down_bf2, K, l, lp.down_ks, wf, pf);
+        pack_bumma(down_bu, K, l, lp.down_ks, wf, pf);
       }
     }
     lp.bf_ok = bf_ok;
@@ -454,6 +488,7 @@ int build_levels(FheContext* ctx) {
     Packer pk;
     const size_t o14 = pk.addv(up_bf), o15 = pk.addv(up_bf_off), o16 = pk.addv(down_bf);
     const size_t o22 = pk.addv(up_bf2), o23 = pk.addv(up_bf2_off), o24 = pk.addv(down_bf2);
+    const size_t o25 = pk.addv(up_bu), o26 = pk.addv(up_bu_off), o27 = pk.addv(down_bu);
     const size_t o17 = pk.addv(crt_M), o18 = pk.addv(crt_Q), o19 = pk.addv(crt_Qh),
                  o20 = pk.addv(crt_inv), o21 = pk.addv(crt_qinv);
     const size_t o1 = pk.addv(up_inv), o2 = pk.addv(up_w), o3 = pk.addv(ext_prime),
@@ -487,6 +522,9 @@ int build_levels(FheContext* ctx) {
       lp.up_bf2 = (const uint2*)(b + o22);
       lp.up_bf2_off = (const int*)(b + o23);
       lp.down_bf2 = K > 0 ? (const uint2*)(b + o24) : nullptr;
+      lp.up_bu = (const uint4*)(b + o25);
+      lp.up_bu_off = (const int*)(b + o26);
+      lp.down_bu = K > 0 ? (const uint4*)(b + o27) : nullptr;
     }
     if (fp64) {
       lp.up_inv_d = (const double2*)(b + o10);

@@ -60,6 +60,11 @@ struct LevelPlan {
   const uint2* up_bf2 = nullptr;     // the same, packed for bconv_imma2_kernel
   const int* up_bf2_off = nullptr;
   const uint2* down_bf2 = nullptr;
+  // the same W' bytes in the tcgen05 operand layout (bconv_umma.cuh): per job
+  // [2 ks][round8(nt)][8 bytes b][16 B], ModUp per digit at up_bu_off (16 B units)
+  const uint4* up_bu = nullptr;
+  const int* up_bu_off = nullptr;
+  const uint4* down_bu = nullptr;
   void* dmem = nullptr;
 };
 

@@ -890,6 +890,31 @@ bool fuse_finish_enabled() {
 }
 
 #include "bconv_imma.cuh"
+#include "bconv_umma.cuh"
+
+// tcgen05 base conversion (default; FHE_BCONV_UMMA=0 takes the mma.sync kernels)
+bool bconv_umma_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("FHE_BCONV_UMMA");
+    on = (e && e[0] == '0') ? 0 : 1;
+  }
+  return on == 1;
+}
+
+// CTAs per job for the tcgen05 conversion: one wave of FHE_BU_MINB CTAs per
+// SM over all jobs, each CTA looping over 128-coefficient tiles
+static unsigned bu_grid_x(long n, int jobs) {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  const long tiles = n / kBuTile;
+  return (unsigned)std::max<long>(1, std::min<long>(tiles, (long)sms * FHE_BU_MINB / jobs));
+}
 
 // tensor-core base conversions (default when the level has the tables and a
 // digit of >= 4 limbs; FHE_BCONV_IMMA=0 keeps the FP64 / integer kernels)
@@ -984,9 +1009,16 @@ int run_keyswitch(const FheContext& ctx, int level, const u64* d, long d_stride,
                    lp.up_inv_d, lp.ext_prime, 0, 0, 0, level, K, l2};
       int max_nt = 0;
       for (int di = 0; di < lp.digits; ++di) max_nt = std::max(max_nt, level + K - lp.dig_na[di]);
-      dim3 g((unsigned)std::max<long>(1, std::min<long>(n / (32 * kBcWarps), 64)), lp.digits,
-             batch);
-      rc = launch_bconv(ch, ba, lp.max_na, max_nt, g, st);
+      if (bconv_umma_enabled() && n >= kBuTile && lp.up_bu) {
+        ba.bumma = lp.up_bu;
+        ba.bu_off = lp.up_bu_off;
+        rc = launch_bconv_umma(ch, ba, lp.max_na, max_nt,
+                               dim3(bu_grid_x(n, lp.digits * batch), lp.digits, batch), st);
+      } else {
+        dim3 g((unsigned)std::max<long>(1, std::min<long>(n / (32 * kBcWarps), 64)), lp.digits,
+               batch);
+        rc = launch_bconv(ch, ba, lp.max_na, max_nt, g, st);
+      }
       if (rc) return rc;
     } else if (ch.fp64_ok && lp.up_w_d) {
       int max_na = 0;
@@ -1070,9 +1102,15 @@ int run_keyswitch(const FheContext& ctx, int level, const u64* d, long d_stride,
         BconvArgs ba{accP, (long)K * n, conv, (long)level * n, nullptr, nullptr,
                      l2 ? lp.down_bf2 : lp.down_bf, lp.down_inv, lp.down_inv_d, nullptr, K, level,
                      L, level, K, l2};
-        dim3 g((unsigned)std::max<long>(1, std::min<long>(n / (32 * kBcWarps), 64)), 1,
-               batch * 2);
-        rc = launch_bconv(ch, ba, K, level, g, st);
+        if (bconv_umma_enabled() && n >= kBuTile && lp.down_bu) {
+          ba.bumma = lp.down_bu;
+          rc = launch_bconv_umma(ch, ba, K, level, dim3(bu_grid_x(n, batch * 2), 1, batch * 2),
+                                 st);
+        } else {
+          dim3 g((unsigned)std::max<long>(1, std::min<long>(n / (32 * kBcWarps), 64)), 1,
+                 batch * 2);
+          rc = launch_bconv(ch, ba, K, level, g, st);
+        }
         if (rc) return rc;
       } else {
         if (K <= 4) go(moddown_conv_fp_kernel<4, FHE_MODUP_U>);

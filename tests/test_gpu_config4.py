@@ -222,8 +222,11 @@ print(h(a), h(c))
 '''
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     digests = set()
-    for fin, tens in (("1", "1"), ("1", "0"), ("0", "1")):
-        env = dict(os.environ, FHE_FUSE_INNER_FINISH=fin, FHE_HMULT_TENS=tens, PYTHONPATH=root)
+    # (fused finish, tensor terms in the finish, cp.async-staged finish kernel)
+    for fin, tens, staged in (("1", "1", "1"), ("1", "1", "0"), ("1", "0", "1"), ("1", "0", "0"),
+                              ("0", "1", "1")):
+        env = dict(os.environ, FHE_FUSE_INNER_FINISH=fin, FHE_HMULT_TENS=tens,
+                   FHE_FIN_STAGED=staged, PYTHONPATH=root)
         out = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True,
                              text=True, timeout=900)
         assert out.returncode == 0, out.stderr[-2000:]
@@ -232,9 +235,10 @@ print(h(a), h(c))
 
 
 def test_tensor_core_bconv_equals_fp64_bconv():
-    """The tensor-core base conversion (csrc/bconv_imma.cuh, the default)
-    and the FP64-pipe conversion give the same words for HMult+Relin (batch
-    3, ragged last digit) and rotate."""
+    """The tcgen05 base conversion (csrc/bconv_umma.cuh, the default), the
+    mma.sync conversions (csrc/bconv_imma.cuh) and the FP64-pipe conversion
+    give the same words for HMult+Relin (batch 3, ragged last digit) and
+    rotate."""
     import json
     import os
     import subprocess
@@ -242,14 +246,15 @@ def test_tensor_core_bconv_equals_fp64_bconv():
 
     script = os.path.join(os.path.dirname(os.path.abspath(__file__)), "helpers", "bconv_paths.py")
     res = {}
-    # tensor cores (register epilogue, the default), tensor cores (shared-memory
-    # transpose epilogue), FP64 pipe
-    for tag, env in (("imma2", {}), ("imma1", {"FHE_BCONV_LAYOUT": "1"}),
+    # tcgen05 (TMEM accumulators, the default), mma.sync (register epilogue),
+    # mma.sync (shared-memory transpose epilogue), FP64 pipe
+    for tag, env in (("umma", {}), ("imma2", {"FHE_BCONV_UMMA": "0"}),
+                     ("imma1", {"FHE_BCONV_UMMA": "0", "FHE_BCONV_LAYOUT": "1"}),
                      ("fp64", {"FHE_BCONV_IMMA": "0"})):
         r = subprocess.run([sys.executable, script], capture_output=True, text=True, timeout=600,
                            env=dict(os.environ, **env))
         assert r.returncode == 0, r.stderr[-2000:]
         res[tag] = json.loads(r.stdout.strip().splitlines()[-1])
-    for tag in ("imma1", "fp64"):
-        assert res["imma2"]["hmult"] == res[tag]["hmult"], tag
-        assert res["imma2"]["rotate"] == res[tag]["rotate"], tag
+    for tag in ("imma2", "imma1", "fp64"):
+        assert res["umma"]["hmult"] == res[tag]["hmult"], tag
+        assert res["umma"]["rotate"] == res[tag]["rotate"], tag
