@@ -86,9 +86,11 @@ def ntt_rows(ctx: Context, t, limbs: int, offset: int = 0, inverse: bool = False
 
 
 # Ring degree from which keys and noise are sampled on the device (the same
-# Philox stream as the host sampler, coremath/sampling.py *_device): below it
-# the numpy draws are cheaper than the launches.
-DEVICE_SAMPLING_MIN_N = 1 << 13
+# Philox stream as the host sampler, coremath/sampling.py *_device).  At
+# N = 2^12 (the PDQ ring) a host encrypt spends 3.3 ms in numpy draws and
+# residue expansion against 0.37 ms on the device (tools/pdq_finish_time.py);
+# below 2^11 the host draws are cheaper than the launches.
+DEVICE_SAMPLING_MIN_N = 1 << 11
 
 
 def device_sampling(ctx: Context) -> bool:
