@@ -1,5 +1,6 @@
 // Internal device-side structures shared by the kernels and the C-ABI layer.
 #pragma once
+#include <utility>
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <string>
@@ -83,6 +84,40 @@ void fhe_set_error(const std::string& msg);
 // every kernel launch of the library is followed by FHE_LAUNCH_CHECK, which
 // also counts it (fhe_launch_count())
 void fhe_count_launch();
+
+// Programmatic dependent launch (PDL).  Kernels launched with fhe_launch
+// carry cudaLaunchAttributeProgrammaticStreamSerialization: the next kernel
+// on the stream may be scheduled while this one runs, once every CTA of this
+// one has executed fhe_pdl_trigger (issued at CTA start).  Every such kernel
+// begins with fhe_pdl_wait before touching memory written by earlier work,
+// which blocks until the preceding grid has completed and its writes are
+// visible -- so the overlap covers launch latency and CTA rasterisation, not
+// data.  Both instructions are no-ops for a kernel launched without the
+// attribute.  Off by default (FHE_PDL=1 turns it on): measured on the PDQ
+// query graphs (N = 2^12, ~640 small kernels) it is 1-4% slower, and eager
+// chains gain nothing (profiles/r2_pdq_latency.md).
+__device__ __forceinline__ void fhe_pdl_wait() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+__device__ __forceinline__ void fhe_pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" :::);
+}
+bool fhe_pdl_enabled();
+template <typename... KArgs, typename... Args>
+inline cudaError_t fhe_launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = fhe_pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 #define FHE_LAUNCH_CHECK()                                                     \
   do {                                                                         \

@@ -331,6 +331,8 @@ __global__ void __launch_bounds__(kThreads, FHE_MODUP_MINB)
                     u64* __restrict__ ext, long ext_stride, const int* __restrict__ dig_info,
                     const double2* __restrict__ up_inv, const double2* __restrict__ up_w, int level,
                     int K, int L) {
+  fhe_pdl_trigger();
+  fhe_pdl_wait();
   const int di = blockIdx.y, b = blockIdx.z;
   const int s0 = dig_info[4 * di], na = dig_info[4 * di + 1];
   const int row_off = dig_info[4 * di + 2], w_off = dig_info[4 * di + 3];
@@ -803,6 +805,8 @@ __global__ void __launch_bounds__(kThreads)
                             u64* __restrict__ accQ, u64* __restrict__ accP, const u64* add0,
                             const u64* add1, long add_stride, u64* out0, u64* out1,
                             long out_stride, int batch) {
+  fhe_pdl_trigger();
+  fhe_pdl_wait();
   extern __shared__ int sinfo[];
   for (int i = threadIdx.x; i < 4 * D; i += blockDim.x) sinfo[i] = dig_info[i];
   __syncthreads();
@@ -1027,8 +1031,8 @@ int run_keyswitch(const FheContext& ctx, int level, const u64* d, long d_stride,
       auto go = [&](auto kern) {
         if (smem_d > 48 * 1024)
           cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_d);
-        kern<<<grid, kThreads, smem_d, st>>>(ch, c, (long)level * n, ext, (long)lp.ext_rows * n,
-                                             lp.dig_info, lp.up_inv_d, lp.up_w_d, level, K, L);
+        fhe_launch(kern, grid, dim3(kThreads), smem_d, st, ch, c, (long)level * n, ext,
+                   (long)lp.ext_rows * n, lp.dig_info, lp.up_inv_d, lp.up_w_d, level, K, L);
       };
       if (max_na <= 4) go(modup_fp_kernel<4, FHE_MODUP_U>);
       else if (max_na <= 12) go(modup_fp_kernel<12, FHE_MODUP_U>);
@@ -1073,9 +1077,10 @@ int run_keyswitch(const FheContext& ctx, int level, const u64* d, long d_stride,
     else if (ch.fp64_ok && lp.digits == 4)
       go(ks_inner_fp_kernel<4>);
     else if (ch.fp64_ok)
-      ks_inner_fp_many_kernel<<<grid_for(work * batch), kThreads, 4 * lp.digits * sizeof(int), st>>>(
-          ch, d, d_stride, ext, (long)lp.ext_rows * n, key, L + K, lp.dig_info, lp.digits, level,
-          K, L, accQ, accP, add0, add1, add_stride, out0, out1, out_stride, batch);
+      fhe_launch(ks_inner_fp_many_kernel, dim3(grid_for(work * batch)), dim3(kThreads),
+                 4 * lp.digits * sizeof(int), st, ch, d, d_stride, ext, (long)lp.ext_rows * n, key,
+                 L + K, lp.dig_info, lp.digits, level, K, L, accQ, accP, add0, add1, add_stride,
+                 out0, out1, out_stride, batch);
     else
       ks_inner_kernel<<<grid_for(work), kThreads, 4 * lp.digits * sizeof(int), st>>>(
           ch, d, d_stride, ext, (long)lp.ext_rows * n, key, L + K, lp.dig_info, lp.digits, level,

@@ -97,6 +97,8 @@ template <class Tile, bool FWD, int IN, int OUT, bool STW>
 __global__ void __launch_bounds__(Tile::THREADS, Tile::MINB)
     ntt_tiles_fp_kernel(const DevChain ch, u64* dst, const u64* src, Tile tl, int ntiles) {
   extern __shared__ __align__(16) u64 smem_raw[];
+  fhe_pdl_trigger();
+  fhe_pdl_wait();
   constexpr int TWM = STW ? Tile::TWMAX : 0;
   double2* tw_raw = reinterpret_cast<double2*>(smem_raw + Tile::NBUF * Tile::SMEM_WORDS);
   // staged tables: [prime][fwd | inv][N]
@@ -126,7 +128,7 @@ __global__ void __launch_bounds__(Tile::THREADS, Tile::MINB)
       if (FWD)
         fwd_passes_fp<Tile::LOG_S, 0, IN, OUT, STW>(smem_raw, tw_raw, cur, dst, ch);
       else
-        inv_passes_fp<Tile::LOG_S, npass(Tile::LOG_S) - 1, IN, OUT, STW>(smem_raw, tw_raw, cur,
+        inv_passes_fp<Tile::LOG_S, npass(Tile::LOG_S, tile_maxe<Tile>::v) - 1, IN, OUT, STW>(smem_raw, tw_raw, cur,
                                                                           dst, ch);
       __syncthreads();
     }
@@ -162,7 +164,7 @@ __global__ void __launch_bounds__(Tile::THREADS, Tile::MINB)
       if (FWD)
         fwd_passes_fp<Tile::LOG_S, 0, IN, OUT, STW>(sm, tws, cur, dst, ch);
       else
-        inv_passes_fp<Tile::LOG_S, npass(Tile::LOG_S) - 1, IN, OUT, STW>(sm, tws, cur, dst, ch);
+        inv_passes_fp<Tile::LOG_S, npass(Tile::LOG_S, tile_maxe<Tile>::v) - 1, IN, OUT, STW>(sm, tws, cur, dst, ch);
     }
   }
 }
@@ -336,7 +338,7 @@ __global__ void __launch_bounds__(Tile::THREADS, Tile::MINB)
     if (FWD)
       fwd_passes_fp<Tile::LOG_S, 0, IN, OUT, true>(sm, tws, cur, nullptr, ch);
     else
-      inv_passes_fp<Tile::LOG_S, npass(Tile::LOG_S) - 1, IN, OUT, true>(sm, tws, cur, nullptr,
+      inv_passes_fp<Tile::LOG_S, npass(Tile::LOG_S, tile_maxe<Tile>::v) - 1, IN, OUT, true>(sm, tws, cur, nullptr,
                                                                         ch);
     __syncthreads();
   }
@@ -408,7 +410,7 @@ __device__ __forceinline__ void fused_run_tile(const DevChain& ch, Tile& tl, u64
     fwd_passes_fp<Tile::LOG_S, 0, Tile::COLS ? FPIN_U64 : FPIN_DOUBLE,
                   Tile::COLS ? FPOUT_DOUBLE : FPOUT_U64, true>(sm, tws, tl, dst, ch);
   else
-    inv_passes_fp<Tile::LOG_S, npass(Tile::LOG_S) - 1, Tile::COLS ? FPIN_DOUBLE : FPIN_U64,
+    inv_passes_fp<Tile::LOG_S, npass(Tile::LOG_S, tile_maxe<Tile>::v) - 1, Tile::COLS ? FPIN_DOUBLE : FPIN_U64,
                   Tile::COLS ? FPOUT_U64 : FPOUT_DOUBLE, true>(sm, tws, tl, dst, ch);
   __syncthreads();
 }
@@ -568,7 +570,7 @@ __global__ void __launch_bounds__(kSplitThreads, FHE_FUSE_CTAS)
           if (FWD)
             fwd_passes_fp<CT::LOG_S, 0, FPIN_U64, FPOUT_DOUBLE, true>(sm, tws, c, nullptr, ch);
           else
-            inv_passes_fp<CT::LOG_S, npass(CT::LOG_S) - 1, FPIN_DOUBLE, FPOUT_U64, true>(
+            inv_passes_fp<CT::LOG_S, npass(CT::LOG_S, tile_maxe<CT>::v) - 1, FPIN_DOUBLE, FPOUT_U64, true>(
                 sm, tws, c, nullptr, ch);
           work = true;
         }
@@ -591,7 +593,7 @@ __global__ void __launch_bounds__(kSplitThreads, FHE_FUSE_CTAS)
           if (FWD)
             fwd_passes_fp<KT::LOG_S, 0, FPIN_DOUBLE, FPOUT_U64, true>(sm, tws, k, nullptr, ch);
           else
-            inv_passes_fp<KT::LOG_S, npass(KT::LOG_S) - 1, FPIN_U64, FPOUT_DOUBLE, true>(
+            inv_passes_fp<KT::LOG_S, npass(KT::LOG_S, tile_maxe<KT>::v) - 1, FPIN_U64, FPOUT_DOUBLE, true>(
                 sm, tws, k, nullptr, ch);
           work = true;
         }
@@ -652,8 +654,8 @@ int launch_tiles_fp(const DevChain& ch, u64* dst, const u64* src, const Tile& tl
                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     attr = true;
   }
-  ntt_tiles_fp_kernel<Tile, FWD, IN, OUT, STW><<<grid, Tile::THREADS, smem, st>>>(ch, dst, src, tl,
-                                                                            ntiles);
+  fhe_launch(ntt_tiles_fp_kernel<Tile, FWD, IN, OUT, STW>, dim3(grid), dim3(Tile::THREADS), smem,
+             st, ch, dst, src, tl, ntiles);
   FHE_LAUNCH_CHECK();
   return 0;
 }

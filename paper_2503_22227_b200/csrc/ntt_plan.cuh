@@ -8,13 +8,14 @@
 
 // A local transform of 2^log_s points runs npass register passes of radix
 // 2^pass_e; pass p starts at local stage pass_r0.
-constexpr int npass(int log_s) { return (log_s + FHE_NTT_MAXE - 1) / FHE_NTT_MAXE; }
-constexpr int pass_e(int log_s, int p) {
-  return log_s / npass(log_s) + (p < log_s % npass(log_s) ? 1 : 0);
+// (maxe: largest pass radix exponent; tiles may lower it, see tile_maxe)
+constexpr int npass(int log_s, int maxe = FHE_NTT_MAXE) { return (log_s + maxe - 1) / maxe; }
+constexpr int pass_e(int log_s, int p, int maxe = FHE_NTT_MAXE) {
+  return log_s / npass(log_s, maxe) + (p < log_s % npass(log_s, maxe) ? 1 : 0);
 }
-constexpr int pass_r0(int log_s, int p) {
+constexpr int pass_r0(int log_s, int p, int maxe = FHE_NTT_MAXE) {
   int r = 0;
-  for (int i = 0; i < p; ++i) r += pass_e(log_s, i);
+  for (int i = 0; i < p; ++i) r += pass_e(log_s, i, maxe);
   return r;
 }
 

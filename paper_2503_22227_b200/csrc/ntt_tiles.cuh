@@ -7,7 +7,15 @@
 // Split (four-step) tiles: 2048 elements, 128 threads, 4 CTAs/SM -- small
 // CTAs keep the SM's FP64 pipe fed while other CTAs sit in their load /
 // barrier / store phases.
-constexpr int kRowThreads = 256;
+#include <type_traits>
+
+#ifndef FHE_ROW_THREADS
+#define FHE_ROW_THREADS 256
+#endif
+constexpr int kRowThreads = FHE_ROW_THREADS;
+#ifndef FHE_ROW_MAXE
+#define FHE_ROW_MAXE FHE_NTT_MAXE
+#endif
 constexpr int kLogRowTile = 12;
 constexpr int kSplitThreads = 128;
 constexpr int kLogSplitTile = 11;
@@ -150,6 +158,7 @@ struct RowsTile {
   static constexpr bool TMA = false;
   static constexpr bool SWZ = false;   // 128B-swizzled rows (TMA chunk tiles)
   static constexpr int THREADS = kRowThreads;
+  static constexpr int MAXE = FHE_ROW_MAXE;  // pass radix limit (tile_maxe)
   double center = 0.0;    // != 0: centred broadcast input (NttArgs::center_q)
   int bcast_limbs = 0;    // != 0: input row r is row r / bcast_limbs of src
   long bcast_stride = 0;  //        (bcast_stride words apart)
@@ -405,11 +414,23 @@ enum OutMode {
 // Every register pass of a LOG_S-stage local transform has the same radix and
 // at most 32 groups per array: with array-major thread mapping each array is
 // owned by one warp in every pass, so passes exchange data under __syncwarp.
-constexpr bool warp_local(int log_s) {
-  for (int p = 1; p < npass(log_s); ++p)
-    if (pass_e(log_s, p) != pass_e(log_s, 0)) return false;
-  return log_s - pass_e(log_s, 0) <= 5;
+constexpr bool warp_local(int log_s, int maxe = FHE_NTT_MAXE) {
+  for (int p = 1; p < npass(log_s, maxe); ++p)
+    if (pass_e(log_s, p, maxe) != pass_e(log_s, 0, maxe)) return false;
+  return log_s - pass_e(log_s, 0, maxe) <= 5;
 }
+
+// Pass radix limit of a tile type: Tile::MAXE when it declares one (the
+// latency-mode row tiles use smaller radices and more threads), else
+// FHE_NTT_MAXE.  FP64 passes only.
+template <class T, class = void>
+struct tile_maxe {
+  static constexpr int v = FHE_NTT_MAXE;
+};
+template <class T>
+struct tile_maxe<T, std::void_t<decltype(T::MAXE)>> {
+  static constexpr int v = T::MAXE;
+};
 
 // Copy a finished tile from shared memory to global memory in 16-byte pairs.
 //  * column tiles: CTA-wide (a k-row of 16 columns = 128 contiguous bytes);
@@ -667,9 +688,10 @@ __device__ __forceinline__ void run_pass_fp(u64* sm, const double2* tws, const T
   // results of the last pass go back to shared memory and leave in 16-byte
   // coalesced stores (no strided 8-byte STGs from the butterfly registers)
   constexpr bool EPI = Tile::EPI;
-  constexpr bool WL = warp_local(LOG_S) && !Tile::LANE_MAJOR;
+  constexpr int MX = tile_maxe<Tile>::v;
+  constexpr bool WL = warp_local(LOG_S, MX) && !Tile::LANE_MAJOR;
   // staged twiddles of the last pass are stored transposed (staged_perm)
-  constexpr bool TT = STW && R0 == pass_r0(LOG_S, npass(LOG_S) - 1) && TMIN_LOG == 0;
+  constexpr bool TT = STW && R0 == pass_r0(LOG_S, npass(LOG_S, MX) - 1, MX) && TMIN_LOG == 0;
   const int total = tl.arrays() << GPA_LOG;
   for (int G = threadIdx.x; G < total; G += blockDim.x) {
     int b, g;
@@ -839,13 +861,14 @@ __device__ __forceinline__ void run_pass_fp(u64* sm, const double2* tws, const T
 template <int LOG_S, int P, int IN, int OUT, bool STW, class Tile>
 __device__ __forceinline__ void fwd_passes_fp(u64* sm, const double2* tws, const Tile& tl,
                                               u64* gout, const DevChain& ch) {
-  constexpr int NP = npass(LOG_S);
+  constexpr int MX = tile_maxe<Tile>::v;
+  constexpr int NP = npass(LOG_S, MX);
   if constexpr (P < NP) {
     constexpr bool last = (P == NP - 1);
-    run_pass_fp<LOG_S, pass_r0(LOG_S, P), pass_e(LOG_S, P), true, P == 0, last, IN, OUT, STW>(
-        sm, tws, tl, gout, ch);
+    run_pass_fp<LOG_S, pass_r0(LOG_S, P, MX), pass_e(LOG_S, P, MX), true, P == 0, last, IN, OUT,
+                STW>(sm, tws, tl, gout, ch);
     if constexpr (!last) {
-      if constexpr (warp_local(LOG_S) && !Tile::LANE_MAJOR) __syncwarp(); else __syncthreads();
+      if constexpr (warp_local(LOG_S, MX) && !Tile::LANE_MAJOR) __syncwarp(); else __syncthreads();
       fwd_passes_fp<LOG_S, P + 1, IN, OUT, STW>(sm, tws, tl, gout, ch);
     }
   }
@@ -854,12 +877,13 @@ __device__ __forceinline__ void fwd_passes_fp(u64* sm, const double2* tws, const
 template <int LOG_S, int P, int IN, int OUT, bool STW, class Tile>
 __device__ __forceinline__ void inv_passes_fp(u64* sm, const double2* tws, const Tile& tl,
                                               u64* gout, const DevChain& ch) {
+  constexpr int MX = tile_maxe<Tile>::v;
   if constexpr (P >= 0) {
     constexpr bool last = (P == 0);
-    run_pass_fp<LOG_S, pass_r0(LOG_S, P), pass_e(LOG_S, P), false, P == npass(LOG_S) - 1, last,
-                IN, OUT, STW>(sm, tws, tl, gout, ch);
+    run_pass_fp<LOG_S, pass_r0(LOG_S, P, MX), pass_e(LOG_S, P, MX), false,
+                P == npass(LOG_S, MX) - 1, last, IN, OUT, STW>(sm, tws, tl, gout, ch);
     if constexpr (!last) {
-      if constexpr (warp_local(LOG_S) && !Tile::LANE_MAJOR) __syncwarp(); else __syncthreads();
+      if constexpr (warp_local(LOG_S, MX) && !Tile::LANE_MAJOR) __syncwarp(); else __syncthreads();
       inv_passes_fp<LOG_S, P - 1, IN, OUT, STW>(sm, tws, tl, gout, ch);
     }
   }

@@ -33,6 +33,8 @@ __global__ void __launch_bounds__(kThreads)
     ewise_kernel(const DevChain ch, int op, u64* __restrict__ out, const u64* __restrict__ a,
                  const u64* __restrict__ b, const u64* __restrict__ c, long rows, int log_n,
                  RowMap map, int b_mode) {
+  fhe_pdl_trigger();
+  fhe_pdl_wait();
   const long half_n = 1L << (log_n - 1);
   const long total = rows * half_n;
   for (long t = blockIdx.x * (long)blockDim.x + threadIdx.x; t < total;
@@ -70,6 +72,8 @@ __global__ void __launch_bounds__(kThreads)
     tensor_kernel(const DevChain ch, u64* __restrict__ out, const u64* __restrict__ x,
                   const u64* __restrict__ y, int limbs, int log_n, long batch, long x_stride,
                   long y_stride, long out_stride, int square) {
+  fhe_pdl_trigger();
+  fhe_pdl_wait();
   const long n = 1L << log_n;
   const long per = (long)limbs << (log_n - 1);  // coefficient pairs per ciphertext
   const long total = batch * per;
@@ -115,6 +119,8 @@ __global__ void __launch_bounds__(kThreads)
 __global__ void __launch_bounds__(kThreads)
     automorph_kernel(u64* __restrict__ out, const u64* __restrict__ in, long rows, int log_n,
                      u64 elt) {
+  fhe_pdl_trigger();
+  fhe_pdl_wait();
   const long n = 1L << log_n;
   const long total = rows * n;
   const u64 mask2n = (2UL << log_n) - 1;
@@ -140,6 +146,8 @@ __global__ void __launch_bounds__(kThreads)
                             const u64* __restrict__ last, int polys, int new_level, int log_n,
                             int last_prime, u64 t_plain, WPair tinv_last,
                             const u64* __restrict__ t_mod, const u64* __restrict__ qlast_mod) {
+  fhe_pdl_trigger();
+  fhe_pdl_wait();
   const long n = 1L << log_n;
   const long total = (long)polys * new_level * n;
   const u64 ql = ch.mc[last_prime].q;
@@ -171,6 +179,8 @@ __global__ void __launch_bounds__(kThreads)
     modswitch_finish_kernel(const DevChain ch, u64* __restrict__ out, const u64* __restrict__ in,
                             const u64* __restrict__ corr, int polys, int level, int log_n,
                             const WPair* __restrict__ inv) {
+  fhe_pdl_trigger();
+  fhe_pdl_wait();
   const int new_level = level - 1;
   const long n = 1L << log_n;
   const long half_n = n >> 1;
@@ -254,6 +264,15 @@ int launch_rescale_small(const DevChain& ch, u64* out, const u64* in, const u64*
   return 0;
 }
 
+bool fhe_pdl_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("FHE_PDL");
+    on = (e && e[0] == '1') ? 1 : 0;
+  }
+  return on == 1;
+}
+
 int grid_for(long work) {
   // enough CTAs for 8 resident per SM on 148 SMs, no more than the work needs
   long g = (work + kThreads - 1) / kThreads;
@@ -265,8 +284,8 @@ int launch_ewise(const DevChain& ch, int op, u64* out, const u64* a, const u64* 
                  long rows, RowMap map, int b_mode, cudaStream_t st) {
   if (rows <= 0) return 0;
   const long work = rows << (ch.log_n - 1);
-  ewise_kernel<<<grid_for(work), kThreads, 0, st>>>(ch, op, out, a, b, c, rows, ch.log_n, map,
-                                                   b_mode);
+  fhe_launch(ewise_kernel, dim3(grid_for(work)), dim3(kThreads), 0, st, ch, op, out, a, b, c, rows,
+             ch.log_n, map, b_mode);
   FHE_LAUNCH_CHECK();
   return 0;
 }
@@ -275,8 +294,8 @@ int launch_tensor(const DevChain& ch, u64* out, const u64* x, const u64* y, int 
                   long x_stride, long y_stride, long out_stride, int square, cudaStream_t st) {
   const long work = batch * ((long)limbs << (ch.log_n - 1));
   if (work <= 0) return 0;
-  tensor_kernel<<<grid_for(work), kThreads, 0, st>>>(ch, out, x, y, limbs, ch.log_n, batch,
-                                                    x_stride, y_stride, out_stride, square);
+  fhe_launch(tensor_kernel, dim3(grid_for(work)), dim3(kThreads), 0, st, ch, out, x, y, limbs,
+             ch.log_n, batch, x_stride, y_stride, out_stride, square);
   FHE_LAUNCH_CHECK();
   return 0;
 }
@@ -284,7 +303,8 @@ int launch_tensor(const DevChain& ch, u64* out, const u64* x, const u64* y, int 
 int launch_automorph(u64* out, const u64* in, long rows, int log_n, u64 elt, cudaStream_t st) {
   const long work = rows << log_n;
   if (work <= 0) return 0;
-  automorph_kernel<<<grid_for(work), kThreads, 0, st>>>(out, in, rows, log_n, elt);
+  fhe_launch(automorph_kernel, dim3(grid_for(work)), dim3(kThreads), 0, st, out, in, rows, log_n,
+             elt);
   FHE_LAUNCH_CHECK();
   return 0;
 }
@@ -293,9 +313,8 @@ int launch_modswitch_expand(const DevChain& ch, u64* corr, const u64* last, int 
                             int new_level, int last_prime, u64 t_plain, WPair tinv_last,
                             const u64* t_mod, const u64* qlast_mod, cudaStream_t st) {
   const long work = ((long)polys * new_level) << ch.log_n;
-  modswitch_expand_kernel<<<grid_for(work), kThreads, 0, st>>>(
-      ch, corr, last, polys, new_level, ch.log_n, last_prime, t_plain, tinv_last, t_mod,
-      qlast_mod);
+  fhe_launch(modswitch_expand_kernel, dim3(grid_for(work)), dim3(kThreads), 0, st, ch, corr, last,
+             polys, new_level, ch.log_n, last_prime, t_plain, tinv_last, t_mod, qlast_mod);
   FHE_LAUNCH_CHECK();
   return 0;
 }
@@ -303,8 +322,8 @@ int launch_modswitch_expand(const DevChain& ch, u64* corr, const u64* last, int 
 int launch_modswitch_finish(const DevChain& ch, u64* out, const u64* in, const u64* corr,
                             int polys, int level, const WPair* inv, cudaStream_t st) {
   const long work = ((long)polys * (level - 1)) << (ch.log_n - 1);
-  modswitch_finish_kernel<<<grid_for(work), kThreads, 0, st>>>(ch, out, in, corr, polys, level,
-                                                              ch.log_n, inv);
+  fhe_launch(modswitch_finish_kernel, dim3(grid_for(work)), dim3(kThreads), 0, st, ch, out, in,
+             corr, polys, level, ch.log_n, inv);
   FHE_LAUNCH_CHECK();
   return 0;
 }
