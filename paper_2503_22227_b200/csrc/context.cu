@@ -144,11 +144,12 @@ int build_chain(const u64* primes, int count, int log_n, FheChain* ch) {
   for (int p = 0; p < count; ++p) fp64 &= primes[p] < ((u64)1 << 50);
   std::vector<double2> twd, itwd, tws, qd(count), nid(count), nwd(count);
   // staged tables: per prime and direction N1 column pairs + N chunk pairs
-  const size_t tws_dir = log_n >= 13 ? n + ((size_t)1 << split_log_n1(log_n)) : 0;
+  // (N <= 2^12: the whole-row plan's table, n pairs per direction)
+  const size_t tws_dir = log_n >= 13 ? n + ((size_t)1 << split_log_n1(log_n)) : n;
   if (fp64) {
     twd.resize(count * n);
     itwd.resize(count * n);
-    if (log_n >= 13) tws.assign(count * 2 * tws_dir, make_double2(0.0, 0.0));
+    tws.assign(count * 2 * tws_dir, make_double2(0.0, 0.0));
     for (int p = 0; p < count; ++p) {
       const double q = (double)primes[p];
       // signed representatives |w| <= q/2: |x w / q| <= |x| / 2, so the FP64
@@ -180,6 +181,16 @@ int build_chain(const u64* primes, int count, int log_n, FheChain* ch) {
           for (int s = 0; s < ls; ++s)
             for (int j = 0; j < (1 << s); ++j)
               put(n1 + ck * s_ + (1u << s) + staged_perm(ls, s, j), ((n1 + ck) << s) + j);
+      } else {
+        // whole-row tiles (RowsTile, one row per tile at N = 2^12)
+        double2* f = &tws[p * 2 * tws_dir];
+        double2* iv = &tws[p * 2 * tws_dir + tws_dir];
+        for (int s = 0; s < log_n; ++s)
+          for (int j = 0; j < (1 << s); ++j) {
+            const size_t d = (1u << s) + staged_perm(log_n, s, j, FHE_ROW_MAXE);
+            f[d] = twd[p * n + (1u << s) + j];
+            iv[d] = itwd[p * n + (1u << s) + j];
+          }
       }
       nid[p] = sd(ninv[p].w);
       nwd[p] = sd(ninv_w1[p].w);
@@ -211,7 +222,7 @@ int build_chain(const u64* primes, int count, int log_n, FheChain* ch) {
   ch->dev.qd = fp64 ? (const double2*)(b + o_qd) : nullptr;
   ch->dev.ninv_d = fp64 ? (const double2*)(b + o_nid) : nullptr;
   ch->dev.ninv_w1_d = fp64 ? (const double2*)(b + o_nwd) : nullptr;
-  ch->dev.tws = (fp64 && log_n >= 13) ? (const double2*)(b + o_tws) : nullptr;
+  ch->dev.tws = fp64 ? (const double2*)(b + o_tws) : nullptr;
   ch->dev.tws_dir = (long)tws_dir;
   ch->dev.fuse = fuse_scratch_new(log_n);
   if (!ch->dev.fuse) {

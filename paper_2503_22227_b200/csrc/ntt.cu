@@ -522,6 +522,8 @@ __global__ void __launch_bounds__(kSplitThreads, FHE_FUSE_CTAS)
   const uint64_t pol_ld = (FHE_FUSE_L2HINT & 1) ? l2_policy_evict_first() : 0;
   const uint64_t pol_mid = (FHE_FUSE_L2HINT & 2) ? l2_policy_evict_last() : 0;
   const uint64_t pol_ld2 = (FHE_FUSE_L2HINT & 4) ? l2_policy_evict_first() : pol_ld;
+  // bit 4 -> second-phase (final) stores evict_first
+  const uint64_t pol_out = (FHE_FUSE_L2HINT & 16) ? l2_policy_evict_first() : 0;
   for (int cur = 0;; cur ^= 1) {
     const int t = s_tk[cur];
     if (t >= fp.total) break;
@@ -557,7 +559,7 @@ __global__ void __launch_bounds__(kSplitThreads, FHE_FUSE_CTAS)
           c.smap_p = &cs_map;
           c.dmap_p = &cd_map;
           c.ld_pol = first ? pol_ld : pol_ld2;
-          c.st_pol = first ? pol_mid : 0;
+          c.st_pol = first ? pol_mid : pol_out;
           c.setup(row * CT::TILES + jb);
           if (threadIdx.x == 0) {
             const unsigned twb = c.tw_pairs() * sizeof(double2);
@@ -579,7 +581,7 @@ __global__ void __launch_bounds__(kSplitThreads, FHE_FUSE_CTAS)
         k.smap_p = &ks_map;
         k.dmap_p = &kd_map;
         k.ld_pol = first ? pol_ld : pol_ld2;
-        k.st_pol = first ? pol_mid : 0;
+        k.st_pol = first ? pol_mid : pol_out;
         k.setup(g * fp.k_per_g + idx);
         if (k.valid) {
           if (threadIdx.x == 0) {
@@ -969,6 +971,16 @@ int launch_cols_tma(const DevChain& ch, u64* dst, const u64* src, const Tile& tl
   return 0;
 }
 
+// whole-row tiles with staged twiddles (FHE_NTT_ROWS_STW=0 reads them through L1)
+bool rows_stw_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("FHE_NTT_ROWS_STW");
+    on = (e && e[0] == '0') ? 0 : 1;
+  }
+  return on == 1;
+}
+
 template <int LOG_N>
 int launch_rows(const DevChain& ch, const NttArgs& a, bool inverse, bool lazy, cudaStream_t st) {
   using T = RowsTile<LOG_N>;
@@ -992,6 +1004,12 @@ int launch_rows(const DevChain& ch, const NttArgs& a, bool inverse, bool lazy, c
     return rc;
   }
   path_hit(ch.fp64_ok ? FHE_NTT_PATH_ROWS : FHE_NTT_PATH_INT);
+  // staged twiddles take 64 KB of shared memory (1 CTA/SM): for launches of at
+  // most one row per SM, where latency, not occupancy, sets the time
+  if (ch.fp64_ok && T::TWMAX > 0 && ch.tws && a.rows <= sm_count() && rows_stw_enabled())
+    return inverse
+               ? launch_tiles_fp<T, false, FPIN_U64, FPOUT_U64, true>(ch, a.dst, a.src, tl, ntiles, st)
+               : launch_tiles_fp<T, true, FPIN_U64, FPOUT_U64, true>(ch, a.dst, a.src, tl, ntiles, st);
   if (ch.fp64_ok)
     return inverse ? launch_tiles_fp<T, false, FPIN_U64, FPOUT_U64>(ch, a.dst, a.src, tl, ntiles, st)
                    : launch_tiles_fp<T, true, FPIN_U64, FPOUT_U64>(ch, a.dst, a.src, tl, ntiles, st);

@@ -5,6 +5,10 @@
 #ifndef FHE_NTT_MAXE
 #define FHE_NTT_MAXE 5
 #endif
+// pass radix limit of the whole-row tiles (ntt_tiles.cuh RowsTile)
+#ifndef FHE_ROW_MAXE
+#define FHE_ROW_MAXE FHE_NTT_MAXE
+#endif
 
 // A local transform of 2^log_s points runs npass register passes of radix
 // 2^pass_e; pass p starts at local stage pass_r0.
@@ -27,8 +31,8 @@ constexpr int split_log_n1(int log_n) { return log_n >= 16 ? 8 : (log_n >= 14 ? 
 // register pass (s >= p_last) hold pair j = (g << rr) | blk (rr = s - p_last,
 // g the thread's group) at (blk << p_last) | g, so the groups of a warp read
 // consecutive pairs.
-constexpr int staged_perm(int log_s, int s, int j) {
-  const int pl = pass_r0(log_s, npass(log_s) - 1);
+constexpr int staged_perm(int log_s, int s, int j, int maxe = FHE_NTT_MAXE) {
+  const int pl = pass_r0(log_s, npass(log_s, maxe) - 1, maxe);
   if (s < pl) return j;
   const int rr = s - pl;
   return ((j & ((1 << rr) - 1)) << pl) | (j >> rr);

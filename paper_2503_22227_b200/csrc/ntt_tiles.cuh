@@ -13,9 +13,6 @@
 #define FHE_ROW_THREADS 256
 #endif
 constexpr int kRowThreads = FHE_ROW_THREADS;
-#ifndef FHE_ROW_MAXE
-#define FHE_ROW_MAXE FHE_NTT_MAXE
-#endif
 constexpr int kLogRowTile = 12;
 constexpr int kSplitThreads = 128;
 constexpr int kLogSplitTile = 11;
@@ -200,12 +197,15 @@ struct RowsTile {
     return ArrCtx{(fwd ? ch.tw : ch.itw) + ((size_t)p << LOG_N), ch.mc[p].q, 1, p, !fwd};
   }
   __device__ __forceinline__ int arrays() const { return nb; }
-  // rows of a tile may use different primes: twiddles are read through L1
-  static constexpr int TWMAX = 0;
-  __device__ __forceinline__ int tw_pairs() const { return 0; }
+  // one row per tile (N = 2^12): the prime's whole staged table (S pairs, in
+  // the row plan's staged_perm order, context.cu) can be staged in shared
+  // memory with the row, so no pass waits on an L2 twiddle read (STW launch);
+  // several rows per tile may use different primes: twiddles through L1
+  static constexpr int TWMAX = NB == 1 ? S : 0;
+  __device__ __forceinline__ int tw_pairs() const { return NB == 1 ? S : 0; }
   __device__ __forceinline__ long tw_src_off() const { return 0; }
-  __device__ __forceinline__ int tw_base(int, int) const { return 0; }
-  __device__ __forceinline__ int tw_prime() const { return 0; }
+  __device__ __forceinline__ int tw_base(int s, int) const { return 1 << s; }
+  __device__ __forceinline__ int tw_prime() const { return prime[0]; }
 };
 
 // First log N1 stages on a [N1][CN] column tile of one row (CN = 2048 / N1

@@ -28,6 +28,31 @@ def main():
     ch.transform(z, 26, True, limbs=13, offset=0)
     assert torch.equal(z, x), "round trip"
     print("fwd digest", hashlib.sha256(y.cpu().numpy().tobytes()).hexdigest()[:16])
+    # graph-node floor: a trivial kernel (automorphism of one row), same harness
+    from paper_2503_22227_b200 import _native
+    lib = _native.lib()
+    a1 = torch.randint(0, 1 << 40, (1, n), dtype=torch.int64, device="cuda")
+    b1 = torch.empty_like(a1)
+    triv = lambda: lib.fhe_automorph(b1.data_ptr(), a1.data_ptr(), 1, 12, 3,  # noqa: E731
+                                     _native.stream_handle())
+    for _ in range(5):
+        triv()
+    g = torch.cuda.CUDAGraph()
+    st = torch.cuda.Stream()
+    st.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(st):
+        with torch.cuda.graph(g, stream=st):
+            for _ in range(reps):
+                triv()
+    g.replay()
+    torch.cuda.synchronize()
+    s0, e0 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s0.record()
+    g.replay()
+    e0.record()
+    e0.synchronize()
+    print(f"trivial kernel (1-row automorphism): graph {s0.elapsed_time(e0) * 1e3 / reps:6.2f} us "
+          f"per launch")
     for rows in (1, 2, 13, 26, 169):
         buf = torch.randint(0, 1 << 40, (rows, n), dtype=torch.int64, device="cuda")
         out = torch.empty_like(buf)
