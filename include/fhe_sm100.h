@@ -68,7 +68,7 @@ enum {
   FHE_NTT_PATH_FUSED_TMA = 2, /* four-step, one ticketed kernel on TMA tiles      */
   FHE_NTT_PATH_FUSED_CP = 3,  /* four-step, one ticketed kernel on cp.async tiles */
   FHE_NTT_PATH_INT = 4,       /* 64-bit integer pipe (a prime >= 2^50)            */
-  FHE_NTT_PATH_CLUSTER = 5,   /* one pass, row held by a CTA cluster (DSMEM)      */
+  FHE_NTT_PATH_CLUSTER = 5,   /* row held by a CTA cluster (DSMEM): N = 2^12 small launches, N = 2^16 opt-in */
   FHE_NTT_PATH_MM = 6,        /* matrix-product variant (fhe_ntt_mm)              */
   FHE_NTT_PATHS = 8
 };

@@ -832,6 +832,7 @@ bool chunks_tensor_map(CUtensorMap* m, const u64* base, int log_n, int log_s, in
 }
 
 #include "ntt_cluster.cuh"
+#include "ntt_row_cluster.cuh"
 
 template <class Tile, bool FWD, int IN, int OUT>
 int launch_chunks_tma(const DevChain& ch, u64* dst, const u64* src, const Tile& tl, int ntiles,
@@ -971,6 +972,22 @@ int launch_cols_tma(const DevChain& ch, u64* dst, const u64* src, const Tile& tl
   return 0;
 }
 
+// N = 2^12 rows on 4-CTA clusters (FHE_NTT_ROW_CLUSTER=0: whole-row tiles)
+// (up to FHE_ROW_CLUSTER_PER_SM rows per SM: 1 row 6.4 -> 3.4 us, 169 rows
+// 11.8 -> 11.0 us, but 1600 rows 61 -> 86 us, tools/small_ntt_time.py and
+// tools/ntt_bench.py 12 40 20)
+#ifndef FHE_ROW_CLUSTER_PER_SM
+#define FHE_ROW_CLUSTER_PER_SM 2
+#endif
+bool row_cluster_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("FHE_NTT_ROW_CLUSTER");
+    on = (e && e[0] == '0') ? 0 : 1;
+  }
+  return on == 1;
+}
+
 // whole-row tiles with staged twiddles (FHE_NTT_ROWS_STW=0 reads them through L1)
 bool rows_stw_enabled() {
   static int on = -1;
@@ -1002,6 +1019,21 @@ int launch_rows(const DevChain& ch, const NttArgs& a, bool inverse, bool lazy, c
     const int rc = launch_tiles_fp<T, true, FPIN_U64, FPOUT_U64>(ch, a.dst, a.bcast_src, tl, ntiles, st);
     if (!rc && a.bcast_done) *a.bcast_done = true;
     return rc;
+  }
+  if constexpr (LOG_N == 12) {
+    // one row per 4-CTA cluster (ntt_row_cluster.cuh) for launches of a few
+    // rows per SM, where the per-row latency sets the time
+    if (ch.fp64_ok && a.rows <= FHE_ROW_CLUSTER_PER_SM * sm_count() && row_cluster_enabled()) {
+      path_hit(FHE_NTT_PATH_CLUSTER);
+      if (inverse)
+        ntt_row_cluster_kernel<false><<<a.rows * 4, kRcThreads, 0, st>>>(ch, a.dst, a.src, a.map,
+                                                                          tl.src, tl.dst);
+      else
+        ntt_row_cluster_kernel<true><<<a.rows * 4, kRcThreads, 0, st>>>(ch, a.dst, a.src, a.map,
+                                                                         tl.src, tl.dst);
+      FHE_LAUNCH_CHECK();
+      return 0;
+    }
   }
   path_hit(ch.fp64_ok ? FHE_NTT_PATH_ROWS : FHE_NTT_PATH_INT);
   // staged twiddles take 64 KB of shared memory (1 CTA/SM): for launches of at
