@@ -1015,6 +1015,17 @@ int launch_rows(const DevChain& ch, const NttArgs& a, bool inverse, bool lazy, c
     tl.bcast_limbs = a.map.limbs;
     tl.bcast_stride = a.bcast_stride;
     tl.center = (double)a.center_q;
+    if constexpr (LOG_N == 12) {
+      if (a.rows <= FHE_ROW_CLUSTER_PER_SM * sm_count() && row_cluster_enabled()) {
+        path_hit(FHE_NTT_PATH_CLUSTER);
+        ntt_row_cluster_kernel<true><<<a.rows * 4, kRcThreads, 0, st>>>(
+            ch, a.dst, a.bcast_src, a.map, tl.src, tl.dst, a.map.limbs, a.bcast_stride,
+            (double)a.center_q);
+        FHE_LAUNCH_CHECK();
+        if (a.bcast_done) *a.bcast_done = true;
+        return 0;
+      }
+    }
     path_hit(FHE_NTT_PATH_ROWS);
     const int rc = launch_tiles_fp<T, true, FPIN_U64, FPOUT_U64>(ch, a.dst, a.bcast_src, tl, ntiles, st);
     if (!rc && a.bcast_done) *a.bcast_done = true;
@@ -1026,11 +1037,11 @@ int launch_rows(const DevChain& ch, const NttArgs& a, bool inverse, bool lazy, c
     if (ch.fp64_ok && a.rows <= FHE_ROW_CLUSTER_PER_SM * sm_count() && row_cluster_enabled()) {
       path_hit(FHE_NTT_PATH_CLUSTER);
       if (inverse)
-        ntt_row_cluster_kernel<false><<<a.rows * 4, kRcThreads, 0, st>>>(ch, a.dst, a.src, a.map,
-                                                                          tl.src, tl.dst);
+        ntt_row_cluster_kernel<false><<<a.rows * 4, kRcThreads, 0, st>>>(
+            ch, a.dst, a.src, a.map, tl.src, tl.dst, 0, 0L, 0.0);
       else
-        ntt_row_cluster_kernel<true><<<a.rows * 4, kRcThreads, 0, st>>>(ch, a.dst, a.src, a.map,
-                                                                         tl.src, tl.dst);
+        ntt_row_cluster_kernel<true><<<a.rows * 4, kRcThreads, 0, st>>>(
+            ch, a.dst, a.src, a.map, tl.src, tl.dst, 0, 0L, 0.0);
       FHE_LAUNCH_CHECK();
       return 0;
     }

@@ -66,7 +66,7 @@ __device__ __forceinline__ void rc_inv_bf(double& a, double& c, double2 w, doubl
 template <bool FWD>
 __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kRcThreads)
     ntt_row_cluster_kernel(const DevChain ch, u64* dst, const u64* src, RowMap map, RowAddr sa,
-                           RowAddr da) {
+                           RowAddr da, int bcast_limbs, long bcast_stride, double center) {
   __shared__ double blk[1024];   // this CTA's 1024-point block (phase B)
   __shared__ double xch[1024];   // inverse: the 4 x 256 cross-block values (phase A)
   const int row = blockIdx.x >> 2;
@@ -89,14 +89,19 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kRcThreads)
     wc[i] = __ldg(tw + (1 << (t1 + 2)) + ((int)k << t1) + 2 * g0 + 1);
   }
   const double2 w0 = __ldg(tw + 1), w1a = __ldg(tw + 2), w1b = __ldg(tw + 3);
-  const u64* s_row = src + sa(row);
+  // broadcast input (forward only): row r reads row r / bcast_limbs of src,
+  // centred about `center` when nonzero (the rescale correction, as RowsTile)
+  const u64* s_row = bcast_limbs ? src + (long)(row / bcast_limbs) * bcast_stride : src + sa(row);
   u64* d_row = dst + da(row);
   if (FWD) {
     // ---- A: stages 0, 1 across the blocks
     const int pos = 256 * (int)k + t;
     double x[4];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) x[j] = fp_from_u52(s_row[pos + 1024 * j]);
+    for (int j = 0; j < 4; ++j) {
+      x[j] = fp_from_u52(s_row[pos + 1024 * j]);
+      if (center != 0.0) x[j] = x[j] > 0.5 * center ? __dadd_rn(x[j], -center) : x[j];
+    }
     rc_fwd_bf(x[0], x[2], w0, qd, 0);
     rc_fwd_bf(x[1], x[3], w0, qd, 0);
     rc_fwd_bf(x[0], x[1], w1a, qd, 1);
