@@ -974,10 +974,10 @@ int launch_cols_tma(const DevChain& ch, u64* dst, const u64* src, const Tile& tl
 
 // N = 2^12 rows on 4-CTA clusters (FHE_NTT_ROW_CLUSTER=0: whole-row tiles)
 // (up to FHE_ROW_CLUSTER_PER_SM rows per SM: 1 row 6.4 -> 3.4 us, 169 rows
-// 11.8 -> 11.0 us, but 1600 rows 61 -> 86 us, tools/small_ntt_time.py and
-// tools/ntt_bench.py 12 40 20)
+// 11.8 -> 11.0 us, 312 rows 24 -> 20 us, but 676 rows 33 -> 38 us and 1600
+// rows 61 -> 86 us; tools/small_ntt_time.py, tools/ntt_bench.py 12 13 26)
 #ifndef FHE_ROW_CLUSTER_PER_SM
-#define FHE_ROW_CLUSTER_PER_SM 2
+#define FHE_ROW_CLUSTER_PER_SM 3
 #endif
 bool row_cluster_enabled() {
   static int on = -1;
