@@ -283,9 +283,11 @@ def hmult_relin_step(w, batch: int):
 
 # FP64-pipe work of one config-4 HMult+Relin (hybrid dnum=3), lane-operations,
 # counted from the kernels (profiles/r1_ntt_notes.md):
-# 150 forward + 50 inverse N=2^16 limb NTTs, ModUp / ModDown base conversions,
-# key inner product.
-FP64_OPS_PER_HMULT = 150 * 4.98e6 + 50 * 5.5e6 + 476e6 + 136e6 + 317e6
+# 150 forward + 50 inverse N=2^16 limb NTTs, the base conversions' FP64
+# prologue (y = x inv mod q: ~9 FP64 ops per source word, 40 ModUp + 2 x 10
+# ModDown source rows; the contraction itself runs on tcgen05, round 2), key
+# inner product + finish.
+FP64_OPS_PER_HMULT = 150 * 4.98e6 + 50 * 5.5e6 + 9 * 65536 * (40 + 20) + 317e6
 DFMA_PER_CLK_PER_SM = 57.9  # measured, profiles/r1_microbench_pipes.txt
 
 
@@ -294,7 +296,8 @@ def fp64_bound(ops_s: float, sm_mhz: float | None, sms: int = 148) -> dict:
     bound = peak / FP64_OPS_PER_HMULT
     return {"fp64_lane_ops_per_op": FP64_OPS_PER_HMULT, "peak_lane_ops_s": peak,
             "bound_ops_s": bound, "frac": ops_s / bound,
-            "note": "HMult+Relin is FP64-pipe bound (200 limb NTTs + base conversions per op); "
+            "note": "FP64 work per op: 200 limb NTTs, the key inner product / finish and the "
+                    "base conversions' prologue (their contraction is on the tensor cores); "
                     "the HBM bound of 420*B per op is ~3.4x higher"}
 
 
