@@ -22,6 +22,11 @@ from paper_2503_22227_b200.schemes import ckks  # noqa: E402
 
 which = sys.argv[1] if len(sys.argv) > 1 else "all"
 n = 1 << 16
+# ks_tc: digits of >= 4 limbs and K >= 4, so ModUp / ModDown run on the tcgen05
+# conversion (csrc/bconv_umma.cuh) and the finish on the staged kernel;
+# ntt12: the N=2^12 row-per-cluster NTT (plain rows and the rescale
+# correction's broadcast input)
+KS_SHAPE = {"ks": (6, 2), "ks_tc": (12, 4)}
 if which in ("all", "ntt"):
     L, rows = 2, 16
     primes = [m.value for m in gen_ntt_prime_chain(50, n, L)]
@@ -36,9 +41,31 @@ if which in ("all", "ntt"):
     torch.cuda.synchronize()
     assert torch.equal(a, b), "NTT round trip"
     print("ntt paths", {k: v - p0[k] for k, v in _native.ntt_path_counts().items() if v != p0[k]})
-if which in ("all", "ks"):
-    ctx = Context(hybrid_params(n, 6, special=2, dnum=3, scale=float(2 ** 49)),
-                  PoolConfig(unit_mb=64, cap_mb=1024))
+if which in ("ntt12",):
+    from paper_2503_22227_b200.context import params_for_profile, Scheme
+    n12 = 1 << 12
+    primes = [m.value for m in gen_ntt_prime_chain(45, n12, 13)]
+    ch = DeviceChain(primes, 12)
+    a = torch.randint(0, 1 << 44, (13, n12), dtype=torch.int64, device="cuda")
+    b = a.clone()
+    p0 = _native.ntt_path_counts()
+    ch.transform(b, 13, False, limbs=13, offset=0)
+    ch.transform(b, 13, True, limbs=13, offset=0)
+    torch.cuda.synchronize()
+    assert torch.equal(a, b), "N=2^12 NTT round trip"
+    ctx = Context(params_for_profile("pdq", Scheme.CKKS), PoolConfig(unit_mb=64, cap_mb=512))
+    sk = keygen(ctx, Rng((1).to_bytes(32, "little")))
+    pk = pk_gen(ctx, sk, Rng((2).to_bytes(32, "little")))
+    x = np.random.default_rng(1).uniform(-1, 1, n12 // 2)
+    cx = ckks.ckks_encrypt(ctx, ckks.ckks_encode(ctx, x), pk, Rng((3).to_bytes(32, "little")))
+    r = ckks.ckks_rescale(ctx, ckks.ckks_multiply_scalar(ctx, cx, 1.0, scale=float(ctx.q_values[-1])))
+    torch.cuda.synchronize()
+    print("ntt paths", {k: v - p0[k] for k, v in _native.ntt_path_counts().items() if v != p0[k]},
+          "rescale level", r.level)
+if which in ("all", "ks", "ks_tc"):
+    Lk, Kk = KS_SHAPE.get(which, KS_SHAPE["ks"])
+    ctx = Context(hybrid_params(n, Lk, special=Kk, dnum=3, scale=float(2 ** 49)),
+                  PoolConfig(unit_mb=64, cap_mb=2048))
     seed = lambda s: Rng(int(s).to_bytes(32, "little"))  # noqa: E731
     sk = keygen(ctx, seed(1))
     pk = pk_gen(ctx, sk, seed(2))
