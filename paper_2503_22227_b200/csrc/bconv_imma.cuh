@@ -78,16 +78,15 @@ struct BconvArgs {
 // most 2 (V / p - qe < V / 2^71 + 2^sh / p + 1 < 3), so V - qe p < 3p and two
 // conditional subtractions give the canonical residue.  Only the low 64 bits
 // of qe p are needed (the remainder is < 2^58).
-struct __align__(16) BcTarget {  // 32 bytes: keeps the smem regions after it 16-byte aligned
+struct __align__(16) BcTarget {  // 16 bytes: one LDS.128; keeps the smem regions after it aligned
   u64 p;
-  u64 mu;
+  u32 mu;  // floor(2^71 / p) < 2^32 (p >= 2^39)
   u32 sh;
-  u32 pad[3];
 };
 
 __device__ __forceinline__ u64 bc_reduce71(u64 hi, u64 lo, const BcTarget& tg) {
   const u64 x = (hi << (64 - tg.sh)) | (lo >> tg.sh);  // V >> sh (hi < 2^7, sh >= 39)
-  const u64 qe = (x * tg.mu) >> (71 - tg.sh);
+  const u64 qe = (x * (u64)tg.mu) >> (71 - tg.sh);
   u64 r = lo - qe * tg.p;
   r = csub(r, tg.p);
   return csub(r, tg.p);
@@ -112,7 +111,7 @@ __device__ __forceinline__ u64 bc_combine71(unsigned a0, unsigned a1, unsigned a
       : "=r"(lo_hi), "=r"(hi)
       : "r"((unsigned)(v >> 32)), "r"((unsigned)h), "r"((unsigned)(h >> 32)));
   const unsigned x = __funnelshift_r(lo_hi, hi, tg.sh - 32);
-  const u64 prod = (u64)x * (unsigned)tg.mu;
+  const u64 prod = (u64)x * tg.mu;
   const unsigned qe = __funnelshift_rc((unsigned)prod, (unsigned)(prod >> 32), 71 - tg.sh);
   const u64 lo = ((u64)lo_hi << 32) | (unsigned)v;
   u64 r = lo - (u64)qe * tg.p;
@@ -159,7 +158,7 @@ __global__ void __launch_bounds__(kBcThreads, FHE_BCONV_MINB)
     const ModConst m = ch.mc[a.tgt_prime ? a.tgt_prime[row_off + t] : t];
     const u32 sh = m.s;  // bitlen(p) - 1
     // mu = floor(2^71 / p) = floor(2^(64+sh) / p) >> (sh - 7) = m.mu >> (sh - 7)
-    tgs[t] = BcTarget{m.q, m.mu >> (sh - 7), sh, {0, 0, 0}};
+    tgs[t] = BcTarget{m.q, (u32)(m.mu >> (sh - 7)), sh};
   }
   for (int s = threadIdx.x; s < SMAX; s += blockDim.x) {
     if (s < ns) {
@@ -309,9 +308,9 @@ __global__ void __launch_bounds__(kBcThreads, FHE_BCONV_MINB)
   for (int t = threadIdx.x; t < 8 * ng; t += blockDim.x) {
     if (t < nt) {
       const ModConst m = ch.mc[a.tgt_prime ? a.tgt_prime[row_off + t] : t];
-      tgs[t] = BcTarget{m.q, m.mu >> (m.s - 7), m.s, {0, 0, 0}};
+      tgs[t] = BcTarget{m.q, (u32)(m.mu >> (m.s - 7)), (u32)m.s};
     } else {
-      tgs[t] = BcTarget{1, 0, 39, {0, 0, 0}};  // padding target (never stored)
+      tgs[t] = BcTarget{1, 0, 39};  // padding target (never stored)
     }
   }
   for (int s = threadIdx.x; s < SMAX; s += blockDim.x) {

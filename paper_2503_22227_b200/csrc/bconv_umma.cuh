@@ -100,9 +100,9 @@ __global__ void __launch_bounds__(kBuThreads, FHE_BU_MINB)
   for (int t = tid; t < ng; t += kBuThreads) {
     if (t < nt) {
       const ModConst m = ch.mc[a.tgt_prime ? a.tgt_prime[row_off + t] : t];
-      tgs[t] = BcTarget{m.q, m.mu >> (m.s - 7), m.s, {0, 0, 0}};
+      tgs[t] = BcTarget{m.q, (u32)(m.mu >> (m.s - 7)), (u32)m.s};
     } else {
-      tgs[t] = BcTarget{1, 0, 39, {0, 0, 0}};
+      tgs[t] = BcTarget{1, 0, 39};
     }
   }
   for (int s = tid; s < SMAX; s += kBuThreads) {
@@ -198,12 +198,16 @@ __global__ void __launch_bounds__(kBuThreads, FHE_BU_MINB)
         tmem_ld_wait();
         umma_fence_before();
         umma_mbar_arrive(&t_empty[b]);
+        const int tb = j * kBuT + h * TH;
+        u64* o = dst + ((long)tb << ch.log_n) + c;
 #pragma unroll
         for (int tl = 0; tl < TH; ++tl) {
-          const int t = j * kBuT + h * TH + tl;
-          if (t < nt)
-            dst[(long)t * n + c] = bc_combine71(r[tl][0], r[tl][1], r[tl][2], r[tl][3],
-                                                r[tl][4], r[tl][5], r[tl][6], tgs[t]);
+          if (tb + tl < nt) {
+            const BcTarget tg = tgs[tb + tl];  // one LDS.128
+            *o = bc_combine71(r[tl][0], r[tl][1], r[tl][2], r[tl][3], r[tl][4], r[tl][5],
+                              r[tl][6], tg);
+          }
+          o += n;
         }
       }
     }
