@@ -794,6 +794,76 @@ __global__ void __launch_bounds__(kThreads, FHE_FINS_MINB)
   }
 }
 
+// P-limb key inner product of the fused path (m in [level, level + K): no
+// digit owns a P limb, every term reads ext), writing accP for the ModDown
+// conversion -- the staged counterpart of ks_inner_fp_kernel<kD> over those
+// limbs: the D words of batch item b + ST - 1 are in flight (cp.async into
+// this thread's slots) while item b computes.  Same arithmetic, same words.
+template <int kD>
+__global__ void __launch_bounds__(kThreads, FHE_FINS_MINB)
+    ks_plimb_staged_kernel(const DevChain ch, const u64* __restrict__ ext, long ext_stride,
+                           const u64* __restrict__ key, int keyL,
+                           const int* __restrict__ dig_info, int D, int level, int K, int L,
+                           u64* __restrict__ accP, int batch) {
+  constexpr int ST = FHE_FIN_STAGES;
+  extern __shared__ __align__(16) unsigned char psm[];
+  int* sinfo = reinterpret_cast<int*>(psm);
+  u64* stage = reinterpret_cast<u64*>(psm + 64);
+  if (threadIdx.x < 4 * D) sinfo[threadIdx.x] = dig_info[threadIdx.x];
+  __syncthreads();
+  const int log_n = ch.log_n;
+  const long n = 1L << log_n;
+  const long total = (long)K << log_n;
+  auto slot = [&](int s, int w) { return stage + ((long)(s * kD + w) * kThreads + threadIdx.x); };
+  for (long t = blockIdx.x * (long)blockDim.x + threadIdx.x; t < total;
+       t += (long)gridDim.x * blockDim.x) {
+    const int k = (int)(t >> log_n);
+    const int m = level + k, p = L + k;
+    const long i = t & (n - 1);
+    const double2 qd = ch.qd[p];
+    const u64* src[kD];
+#pragma unroll
+    for (int di = 0; di < kD; ++di)
+      if (di < D) src[di] = ext + (long)(sinfo[4 * di + 2] + m - sinfo[4 * di + 1]) * n + i;
+    auto issue = [&](int b) {
+      if (b < batch) {
+#pragma unroll
+        for (int di = 0; di < kD; ++di)
+          if (di < D) ks_cp8(slot(b % ST, di), src[di] + b * ext_stride);
+      }
+      ks_cp_commit();
+    };
+#pragma unroll
+    for (int s = 0; s < ST - 1; ++s) issue(s);
+    double2 kb[kD], ka[kD];
+#pragma unroll
+    for (int di = 0; di < kD; ++di) {
+      if (di < D) {
+        const double b = fp_from_u52(__ldg(key + ((long)(2 * di) * keyL + p) * n + i));
+        const double a = fp_from_u52(__ldg(key + ((long)(2 * di + 1) * keyL + p) * n + i));
+        kb[di] = make_double2(b, __dmul_rn(b, qd.y));
+        ka[di] = make_double2(a, __dmul_rn(a, qd.y));
+      }
+    }
+    for (int b = 0; b < batch; ++b) {
+      issue(b + ST - 1);
+      ks_cp_wait<ST - 1>();
+      double sb = 0.0, sa = 0.0;
+#pragma unroll
+      for (int di = 0; di < kD; ++di) {
+        if (di < D) {
+          const double x = fp_from_u52(*slot(b % ST, di));
+          sb = __dadd_rn(sb, fp_mulmod(x, kb[di], qd.x));
+          sa = __dadd_rn(sa, fp_mulmod(x, ka[di], qd.x));
+        }
+      }
+      accP[((long)(b * 2 + 0) * K + k) * n + i] = fp_canon_half(fp_reduce(sb, qd), qd.x);
+      accP[((long)(b * 2 + 1) * K + k) * n + i] = fp_canon_half(fp_reduce(sa, qd), qd.x);
+    }
+    ks_cp_wait<0>();
+  }
+}
+
 // FP64 key inner product for many digits (the reference's per-prime gadget,
 // alpha = 1, D = level digits): digits stream through one accumulator pair
 // per output, reduced every 8 terms (|sum| <= 8 * 0.75p + p < 2^53).
@@ -1064,13 +1134,24 @@ int run_keyswitch(const FheContext& ctx, int level, const u64* d, long d_stride,
   {
     const int m_end = level + K, m_begin = fin_inner ? level : 0;
     const long work = (long)(m_end - m_begin) << log_n;
+    auto go_p = [&](auto kern, int kd) {
+      const size_t sm = 64 + (size_t)FHE_FIN_STAGES * kd * kThreads * sizeof(u64);
+      if (sm > 48 * 1024)
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      kern<<<grid_for(work), kThreads, sm, st>>>(ch, ext, (long)lp.ext_rows * n, key, L + K,
+                                                 lp.dig_info, lp.digits, level, K, L, accP, batch);
+    };
     auto go = [&](auto kern) {
       kern<<<grid_for(work), kThreads, 4 * lp.digits * sizeof(int), st>>>(
           ch, d, d_stride, ext, (long)lp.ext_rows * n, key, L + K, lp.dig_info, lp.digits, level,
           K, L, accQ, accP, add0, add1, add_stride, out0, out1, out_stride, batch, m_begin, m_end,
           nullptr, nullptr);
     };
-    if (ch.fp64_ok && lp.digits <= 2)
+    if (fin_inner && ch.fp64_ok && lp.digits <= 4 && fin_staged_enabled()) {
+      if (lp.digits <= 2) go_p(ks_plimb_staged_kernel<2>, 2);
+      else if (lp.digits == 3) go_p(ks_plimb_staged_kernel<3>, 3);
+      else go_p(ks_plimb_staged_kernel<4>, 4);
+    } else if (ch.fp64_ok && lp.digits <= 2)
       go(ks_inner_fp_kernel<2>);
     else if (ch.fp64_ok && lp.digits == 3)
       go(ks_inner_fp_kernel<3>);
