@@ -649,6 +649,10 @@ __device__ __forceinline__ void ks_cp_wait() {
 #ifndef FHE_FIN_STAGES
 #define FHE_FIN_STAGES 4
 #endif
+// the staged finish's ModDown step on the FP64 pipe (0: integer Shoup form)
+#ifndef FHE_FIN_FP
+#define FHE_FIN_FP 1
+#endif
 #ifndef FHE_FINS_MINB
 #define FHE_FINS_MINB 3
 #endif
@@ -670,7 +674,7 @@ __global__ void __launch_bounds__(kThreads, FHE_FINS_MINB)
                          int keyL, const int* __restrict__ dig_info, int D, int level,
                          const u64* add0, const u64* add1, long add_stride, u64* out0, u64* out1,
                          long out_stride, int batch, const u64* __restrict__ conv,
-                         const WPair* __restrict__ p_inv) {
+                         const WPair* __restrict__ p_inv, const double2* __restrict__ p_inv_d) {
   constexpr int W = fin_words<kD, TENS>();
   constexpr int ST = FHE_FIN_STAGES;
   extern __shared__ __align__(16) unsigned char fsm[];
@@ -744,6 +748,7 @@ __global__ void __launch_bounds__(kThreads, FHE_FINS_MINB)
       }
     }
     const WPair pi = p_inv[m];
+    const double2 pd = p_inv_d[m];
     for (int b = 0; b < batch; ++b) {
       issue(b + ST - 1);
       ks_cp_wait<ST - 1>();
@@ -751,19 +756,29 @@ __global__ void __launch_bounds__(kThreads, FHE_FINS_MINB)
       const int k0 = TENS ? kD - 1 : kD;
       double d2 = 0.0;
       u64 av0 = 0, av1 = 0;
+      double avd0 = 0.0, avd1 = 0.0;
       if constexpr (TENS) {
         const double a0 = fp_from_u52(*slot(s, k0 + 2)), a1 = fp_from_u52(*slot(s, k0 + 3));
         const double c0 = fp_from_u52(*slot(s, k0 + 4)), c1 = fp_from_u52(*slot(s, k0 + 5));
         const double2 w0 = make_double2(c0, __dmul_rn(c0, qd.y));
         const double2 w1 = make_double2(c1, __dmul_rn(c1, qd.y));
+#if FHE_FIN_FP
+        avd0 = fp_mulmod(a0, w0, qd.x);
+        avd1 = fp_reduce(__dadd_rn(fp_mulmod(a0, w1, qd.x), fp_mulmod(a1, w0, qd.x)), qd);
+#else
         av0 = fp_canon_half(fp_reduce(fp_mulmod(a0, w0, qd.x), qd), qd.x);
         av1 = fp_canon_half(
             fp_reduce(__dadd_rn(fp_mulmod(a0, w1, qd.x), fp_mulmod(a1, w0, qd.x)), qd), qd.x);
+#endif
         const double r2 = fp_reduce(fp_mulmod(a1, w1, qd.x), qd);
         d2 = r2 < 0.0 ? __dadd_rn(r2, qd.x) : r2;
       } else {
         if (add0) av0 = *slot(s, k0 + 2);
         if (add1) av1 = *slot(s, k0 + 3);
+#if FHE_FIN_FP
+        avd0 = add0 ? fp_from_u52(av0) : 0.0;
+        avd1 = add1 ? fp_from_u52(av1) : 0.0;
+#endif
       }
       double sb = 0.0, sa = 0.0;
       int k = 0;
@@ -781,6 +796,22 @@ __global__ void __launch_bounds__(kThreads, FHE_FINS_MINB)
           sa = __dadd_rn(sa, fp_mulmod(x, ka[di], qd.x));
         }
       }
+#if FHE_FIN_FP
+      // ModDown finish on the FP64 pipe: (acc - conv) P^-1 + add with signed
+      // representatives (|acc - conv| < 1.5 q, |product| <= q/2, |sum| < 2q),
+      // one reduction and the canonical word -- the same word as the integer
+      // Shoup form below
+      const double yb = fp_mulmod(__dadd_rn(fp_reduce(sb, qd), -fp_from_u52(*slot(s, k0))), pd,
+                                  qd.x);
+      const double ya = fp_mulmod(__dadd_rn(fp_reduce(sa, qd), -fp_from_u52(*slot(s, k0 + 1))),
+                                  pd, qd.x);
+      out0[b * out_stride + w] =
+          (TENS || add0) ? fp_canon_half(fp_reduce(__dadd_rn(yb, avd0), qd), qd.x)
+                         : fp_canon_half(yb, qd.x);
+      out1[b * out_stride + w] =
+          (TENS || add1) ? fp_canon_half(fp_reduce(__dadd_rn(ya, avd1), qd), qd.x)
+                         : fp_canon_half(ya, qd.x);
+#else
       const u64 rb = fp_canon_half(fp_reduce(sb, qd), qd.x);
       const u64 ra = fp_canon_half(fp_reduce(sa, qd), qd.x);
       u64 v0 = shoup_mul(sub_mod(rb, *slot(s, k0), q), pi.w, pi.sh, q);
@@ -789,6 +820,7 @@ __global__ void __launch_bounds__(kThreads, FHE_FINS_MINB)
       if (TENS || add1) v1 = add_mod(av1, v1, q);
       out0[b * out_stride + w] = v0;
       out1[b * out_stride + w] = v1;
+#endif
     }
     ks_cp_wait<0>();
   }
@@ -1228,7 +1260,7 @@ int run_keyswitch(const FheContext& ctx, int level, const u64* d, long d_stride,
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_b);
       kern<<<grid_for((long)level << log_n), kThreads, smem_b, st>>>(
           ch, d, d_stride, ext, (long)lp.ext_rows * n, key, L + K, lp.dig_info, lp.digits, level,
-          add0, add1, add_stride, out0, out1, out_stride, batch, conv, lp.p_inv);
+          add0, add1, add_stride, out0, out1, out_stride, batch, conv, lp.p_inv, lp.p_inv_d);
     };
     if (tens) {
       if (lp.digits <= 2) go(ks_fin_staged_kernel<2, true>, fin_staged_smem<2, true>());
