@@ -18,7 +18,7 @@
 typedef uint64_t u64;
 typedef uint32_t u32;
 
-// Per-prime reduction constants (built on the host, see context.cpp).
+// Per-prime reduction constants (built on the host, see context.cu).
 //   mu   = floor(2^(64+s) / q) with s = bitlen(q) - 1   (fits in 64 bits)
 //   r64  = 2^64 mod q
 struct ModConst {

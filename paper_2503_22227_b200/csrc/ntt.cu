@@ -54,9 +54,21 @@ unsigned long long ntt_path_count(int p) {
 namespace {
 #include "ntt_tiles.cuh"
 
+// Integer-pipe tiles (a prime >= 2^50) need more registers than the FP64
+// tiles' occupancy leaves (64-bit products): their CTAs per SM are capped at
+// 3, which removes their 100-180 B spills (config-4 with 60-bit special
+// primes: 2140 -> 2254 ops/s; 4 CTAs/SM: 2073).
+#ifndef FHE_INT_MINB
+#define FHE_INT_MINB 3
+#endif
+template <class Tile>
+constexpr int int_minb() {
+  return Tile::MINB < FHE_INT_MINB ? Tile::MINB : FHE_INT_MINB;
+}
+
 // Persistent, double-buffered transform kernel over the tiles of one policy.
 template <class Tile, bool FWD, bool LAZY, int OUT>
-__global__ void __launch_bounds__(Tile::THREADS, Tile::MINB)
+__global__ void __launch_bounds__(Tile::THREADS, int_minb<Tile>())
     ntt_tiles_kernel(const DevChain ch, u64* dst, const u64* src, Tile tl, int ntiles) {
   extern __shared__ __align__(16) u64 smem_raw[];
   // contiguous tile range per CTA (keeps the tile order's twiddle locality)
@@ -628,7 +640,7 @@ template <class Tile, bool FWD, bool LAZY, int OUT>
 int launch_tiles(const DevChain& ch, u64* dst, const u64* src, const Tile& tl, int ntiles,
                  cudaStream_t st) {
   if (ntiles <= 0) return 0;
-  const int grid = std::min(ntiles, Tile::MINB * sm_count());
+  const int grid = std::min(ntiles, int_minb<Tile>() * sm_count());
   constexpr int smem = 2 * Tile::SMEM_WORDS * sizeof(u64);
   static bool attr = false;  // once per instantiation
   if (!attr) {
