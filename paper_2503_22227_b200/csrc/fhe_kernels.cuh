@@ -33,7 +33,7 @@ struct NttArgs {
   long dst_bstride;
   const NttFinish* fin = nullptr;  // forward only; *fin_done tells if it was applied
   bool* fin_done = nullptr;
-  // Broadcast input (forward, N = 2^16 TMA column path only): input row r is
+  // Broadcast input (forward; N = 2^16 TMA column path and N <= 2^12 rows): input row r is
   // bcast_src + (r / map.limbs) * bcast_stride -- one row per batch item,
   // shared by its map.limbs target rows -- read as the centred integer
   // (v > center_q / 2 ? v - center_q : v).  Rescale's correction (ckks.py:
@@ -43,8 +43,9 @@ struct NttArgs {
   // = false and leaves dst untouched.
   const u64* bcast_src = nullptr;
   long bcast_stride = 0;
-  u64 center_q = 0;
+  u64 center_q = 0;               // 0: the source words are used as they are
   bool* bcast_done = nullptr;
+  int bcast_div = 0;              // target rows per source row (0: map.limbs); rows path only
 };
 int launch_ntt(const DevChain& ch, const NttArgs& a, bool inverse, cudaStream_t st);
 unsigned long long ntt_path_count(int path);

@@ -976,6 +976,16 @@ static bool fin_staged_enabled() {
   return on == 1;
 }
 
+// FHE_BCAST_MODUP=0: per-prime gadget ModUp through the conversion kernel
+static bool bcast_modup_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("FHE_BCAST_MODUP");
+    on = (e && e[0] == '0') ? 0 : 1;
+  }
+  return on == 1;
+}
+
 bool fin_inner_enabled() {
   static int on = -1;
   if (on < 0) {
@@ -1101,8 +1111,26 @@ int run_keyswitch(const FheContext& ctx, int level, const u64* d, long d_stride,
   rc = launch_ntt(ch, NttArgs{c, d, batch * level, RowMap{nullptr, level, 0}, d_stride, 0},
                   true, st);
   if (rc) return rc;
-  // 2. ModUp: basis extension of every digit, then NTT of the extended rows
-  {
+  // 2. ModUp: basis extension of every digit, then NTT of the extended rows.
+  // Per-prime gadget (alpha = 1, K = 0) on the rows path: ext(d, m) = c_d mod
+  // q_m, so the forward NTT of the ext rows reads the coefficient rows c_d
+  // themselves as a broadcast input (no conversion kernel, no ext write +
+  // re-read).  The words c_d < 2^50 enter the FP64 butterflies unreduced,
+  // which stay below 2^52 until the first lazy reduction (stage 3); the
+  // transform's canonical output is NTT_m(c_d mod q_m) word for word.
+  bool modup_done = false;
+  if (lp.max_na == 1 && K == 0 && ch.fp64_ok && log_n <= 12 && lp.ext_rows > 0 &&
+      bcast_modup_enabled()) {
+    NttArgs na{ext, ext, batch * lp.ext_rows, RowMap{lp.ext_prime, lp.ext_rows, 0}, 0, 0};
+    na.bcast_src = c;
+    na.bcast_stride = n;
+    na.center_q = 0;
+    na.bcast_div = level - 1;
+    na.bcast_done = &modup_done;
+    rc = launch_ntt(ch, na, false, st);
+    if (rc) return rc;
+  }
+  if (!modup_done) {
     int max_w = 0;
     for (int di = 0; di < lp.digits; ++di)
       max_w = std::max(max_w, lp.dig_na[di] * (level + K - lp.dig_na[di]));

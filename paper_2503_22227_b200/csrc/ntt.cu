@@ -1024,14 +1024,15 @@ int launch_rows(const DevChain& ch, const NttArgs& a, bool inverse, bool lazy, c
     // centred broadcast input (rescale correction), FP64 path
     if (a.bcast_done) *a.bcast_done = false;
     if (inverse || !ch.fp64_ok) return 0;
-    tl.bcast_limbs = a.map.limbs;
+    const int bdiv = a.bcast_div ? a.bcast_div : a.map.limbs;
+    tl.bcast_limbs = bdiv;
     tl.bcast_stride = a.bcast_stride;
     tl.center = (double)a.center_q;
     if constexpr (LOG_N == 12) {
       if (a.rows <= FHE_ROW_CLUSTER_PER_SM * sm_count() && row_cluster_enabled()) {
         path_hit(FHE_NTT_PATH_CLUSTER);
         ntt_row_cluster_kernel<true><<<a.rows * 4, kRcThreads, 0, st>>>(
-            ch, a.dst, a.bcast_src, a.map, tl.src, tl.dst, a.map.limbs, a.bcast_stride,
+            ch, a.dst, a.bcast_src, a.map, tl.src, tl.dst, bdiv, a.bcast_stride,
             (double)a.center_q);
         FHE_LAUNCH_CHECK();
         if (a.bcast_done) *a.bcast_done = true;
@@ -1101,8 +1102,10 @@ int launch_split(const DevChain& ch, const NttArgs& a, bool inverse, bool lazy,
   const bool use_ktma = (LOG_N - LOG_N1 == 8) && ch.fp64_ok && kstage && tma_enabled() &&
                         a.rows % a.map.limbs == 0 && std::getenv("FHE_NTT_KTMA") == nullptr;
   if (a.bcast_src) {
-    // centred broadcast input (rescale): TMA column tiles only
+    // centred broadcast input (rescale): TMA column tiles only, one source
+    // row per map.limbs target rows
     if (a.bcast_done) *a.bcast_done = false;
+    if (a.bcast_div && a.bcast_div != a.map.limbs) return 0;
     if constexpr (kTmaShape) {
       if (inverse || !use_tma || a.fin) return 0;
       const double center = (double)a.center_q;
