@@ -985,11 +985,13 @@ int launch_cols_tma(const DevChain& ch, u64* dst, const u64* src, const Tile& tl
 }
 
 // N = 2^12 rows on 4-CTA clusters (FHE_NTT_ROW_CLUSTER=0: whole-row tiles)
-// (up to FHE_ROW_CLUSTER_PER_SM rows per SM: 1 row 6.4 -> 3.4 us, 169 rows
-// 11.8 -> 11.0 us, 312 rows 24 -> 20 us, but 676 rows 33 -> 38 us and 1600
-// rows 61 -> 86 us; tools/small_ntt_time.py, tools/ntt_bench.py 12 13 26)
+// (up to FHE_ROW_CLUSTER_PER_SM rows per SM; latency mode (twiddles
+// prefetched) up to half a row per SM, throughput mode (64 registers, 4
+// CTAs/SM) above: 1 row 6.4 -> 3.2 us, 169 rows 11.8 -> 9.8 us, 312 rows 25
+// -> 17 us, 676 rows 34 -> 31 us, but 1040 rows 42 -> 45 us and 2080 rows
+// 77 -> 82 us; tools/small_ntt_time.py, tools/ntt_bench.py 12 13 <cts>)
 #ifndef FHE_ROW_CLUSTER_PER_SM
-#define FHE_ROW_CLUSTER_PER_SM 3
+#define FHE_ROW_CLUSTER_PER_SM 5
 #endif
 bool row_cluster_enabled() {
   static int on = -1;
@@ -1031,9 +1033,12 @@ int launch_rows(const DevChain& ch, const NttArgs& a, bool inverse, bool lazy, c
     if constexpr (LOG_N == 12) {
       if (a.rows <= FHE_ROW_CLUSTER_PER_SM * sm_count() && row_cluster_enabled()) {
         path_hit(FHE_NTT_PATH_CLUSTER);
-        ntt_row_cluster_kernel<true><<<a.rows * 4, kRcThreads, 0, st>>>(
-            ch, a.dst, a.bcast_src, a.map, tl.src, tl.dst, bdiv, a.bcast_stride,
-            (double)a.center_q);
+        auto go = [&](auto kern) {
+          kern<<<a.rows * 4, kRcThreads, 0, st>>>(ch, a.dst, a.bcast_src, a.map, tl.src, tl.dst,
+                                                  bdiv, a.bcast_stride, (double)a.center_q);
+        };
+        if (a.rows <= sm_count() / 2) go(ntt_row_cluster_kernel<true, true>);
+        else go(ntt_row_cluster_kernel<true, false>);
         FHE_LAUNCH_CHECK();
         if (a.bcast_done) *a.bcast_done = true;
         return 0;
@@ -1049,12 +1054,12 @@ int launch_rows(const DevChain& ch, const NttArgs& a, bool inverse, bool lazy, c
     // rows per SM, where the per-row latency sets the time
     if (ch.fp64_ok && a.rows <= FHE_ROW_CLUSTER_PER_SM * sm_count() && row_cluster_enabled()) {
       path_hit(FHE_NTT_PATH_CLUSTER);
-      if (inverse)
-        ntt_row_cluster_kernel<false><<<a.rows * 4, kRcThreads, 0, st>>>(
-            ch, a.dst, a.src, a.map, tl.src, tl.dst, 0, 0L, 0.0);
-      else
-        ntt_row_cluster_kernel<true><<<a.rows * 4, kRcThreads, 0, st>>>(
-            ch, a.dst, a.src, a.map, tl.src, tl.dst, 0, 0L, 0.0);
+      const bool pf = a.rows <= sm_count() / 2;  // latency mode: <= 2 CTAs per SM
+      auto go = [&](auto kern) {
+        kern<<<a.rows * 4, kRcThreads, 0, st>>>(ch, a.dst, a.src, a.map, tl.src, tl.dst, 0, 0L, 0.0);
+      };
+      if (inverse) pf ? go(ntt_row_cluster_kernel<false, true>) : go(ntt_row_cluster_kernel<false, false>);
+      else pf ? go(ntt_row_cluster_kernel<true, true>) : go(ntt_row_cluster_kernel<true, false>);
       FHE_LAUNCH_CHECK();
       return 0;
     }

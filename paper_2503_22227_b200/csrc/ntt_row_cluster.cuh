@@ -63,8 +63,12 @@ __device__ __forceinline__ void rc_inv_bf(double& a, double& c, double2 w, doubl
   c = fp_mulmod(d, w, qd.x);
 }
 
-template <bool FWD>
-__global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kRcThreads)
+// PF: every twiddle prefetched into registers before the data (latency mode,
+// 96 registers, 2 CTAs/SM); !PF: each radix-4 step loads its 3 twiddles when
+// it starts and the register budget admits 4 CTAs/SM (throughput mode, larger
+// launches, where other CTAs cover the loads)
+template <bool FWD, bool PF = true>
+__global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kRcThreads, PF ? 1 : 4)
     ntt_row_cluster_kernel(const DevChain ch, u64* dst, const u64* src, RowMap map, RowAddr sa,
                            RowAddr da, int bcast_limbs, long bcast_stride, double center) {
   __shared__ double blk[1024];   // this CTA's 1024-point block (phase B)
@@ -78,16 +82,30 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kRcThreads)
   // all blocks of the cluster are running before any DSMEM store
   rc_barrier_arrive_relaxed();
   // twiddles: phase A (stages 0, 1) and the 5 radix-4 steps of phase B
-  double2 wa[5], wb[5], wc[5];
+  // step i's twiddles: group g0 = t / (h / 2) of local stage 2 i, groups
+  // 2 g0, 2 g0 + 1 of local stage 2 i + 1
+  auto twa = [&](int i) {
+    return __ldg(tw + (1 << (2 * i + 2)) + ((int)k << (2 * i)) + t / (256 >> (2 * i)));
+  };
+  auto twb = [&](int i) {
+    return __ldg(tw + (1 << (2 * i + 3)) + ((int)k << (2 * i + 1)) + 2 * (t / (256 >> (2 * i))));
+  };
+  auto twc = [&](int i) {
+    return __ldg(tw + (1 << (2 * i + 3)) + ((int)k << (2 * i + 1)) + 2 * (t / (256 >> (2 * i))) +
+                 1);
+  };
+  double2 wa[PF ? 5 : 1], wb[PF ? 5 : 1], wc[PF ? 5 : 1];
+  if constexpr (PF) {
 #pragma unroll
-  for (int i = 0; i < 5; ++i) {
-    const int t0 = 2 * i, t1 = t0 + 1;
-    const int h2 = 256 >> t0;  // h / 2
-    const int g0 = t / h2;
-    wa[i] = __ldg(tw + (1 << (t0 + 2)) + ((int)k << t0) + g0);
-    wb[i] = __ldg(tw + (1 << (t1 + 2)) + ((int)k << t1) + 2 * g0);
-    wc[i] = __ldg(tw + (1 << (t1 + 2)) + ((int)k << t1) + 2 * g0 + 1);
+    for (int i = 0; i < 5; ++i) {
+      wa[i] = twa(i);
+      wb[i] = twb(i);
+      wc[i] = twc(i);
+    }
   }
+  auto WA = [&](int i) { return PF ? wa[PF ? i : 0] : twa(i); };
+  auto WB = [&](int i) { return PF ? wb[PF ? i : 0] : twb(i); };
+  auto WC = [&](int i) { return PF ? wc[PF ? i : 0] : twc(i); };
   const double2 w0 = __ldg(tw + 1), w1a = __ldg(tw + 2), w1b = __ldg(tw + 3);
   // broadcast input (forward only): row r reads row r / bcast_limbs of src,
   // centred about `center` when nonzero (the rescale correction, as RowsTile)
@@ -117,11 +135,12 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kRcThreads)
     for (int i = 0; i < 5; ++i) {
       const int t0 = 2 * i, h = 512 >> t0, h2 = h >> 1;
       const int b = (t / h2) * 2 * h + (t % h2);
+      const double2 sa = WA(i), sb = WB(i), sc = WC(i);
       double y0 = blk[b], y1 = blk[b + h2], y2 = blk[b + h], y3 = blk[b + h + h2];
-      rc_fwd_bf(y0, y2, wa[i], qd, t0 + 2);
-      rc_fwd_bf(y1, y3, wa[i], qd, t0 + 2);
-      rc_fwd_bf(y0, y1, wb[i], qd, t0 + 3);
-      rc_fwd_bf(y2, y3, wc[i], qd, t0 + 3);
+      rc_fwd_bf(y0, y2, sa, qd, t0 + 2);
+      rc_fwd_bf(y1, y3, sa, qd, t0 + 2);
+      rc_fwd_bf(y0, y1, sb, qd, t0 + 3);
+      rc_fwd_bf(y2, y3, sc, qd, t0 + 3);
       if (i < 4) {
         __syncthreads();
         blk[b] = y0;
@@ -149,10 +168,11 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kRcThreads)
       double y0 = fp_from_u52(v0.x), y1 = fp_from_u52(v0.y), y2 = fp_from_u52(v1.x),
              y3 = fp_from_u52(v1.y);
       // step 4 (stages 11, 10): b = 4 t
-      rc_inv_bf(y0, y1, wb[4], qd, 11);
-      rc_inv_bf(y2, y3, wc[4], qd, 11);
-      rc_inv_bf(y0, y2, wa[4], qd, 10);
-      rc_inv_bf(y1, y3, wa[4], qd, 10);
+      const double2 sa = WA(4), sb = WB(4), sc = WC(4);
+      rc_inv_bf(y0, y1, sb, qd, 11);
+      rc_inv_bf(y2, y3, sc, qd, 11);
+      rc_inv_bf(y0, y2, sa, qd, 10);
+      rc_inv_bf(y1, y3, sa, qd, 10);
       blk[4 * t] = y0;
       blk[4 * t + 1] = y1;
       blk[4 * t + 2] = y2;
@@ -164,11 +184,12 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kRcThreads)
     for (int i = 3; i >= 0; --i) {
       const int t0 = 2 * i, h = 512 >> t0, h2 = h >> 1;
       const int b = (t / h2) * 2 * h + (t % h2);
+      const double2 sa = WA(i), sb = WB(i), sc = WC(i);
       double y0 = blk[b], y1 = blk[b + h2], y2 = blk[b + h], y3 = blk[b + h + h2];
-      rc_inv_bf(y0, y1, wb[i], qd, t0 + 3);
-      rc_inv_bf(y2, y3, wc[i], qd, t0 + 3);
-      rc_inv_bf(y0, y2, wa[i], qd, t0 + 2);
-      rc_inv_bf(y1, y3, wa[i], qd, t0 + 2);
+      rc_inv_bf(y0, y1, sb, qd, t0 + 3);
+      rc_inv_bf(y2, y3, sc, qd, t0 + 3);
+      rc_inv_bf(y0, y2, sa, qd, t0 + 2);
+      rc_inv_bf(y1, y3, sa, qd, t0 + 2);
       if (i > 0) {
         __syncthreads();
         blk[b] = y0;

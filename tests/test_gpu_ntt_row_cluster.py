@@ -1,5 +1,5 @@
 """The N = 2^12 row-per-cluster NTT (csrc/ntt_row_cluster.cuh, the default
-for launches of up to 3 rows per SM) is bit-identical to the C oracle
+for launches of up to 5 rows per SM) is bit-identical to the C oracle
 restatement of the reference transform (coremath/_kernels.py:35-99) and is
 the path that ran; above the row cap the whole-row tiles run instead."""
 import numpy as np
@@ -10,7 +10,7 @@ pytestmark = pytest.mark.gpu
 
 
 @pytest.mark.parametrize("bits,L,rows", [(36, 1, 1), (45, 13, 13), (49, 13, 26), (50, 7, 169),
-                                         (45, 13, 445), (50, 40, 600)])
+                                         (45, 13, 445), (50, 40, 600), (45, 13, 741)])
 def test_row_cluster_ntt_matches_oracle(bits, L, rows):
     from oracle import fast
     from paper_2503_22227_b200 import _native
@@ -31,7 +31,7 @@ def test_row_cluster_ntt_matches_oracle(bits, L, rows):
         ch.transform(buf, rows, inverse, limbs=L, offset=0)
         torch.cuda.synchronize()
         took = _native.ntt_path_counts()["cluster"] - c0
-        assert took == (1 if rows <= 3 * sms else 0), (rows, took)
+        assert took == (1 if rows <= 5 * sms else 0), (rows, took)
         want = fast.ntt_forward(a, primes, midx, inverse=inverse)
         got = buf.cpu().numpy().view(np.uint64)
         bad = int((got != want).any(axis=1).sum())
