@@ -17,8 +17,11 @@ graph and replayed per query with one launch:
   constant columns (passed at capture and kept alive here); the outputs are
   the captured ciphertexts, overwritten by every replay -- a result is valid
   until the next replay of the same CapturedQuery;
-* the host part (two-party inverse: decrypt, reciprocal, re-encrypt) and the
-  one or two products after it run eagerly (PdqEngine.finish).
+* the host part (two-party inverse: mask, decrypt, reciprocal, re-encrypt)
+  runs eagerly; the products after it (unmask with the same r, then one or
+  two ciphertext products) are a second graph, captured at the first run:
+  per run the fresh ciphertext and the mask's encoding (host FFT, as the
+  reference) are copied into that graph's static inputs before its replay.
 
 Every replay computes the same words as the eager path (same kernels, same
 order); tests/test_gpu_pdq_graph.py checks them against the reference goldens.
@@ -27,7 +30,11 @@ Single-GPU only (the sharded layouts exchange through collectives).
 
 from __future__ import annotations
 
+import numpy as np
+
 from ..pools import MemoryPool
+from ..rnspoly import CData
+from ..schemes.ckks import (CkksCiphertext, CkksPlaintext, ckks_multiply_plain, ckks_rescale)
 from .engine import PdqEngine, QueryResult, QuerySpec
 
 
@@ -75,4 +82,72 @@ class CapturedQuery:
         return self.parts
 
     def run(self, channel=None, rng=None) -> QueryResult:
-        return self.engine.finish(self.spec, self.replay(), channel, rng)
+        parts = self.replay()
+        if self.spec.agg not in ("avg", "ratio"):
+            return self.engine.finish(self.spec, parts, channel, rng)
+        return self._finish_inverse(parts, channel, rng)
+
+    # -- the products after the two-party inverse ---------------------------------
+    def _post(self, parts: dict, fresh: CkksCiphertext, pt: CkksPlaintext):
+        """engine.finish's device work after the reciprocal (reference
+        engine.py:209-244, two_party_multiply_inverse's last line)."""
+        ev = self.engine.ev
+        inv = ckks_rescale(ev.ctx, ckks_multiply_plain(ev.ctx, fresh, pt))
+        inv.scale = fresh.scale
+        if self.spec.agg == "avg":
+            return {"avg": ev.mul(parts["total"], inv), "count": parts["count"]}
+        return {"ratio": ev.mul(ev.mul(parts["num"], inv), parts["mask"])}
+
+    def _finish_inverse(self, parts: dict, channel, rng) -> QueryResult:
+        import gc
+
+        import torch
+
+        ev, cfg = self.engine.ev, self.engine.cfg
+        ct = parts["count"] if self.spec.agg == "avg" else parts["denom"]
+        # two_party_multiply_inverse (engine.py), with the unmasking product
+        # replayed from a graph: the same random draws in the same order
+        rng = rng or np.random.default_rng()
+        e = cfg.mask_exp_range
+        r = rng.uniform(2.0 ** -e, 2.0 ** e, ev.slots)
+        r *= rng.choice([-1.0, 1.0], ev.slots)
+        masked = ev.mul_plain_vec(ct, r)
+        fresh, flags = channel.reciprocal(masked)
+        pt = ev.encode(r, level=fresh.level, scale=ev._q_last(fresh))
+        post = getattr(self, "_post_graph", None)
+        if post is None or post["key"] != (fresh.level, fresh.scale, pt.scale):
+            # first run (or new metadata): eager result, then capture
+            cts = self._post(parts, fresh, pt)
+            ctx = ev.ctx
+            fbuf = fresh.data.view().clone()
+            pbuf = pt.data.view().clone()
+            sf = CkksCiphertext(CData.wrap(fbuf.reshape(-1), fresh.data.size_poly,
+                                           fresh.data.size_modulus, ctx.n, fresh.data.domains[0]),
+                                fresh.scale, fresh.level)
+            sp = CkksPlaintext(CData.wrap(pbuf.reshape(-1), pt.data.size_poly,
+                                          pt.data.size_modulus, ctx.n, pt.data.domains[0]),
+                               pt.scale, pt.level)
+            torch.cuda.synchronize()
+            self._post_pool = MemoryPool(1, unit_mb=64, cap_mb=64)
+            g = torch.cuda.CUDAGraph()
+            gc.collect()
+            gc_was_on = gc.isenabled()
+            gc.disable()
+            saved = ctx.pool
+            ctx.pool = self._post_pool
+            try:
+                with torch.cuda.graph(g):
+                    outs = self._post(parts, sf, sp)
+            finally:
+                ctx.pool = saved
+                if gc_was_on:
+                    gc.enable()
+            torch.cuda.synchronize()
+            self._post_graph = {"key": (fresh.level, fresh.scale, pt.scale), "graph": g,
+                                "fbuf": fbuf, "pbuf": pbuf, "outs": outs}
+        else:
+            post["fbuf"].copy_(fresh.data.view())
+            post["pbuf"].copy_(pt.data.view())
+            post["graph"].replay()
+            cts = post["outs"]
+        return QueryResult(self.spec.agg, cts, {"recip_flags": flags.tolist()})

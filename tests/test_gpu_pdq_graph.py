@@ -44,3 +44,17 @@ def test_captured_queries_match_reference(golden):
         for k, c in res.cts.items():
             assert digest(c.data.view()) == want[k]["sha"], (qid, k)
             assert c.scale == want[k]["scale"] and c.level == want[k]["level"]
+        if qid in (3, 4):
+            # second run: the products after the inverse replay from their own
+            # graph; same words as the eager finish on the same draws
+            from paper_2503_22227_b200.coremath.sampling import Rng
+
+            def client():
+                return LocalInverseClient(ev, cfg, sk, pk, rng=Rng((77).to_bytes(32, "little")))
+
+            res_g = cq.run(channel=client(), rng=np.random.default_rng(5))
+            got = {k: (digest(c.data.view()), c.scale, c.level) for k, c in res_g.cts.items()}
+            res_e = engine.finish(spec, cq.replay(), client(), np.random.default_rng(5))
+            exp = {k: (digest(c.data.view()), c.scale, c.level) for k, c in res_e.cts.items()}
+            assert got == exp, qid
+            assert res_g.meta == res_e.meta
