@@ -192,9 +192,19 @@ def ckks_encrypt(ctx: Context, pt: CkksPlaintext, pk: PublicKey,
     level, n = pt.level, ctx.n
     primes = ctx.q_arr(level)
     if device_sampling(ctx):  # the same Philox stream, drawn on the device
-        u = signed_eval(ctx, rng.ternary_device(n), primes)
-        e0 = signed_eval(ctx, rng.cbd_error_device(n), primes)
-        e1 = signed_eval(ctx, rng.cbd_error_device(n), primes)
+        # u, e0, e1 lifted into one (3, level, n) block and transformed by
+        # one launch; e0 and e1 share one flip draw (cbd_error_pair_device)
+        import torch
+
+        uc = rng.ternary_device(n)
+        e0c, e1c = rng.cbd_error_pair_device(n)
+        rows = torch.empty((3, level, n), dtype=torch.int64, device="cuda")
+        for k, c in enumerate((uc, e0c, e1c)):
+            _native.check(_native.lib().fhe_signed_lift(ctx.chain.handle, rows[k].data_ptr(),
+                                                        c.data_ptr(), n, level, 0,
+                                                        _native.stream_handle()), "fhe_signed_lift")
+        ctx.chain.transform(rows, 3 * level, False, limbs=level, offset=0)
+        u, e0, e1 = rows[0], rows[1], rows[2]
     else:
         u = signed_eval(ctx, rng.ternary(n), primes)
         e0 = signed_eval(ctx, rng.cbd_error(n), primes)
