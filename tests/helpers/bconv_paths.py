@@ -1,6 +1,7 @@
-"""Run with FHE_BCONV_IMMA=0 or 1 (read once per process): HMult+Relin and
-rotate at a hybrid N=2^16 parameter set (L=17 with a ragged last digit,
-batch 3), printing sha256 digests of the results, so the tensor-core and the
+"""Run with FHE_BCONV_IMMA=0 or 1 / FHE_BCONV_UMMA=0 or 1 (read once per
+process): HMult+Relin and rotate at a hybrid N=2^16 parameter set (default
+L=17 with a ragged last digit; BCONV_SHAPE=L,special,dnum), batch 3,
+printing sha256 digests of the results, so the tcgen05, mma.sync and
 FP64-pipe base conversions can be compared word for word."""
 import hashlib
 import json
@@ -18,8 +19,10 @@ from paper_2503_22227_b200.keys import (galois_keygen, hmult_relin_into, keygen,
 from paper_2503_22227_b200.schemes import ckks  # noqa: E402
 
 n = 1 << 16
-ctx = Context(hybrid_params(n, 17, special=6, dnum=3, scale=float(2 ** 49)),
-              PoolConfig(unit_mb=64, cap_mb=2048))
+# BCONV_SHAPE=L,special,dnum (default 17,6,3: digits of 6/6/5 limbs, K-steps 2)
+Lq, Ksp, Dn = (int(v) for v in os.environ.get("BCONV_SHAPE", "17,6,3").split(","))
+ctx = Context(hybrid_params(n, Lq, special=Ksp, dnum=Dn, scale=float(2 ** 49)),
+              PoolConfig(unit_mb=64, cap_mb=4096))
 seed = lambda s: Rng(int(s).to_bytes(32, "little"))  # noqa: E731
 sk = keygen(ctx, seed(1))
 pk = pk_gen(ctx, sk, seed(2))

@@ -258,3 +258,23 @@ def test_tensor_core_bconv_equals_fp64_bconv():
     for tag in ("imma2", "imma1", "fp64"):
         assert res["umma"]["hmult"] == res[tag]["hmult"], tag
         assert res["umma"]["rotate"] == res[tag]["rotate"], tag
+
+
+@pytest.mark.parametrize("shape", ["12,4,3", "32,16,2"])
+def test_tcgen05_bconv_k_steps(shape):
+    """The tcgen05 conversion at 1 and 4 K-steps (digits / P of 4 and 16
+    limbs: 28 and 112 bytes of K) gives the FP64 conversion's words."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    script = os.path.join(os.path.dirname(os.path.abspath(__file__)), "helpers", "bconv_paths.py")
+    res = {}
+    for tag, env in (("umma", {}), ("fp64", {"FHE_BCONV_IMMA": "0"})):
+        r = subprocess.run([sys.executable, script], capture_output=True, text=True, timeout=900,
+                           env=dict(os.environ, BCONV_SHAPE=shape, **env))
+        assert r.returncode == 0, r.stderr[-2000:]
+        res[tag] = json.loads(r.stdout.strip().splitlines()[-1])
+    assert res["umma"]["hmult"] == res["fp64"]["hmult"]
+    assert res["umma"]["rotate"] == res["fp64"]["rotate"]
