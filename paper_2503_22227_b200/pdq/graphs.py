@@ -98,56 +98,71 @@ class CapturedQuery:
             return {"avg": ev.mul(parts["total"], inv), "count": parts["count"]}
         return {"ratio": ev.mul(ev.mul(parts["num"], inv), parts["mask"])}
 
-    def _finish_inverse(self, parts: dict, channel, rng) -> QueryResult:
+    def _staged(self, name: str, key, fn, inputs: list):
+        """fn(*inputs) replayed from a graph captured at its first use (per
+        name and metadata key): the first call runs eagerly, then records fn
+        over static copies of the inputs (device plaintexts / ciphertexts) in a
+        private pool; later calls copy the inputs in and replay."""
         import gc
 
         import torch
 
+        st = self._finish_graphs.get(name)
+        if st is not None and st["key"] == key:
+            for buf, x in zip(st["bufs"], inputs):
+                buf.copy_(x.data.view())
+            st["graph"].replay()
+            return st["outs"]
+        result = fn(*inputs)
+        ctx = self.engine.ev.ctx
+        bufs, statics = [], []
+        for x in inputs:
+            b = x.data.view().clone()
+            cd = CData.wrap(b.reshape(-1), x.data.size_poly, x.data.size_modulus, ctx.n,
+                            x.data.domains[0])
+            statics.append(type(x)(cd, x.scale, x.level))
+            bufs.append(b)
+        torch.cuda.synchronize()
+        pool = MemoryPool(1, unit_mb=64, cap_mb=64)
+        g = torch.cuda.CUDAGraph()
+        gc.collect()
+        gc_was_on = gc.isenabled()
+        gc.disable()
+        saved = ctx.pool
+        ctx.pool = pool
+        try:
+            with torch.cuda.graph(g):
+                outs = fn(*statics)
+        finally:
+            ctx.pool = saved
+            if gc_was_on:
+                gc.enable()
+        torch.cuda.synchronize()
+        self._finish_graphs[name] = {"key": key, "graph": g, "bufs": bufs, "outs": outs,
+                                     "pool": pool}
+        return result
+
+    def _finish_inverse(self, parts: dict, channel, rng) -> QueryResult:
         ev, cfg = self.engine.ev, self.engine.cfg
+        if not hasattr(self, "_finish_graphs"):
+            self._finish_graphs = {}
         ct = parts["count"] if self.spec.agg == "avg" else parts["denom"]
-        # two_party_multiply_inverse (engine.py), with the unmasking product
-        # replayed from a graph: the same random draws in the same order
+        # two_party_multiply_inverse (engine.py) with its two mask products
+        # replayed from graphs: the same random draws in the same order
         rng = rng or np.random.default_rng()
         e = cfg.mask_exp_range
         r = rng.uniform(2.0 ** -e, 2.0 ** e, ev.slots)
         r *= rng.choice([-1.0, 1.0], ev.slots)
-        masked = ev.mul_plain_vec(ct, r)
+        pt1 = ev.encode(r, level=ct.level, scale=ev._q_last(ct))
+
+        def mask(p):
+            out = ckks_rescale(ev.ctx, ckks_multiply_plain(ev.ctx, ct, p))
+            out.scale = ct.scale
+            return out
+
+        masked = self._staged("mask", (ct.level, ct.scale, pt1.scale), mask, [pt1])
         fresh, flags = channel.reciprocal(masked)
         pt = ev.encode(r, level=fresh.level, scale=ev._q_last(fresh))
-        post = getattr(self, "_post_graph", None)
-        if post is None or post["key"] != (fresh.level, fresh.scale, pt.scale):
-            # first run (or new metadata): eager result, then capture
-            cts = self._post(parts, fresh, pt)
-            ctx = ev.ctx
-            fbuf = fresh.data.view().clone()
-            pbuf = pt.data.view().clone()
-            sf = CkksCiphertext(CData.wrap(fbuf.reshape(-1), fresh.data.size_poly,
-                                           fresh.data.size_modulus, ctx.n, fresh.data.domains[0]),
-                                fresh.scale, fresh.level)
-            sp = CkksPlaintext(CData.wrap(pbuf.reshape(-1), pt.data.size_poly,
-                                          pt.data.size_modulus, ctx.n, pt.data.domains[0]),
-                               pt.scale, pt.level)
-            torch.cuda.synchronize()
-            self._post_pool = MemoryPool(1, unit_mb=64, cap_mb=64)
-            g = torch.cuda.CUDAGraph()
-            gc.collect()
-            gc_was_on = gc.isenabled()
-            gc.disable()
-            saved = ctx.pool
-            ctx.pool = self._post_pool
-            try:
-                with torch.cuda.graph(g):
-                    outs = self._post(parts, sf, sp)
-            finally:
-                ctx.pool = saved
-                if gc_was_on:
-                    gc.enable()
-            torch.cuda.synchronize()
-            self._post_graph = {"key": (fresh.level, fresh.scale, pt.scale), "graph": g,
-                                "fbuf": fbuf, "pbuf": pbuf, "outs": outs}
-        else:
-            post["fbuf"].copy_(fresh.data.view())
-            post["pbuf"].copy_(pt.data.view())
-            post["graph"].replay()
-            cts = post["outs"]
+        cts = self._staged("post", (fresh.level, fresh.scale, pt.scale),
+                           lambda f, p: self._post(parts, f, p), [fresh, pt])
         return QueryResult(self.spec.agg, cts, {"recip_flags": flags.tolist()})

@@ -93,13 +93,21 @@ def _twist(n: int) -> np.ndarray:
     return t
 
 
+_embed_inv_cache: dict = {}
+
+
 def embed_inverse(values: np.ndarray, n: int) -> np.ndarray:
-    """n/2 complex slots -> n real coefficients."""
-    idx = _slots(n)
+    """n/2 complex slots -> n real coefficients (the reference expression;
+    the mirrored slot indices and conj(twist) are cached: same values)."""
+    c = _embed_inv_cache.get(n)
+    if c is None:
+        idx = _slots(n)
+        c = _embed_inv_cache[n] = (idx, n - 1 - idx, np.conj(_twist(n)))
+    idx, ridx, ctw = c
     u = np.zeros(n, dtype=np.complex128)
     u[idx] = values
-    u[n - 1 - idx] = np.conj(values)
-    return (np.fft.fft(u) / n * np.conj(_twist(n))).real
+    u[ridx] = np.conj(values)
+    return (np.fft.fft(u) / n * ctw).real
 
 
 def embed_forward(coeffs: np.ndarray, n: int) -> np.ndarray:
@@ -168,7 +176,7 @@ def _coeff_rows(ctx: Context, cd: CData, level: int) -> np.ndarray:
     return t.cpu().numpy().view(np.uint64)
 
 
-def ckks_decode(ctx: Context, pt: CkksPlaintext) -> np.ndarray:
+def ckks_decode(ctx: Context, pt: CkksPlaintext, inplace: bool = False) -> np.ndarray:
     """ckks.py:157-166: INTT, centred CRT lift to float64 and the division by
     the scale on the device (exact Python-integer float() rounding, same IEEE
     division: fhe_crt_lift), then the canonical-embedding FFT on the host
@@ -176,7 +184,8 @@ def ckks_decode(ctx: Context, pt: CkksPlaintext) -> np.ndarray:
     from .. import _native
     from ..coremath.crt import device_lift
 
-    t = pt.data.view()[0].clone()
+    # inplace: pt is a temporary (decrypt's output) and may be transformed in place
+    t = pt.data.view()[0] if inplace else pt.data.view()[0].clone()
     ctx.chain.transform(t, pt.level, True, limbs=pt.level, offset=0)
     vals = device_lift(ctx, t, pt.level, _native.CRT_FLOAT, scale=pt.scale).cpu().numpy()
     if not np.isfinite(vals).all():
@@ -226,6 +235,9 @@ def ckks_decrypt(ctx: Context, ct: CkksCiphertext, sk: SecretKey) -> CkksPlainte
     s = sk.s.view()[0, :level]
     out = cdata_new(ctx.pool, 1, level, ctx.n, Domain.EVALUATION, zero=False)
     acc = out.view()[0]
+    if ct.data.size_poly == 2:  # c0 + c1 s in one launch
+        _ew(ctx, _native.EW_MUL_ADD, acc, v[1], s, v[0], rows=level, limbs=level)
+        return CkksPlaintext(out, ct.scale, level)
     acc.copy_(v[0])
     s_pow = s
     for p in range(1, ct.data.size_poly):
