@@ -406,8 +406,10 @@ int build_levels(FheContext* ctx) {
     }
     // FP64 pairs (value, value / modulus) for the FP64-pipe base conversions
     const bool fp64 = ctx->chain->dev.fp64_ok;
-    std::vector<double2> up_inv_d, up_w_d, down_inv_d, down_w_d, p_inv_d;
+    std::vector<double2> up_inv_d, up_w_d, down_inv_d, down_w_d, p_inv_d, rs_inv_d;
     if (fp64) {
+      for (int j = 0; j + 1 < l; ++j)
+        rs_inv_d.push_back(make_double2((double)rs_inv[j].w, (double)rs_inv[j].w / (double)pr[j]));
       for (int j = 0; j < l; ++j)
         p_inv_d.push_back(make_double2((double)p_inv[j].w, (double)p_inv[j].w / (double)pr[j]));
       for (int s = 0; s < l; ++s)
@@ -508,7 +510,7 @@ int build_levels(FheContext* ctx) {
                  o4 = pk.addv(info), o5 = pk.addv(down_inv), o6 = pk.addv(down_w),
                  o7 = pk.addv(p_inv), o8 = pk.addv(rs_inv), o9 = pk.addv(rs_qlast);
     const size_t o10 = pk.addv(up_inv_d), o11 = pk.addv(up_w_d), o12 = pk.addv(down_inv_d),
-                 o13 = pk.addv(down_w_d), o28 = pk.addv(p_inv_d);
+                 o13 = pk.addv(down_w_d), o28 = pk.addv(p_inv_d), o29 = pk.addv(rs_inv_d);
     void* d = nullptr;
     FHE_CUDA_CHECK(cudaMalloc(&d, pk.buf.size()));
     FHE_CUDA_CHECK(cudaMemcpy(d, pk.buf.data(), pk.buf.size(), cudaMemcpyHostToDevice));
@@ -545,6 +547,7 @@ int build_levels(FheContext* ctx) {
       lp.down_inv_d = (const double2*)(b + o12);
       lp.down_w_d = (const double2*)(b + o13);
       lp.p_inv_d = (const double2*)(b + o28);
+      lp.rs_inv_d = l > 1 ? (const double2*)(b + o29) : nullptr;
     }
   }
   return 0;

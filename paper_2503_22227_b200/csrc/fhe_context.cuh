@@ -39,6 +39,7 @@ struct LevelPlan {
   const double2* down_inv_d = nullptr;
   const double2* down_w_d = nullptr;
   const double2* p_inv_d = nullptr;  // (P^-1 mod q_j, / q_j): the FP64 ModDown finish
+  const double2* rs_inv_d = nullptr; // (q_{l-1}^-1 mod q_j, / q_j): the FP64 rescale finish
   // tensor-core base conversion (bconv_imma.cuh), every chain prime < 2^56:
   // packed byte-split W' fragments, ModUp per digit ([nt][up_ks][32] each,
   // offsets in up_bf_off) and ModDown ([level][down_ks][32])

@@ -46,6 +46,15 @@ struct NttArgs {
   u64 center_q = 0;               // 0: the source words are used as they are
   bool* bcast_done = nullptr;
   int bcast_div = 0;              // target rows per source row (0: map.limbs); rows path only
+  // Rescale finish fused into the broadcast transform's epilogue (N = 2^12
+  // cluster path): row r = (poly, j) writes rs_out[poly][j] = (rs_in[poly][j]
+  // - NTT(row)) * rs_inv_d[j] instead of dst (rs_in has rs_level rows per
+  // poly, rs_out rs_level - 1); *rs_done tells whether it was applied.
+  const u64* rs_in = nullptr;
+  u64* rs_out = nullptr;
+  const double2* rs_inv_d = nullptr;
+  int rs_level = 0;
+  bool* rs_done = nullptr;
 };
 int launch_ntt(const DevChain& ch, const NttArgs& a, bool inverse, cudaStream_t st);
 unsigned long long ntt_path_count(int path);

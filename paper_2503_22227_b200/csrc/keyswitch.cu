@@ -976,6 +976,16 @@ static bool fin_staged_enabled() {
   return on == 1;
 }
 
+// FHE_RESCALE_FUSED_FIN=0: the rescale finish as its own kernel
+static bool rescale_fin_fused_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("FHE_RESCALE_FUSED_FIN");
+    on = (e && e[0] == '0') ? 0 : 1;
+  }
+  return on == 1;
+}
+
 // FHE_BCAST_MODUP=0: per-prime gadget ModUp through the conversion kernel
 static bool bcast_modup_enabled() {
   static int on = -1;
@@ -1479,8 +1489,18 @@ int run_rescale(FheContext& ctx, u64* out, const u64* in, int polys, int level, 
     na.bcast_stride = n;
     na.center_q = ch_prime(ctx, level - 1);
     na.bcast_done = &bcast;
+    bool fused_fin = false;
+    if (lp.rs_inv_d && rescale_fin_fused_enabled()) {
+      // the cluster transform applies the finish in its epilogue
+      na.rs_in = in;
+      na.rs_out = out;
+      na.rs_inv_d = lp.rs_inv_d;
+      na.rs_level = level;
+      na.rs_done = &fused_fin;
+    }
     rc = launch_ntt(ch, na, false, st);
     if (rc) return rc;
+    if (bcast && fused_fin) return 0;
   }
   if (!bcast) {
     rc = launch_modswitch_expand(ch, corr, last, polys, level - 1, level - 1, t_plain, tinv,

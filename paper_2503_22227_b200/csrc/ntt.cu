@@ -1035,8 +1035,10 @@ int launch_rows(const DevChain& ch, const NttArgs& a, bool inverse, bool lazy, c
         path_hit(FHE_NTT_PATH_CLUSTER);
         auto go = [&](auto kern) {
           kern<<<a.rows * 4, kRcThreads, 0, st>>>(ch, a.dst, a.bcast_src, a.map, tl.src, tl.dst,
-                                                  bdiv, a.bcast_stride, (double)a.center_q);
+                                                  bdiv, a.bcast_stride, (double)a.center_q,
+                                                  a.rs_in, a.rs_out, a.rs_inv_d, a.rs_level);
         };
+        if (a.rs_done) *a.rs_done = a.rs_in != nullptr;
         if (a.rows <= sm_count() / 2) go(ntt_row_cluster_kernel<true, true>);
         else go(ntt_row_cluster_kernel<true, false>);
         FHE_LAUNCH_CHECK();
@@ -1056,7 +1058,8 @@ int launch_rows(const DevChain& ch, const NttArgs& a, bool inverse, bool lazy, c
       path_hit(FHE_NTT_PATH_CLUSTER);
       const bool pf = a.rows <= sm_count() / 2;  // latency mode: <= 2 CTAs per SM
       auto go = [&](auto kern) {
-        kern<<<a.rows * 4, kRcThreads, 0, st>>>(ch, a.dst, a.src, a.map, tl.src, tl.dst, 0, 0L, 0.0);
+        kern<<<a.rows * 4, kRcThreads, 0, st>>>(ch, a.dst, a.src, a.map, tl.src, tl.dst, 0, 0L, 0.0,
+                                                nullptr, nullptr, nullptr, 0);
       };
       if (inverse) pf ? go(ntt_row_cluster_kernel<false, true>) : go(ntt_row_cluster_kernel<false, false>);
       else pf ? go(ntt_row_cluster_kernel<true, true>) : go(ntt_row_cluster_kernel<true, false>);

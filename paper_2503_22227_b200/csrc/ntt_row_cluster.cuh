@@ -70,7 +70,9 @@ __device__ __forceinline__ void rc_inv_bf(double& a, double& c, double2 w, doubl
 template <bool FWD, bool PF = true>
 __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kRcThreads, PF ? 1 : 4)
     ntt_row_cluster_kernel(const DevChain ch, u64* dst, const u64* src, RowMap map, RowAddr sa,
-                           RowAddr da, int bcast_limbs, long bcast_stride, double center) {
+                           RowAddr da, int bcast_limbs, long bcast_stride, double center,
+                           const u64* __restrict__ rs_in = nullptr, u64* rs_out = nullptr,
+                           const double2* __restrict__ rs_inv_d = nullptr, int rs_level = 0) {
   __shared__ double blk[1024];   // this CTA's 1024-point block (phase B)
   __shared__ double xch[1024];   // inverse: the 4 x 256 cross-block values (phase A)
   const int row = blockIdx.x >> 2;
@@ -103,9 +105,15 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kRcThreads, PF ? 1 :
       wc[i] = twc(i);
     }
   }
-  auto WA = [&](int i) { return PF ? wa[PF ? i : 0] : twa(i); };
-  auto WB = [&](int i) { return PF ? wb[PF ? i : 0] : twb(i); };
-  auto WC = [&](int i) { return PF ? wc[PF ? i : 0] : twc(i); };
+  auto WA = [&](int i) {
+    if constexpr (PF) return wa[i]; else return twa(i);
+  };
+  auto WB = [&](int i) {
+    if constexpr (PF) return wb[i]; else return twb(i);
+  };
+  auto WC = [&](int i) {
+    if constexpr (PF) return wc[i]; else return twc(i);
+  };
   const double2 w0 = __ldg(tw + 1), w1a = __ldg(tw + 2), w1b = __ldg(tw + 3);
   // broadcast input (forward only): row r reads row r / bcast_limbs of src,
   // centred about `center` when nonzero (the rescale correction, as RowsTile)
@@ -150,13 +158,33 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kRcThreads, PF ? 1 :
         __syncthreads();
       } else {
         // last step: b = 4 t, four consecutive outputs
-        u64* o = d_row + 1024 * k + b;
-        *reinterpret_cast<ulonglong2*>(o) =
-            make_ulonglong2(fp_canon_half(fp_reduce(y0, qd), qd.x),
-                            fp_canon_half(fp_reduce(y1, qd), qd.x));
-        *reinterpret_cast<ulonglong2*>(o + 2) =
-            make_ulonglong2(fp_canon_half(fp_reduce(y2, qd), qd.x),
-                            fp_canon_half(fp_reduce(y3, qd), qd.x));
+        if (rs_in) {
+          // rescale finish: (in - correction) * q_last^-1 on the FP64 pipe
+          // (|in - x| < 1.5 q, one product, canonical word), written to the
+          // new level's row (poly, j) -- the word launch_modswitch_finish makes
+          const int nl = rs_level - 1, poly = row / nl, j = row - poly * nl;
+          const long off = 1024 * (long)k + b;
+          const ulonglong2 i01 =
+              *reinterpret_cast<const ulonglong2*>(rs_in + ((long)poly * rs_level + j) * 4096 + off);
+          const ulonglong2 i23 = *reinterpret_cast<const ulonglong2*>(
+              rs_in + ((long)poly * rs_level + j) * 4096 + off + 2);
+          const double2 iv = rs_inv_d[j];
+          auto fin = [&](u64 a, double y) {
+            const double d = __dadd_rn(fp_from_u52(a), -fp_reduce(y, qd));
+            return fp_canon_half(fp_mulmod(d, iv, qd.x), qd.x);
+          };
+          u64* o = rs_out + ((long)poly * nl + j) * 4096 + off;
+          *reinterpret_cast<ulonglong2*>(o) = make_ulonglong2(fin(i01.x, y0), fin(i01.y, y1));
+          *reinterpret_cast<ulonglong2*>(o + 2) = make_ulonglong2(fin(i23.x, y2), fin(i23.y, y3));
+        } else {
+          u64* o = d_row + 1024 * k + b;
+          *reinterpret_cast<ulonglong2*>(o) =
+              make_ulonglong2(fp_canon_half(fp_reduce(y0, qd), qd.x),
+                              fp_canon_half(fp_reduce(y1, qd), qd.x));
+          *reinterpret_cast<ulonglong2*>(o + 2) =
+              make_ulonglong2(fp_canon_half(fp_reduce(y2, qd), qd.x),
+                              fp_canon_half(fp_reduce(y3, qd), qd.x));
+        }
       }
     }
   } else {
