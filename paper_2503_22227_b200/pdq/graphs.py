@@ -34,7 +34,8 @@ import numpy as np
 
 from ..pools import MemoryPool
 from ..rnspoly import CData
-from ..schemes.ckks import (CkksCiphertext, CkksPlaintext, ckks_multiply_plain, ckks_rescale)
+from ..schemes.ckks import (CkksCiphertext, CkksPlaintext, ckks_multiply_plain, ckks_rescale,
+                            embed_inverse, encode_embedded)
 from .engine import PdqEngine, QueryResult, QuerySpec
 
 
@@ -153,7 +154,10 @@ class CapturedQuery:
         e = cfg.mask_exp_range
         r = rng.uniform(2.0 ** -e, 2.0 ** e, ev.slots)
         r *= rng.choice([-1.0, 1.0], ev.slots)
-        pt1 = ev.encode(r, level=ct.level, scale=ev._q_last(ct))
+        # r is encoded twice (at the masked and the fresh ciphertext's level):
+        # one embedding, two scalings -- the words ev.encode gives each time
+        emb = embed_inverse(r.astype(np.complex128), ev.ctx.n)
+        pt1 = encode_embedded(ev.ctx, emb, ev._q_last(ct), ct.level)
 
         def mask(p):
             out = ckks_rescale(ev.ctx, ckks_multiply_plain(ev.ctx, ct, p))
@@ -162,7 +166,7 @@ class CapturedQuery:
 
         masked = self._staged("mask", (ct.level, ct.scale, pt1.scale), mask, [pt1])
         fresh, flags = channel.reciprocal(masked)
-        pt = ev.encode(r, level=fresh.level, scale=ev._q_last(fresh))
+        pt = encode_embedded(ev.ctx, emb, ev._q_last(fresh), fresh.level)
         cts = self._staged("post", (fresh.level, fresh.scale, pt.scale),
                            lambda f, p: self._post(parts, f, p), [fresh, pt])
         return QueryResult(self.spec.agg, cts, {"recip_flags": flags.tolist()})

@@ -146,7 +146,14 @@ def ckks_encode(ctx: Context, values, scale: float | None = None,
         raise ParameterError(f"{v.size} values exceed {half} slots")
     if v.size < half:
         v = np.concatenate([v, np.zeros(half - v.size, dtype=np.complex128)])
-    coeffs = embed_inverse(v, n) * scale
+    return encode_embedded(ctx, embed_inverse(v, n), scale, level)
+
+
+def encode_embedded(ctx: Context, emb: np.ndarray, scale: float, level: int) -> CkksPlaintext:
+    """ckks_encode from the slots' embedding (embed_inverse), so one vector
+    encoded at several scales / levels pays for one host FFT."""
+    n = ctx.n
+    coeffs = emb * scale
     peak = float(np.max(np.abs(coeffs))) if coeffs.size else 0.0
     budget = ctx.level_product(level)
     if peak * 2 >= budget:
