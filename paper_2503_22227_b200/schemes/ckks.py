@@ -149,6 +149,34 @@ def ckks_encode(ctx: Context, values, scale: float | None = None,
     return encode_embedded(ctx, embed_inverse(v, n), scale, level)
 
 
+_STAGE_RING = 4
+
+
+def _upload_f64(ctx: Context, host: np.ndarray):
+    """float64 host vector -> device, through a small ring of pinned staging
+    buffers per context (asynchronous copy; a ring slot is reused only after
+    the event of its previous copy has completed)."""
+    import torch
+
+    ring = getattr(ctx, "_f64_stage", None)
+    if ring is None or ring["n"] != host.size:
+        ring = ctx._f64_stage = {"n": host.size, "i": 0, "slots": [
+            (torch.empty(host.size, dtype=torch.float64, pin_memory=True), None)
+            for _ in range(_STAGE_RING)]}
+    i = ring["i"]
+    ring["i"] = (i + 1) % _STAGE_RING
+    buf, ev = ring["slots"][i]
+    if ev is not None:
+        ev.synchronize()
+    buf.numpy()[:] = host
+    out = torch.empty(host.size, dtype=torch.float64, device="cuda")
+    out.copy_(buf, non_blocking=True)
+    ev = torch.cuda.Event()
+    ev.record()
+    ring["slots"][i] = (buf, ev)
+    return out
+
+
 def encode_embedded(ctx: Context, emb: np.ndarray, scale: float, level: int) -> CkksPlaintext:
     """ckks_encode from the slots' embedding (embed_inverse), so one vector
     encoded at several scales / levels pays for one host FFT."""
@@ -165,7 +193,7 @@ def encode_embedded(ctx: Context, emb: np.ndarray, scale: float, level: int) -> 
     # doubles themselves (fhe_real_lift): N words go up instead of L x N
     import torch
 
-    vals = torch.from_numpy(np.ascontiguousarray(rounded, dtype=np.float64)).cuda()
+    vals = _upload_f64(ctx, rounded)
     cd = cdata_new(ctx.pool, 1, level, n, zero=False)
     _native.check(_native.lib().fhe_real_lift(ctx.chain.handle, cd.view().data_ptr(),
                                               vals.data_ptr(), n, level, 0,
