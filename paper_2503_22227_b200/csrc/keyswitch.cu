@@ -931,22 +931,36 @@ __global__ void __launch_bounds__(kThreads)
     const double2 qd = ch.qd[p];
     const u64 q = ch.mc[p].q;
     {
+      // digits in chunks of 8: the chunk's 24 words are all loaded before
+      // any is used (one memory latency per chunk instead of one per few
+      // digits), then summed in digit order, reduced after every 8 terms
       double sb = 0.0, sa = 0.0;
-#pragma unroll 4
-      for (int di = 0; di < D; ++di) {
-        const int s0 = sinfo[4 * di], na = sinfo[4 * di + 1], ro = sinfo[4 * di + 2];
-        const bool own = m >= s0 && m < s0 + na;
-        const u64* src = own ? d + b * d_stride + (long)m * n + i
-                             : ext + b * ext_stride + (long)(ro + (m < s0 ? m : m - na)) * n + i;
-        const double x = fp_from_u52(__ldg(src));
-        const double kbv = fp_from_u52(__ldg(key + ((long)(2 * di) * keyL + p) * n + i));
-        const double kav = fp_from_u52(__ldg(key + ((long)(2 * di + 1) * keyL + p) * n + i));
-        sb = __dadd_rn(sb, fp_mulmod(x, make_double2(kbv, __dmul_rn(kbv, qd.y)), qd.x));
-        sa = __dadd_rn(sa, fp_mulmod(x, make_double2(kav, __dmul_rn(kav, qd.y)), qd.x));
-        if ((di & 7) == 7) {
-          sb = fp_reduce(sb, qd);
-          sa = fp_reduce(sa, qd);
+      for (int d0 = 0; d0 < D; d0 += 8) {
+        u64 xw[8], bw[8], aw[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int di = d0 + u;
+          if (di < D) {
+            const int s0 = sinfo[4 * di], na = sinfo[4 * di + 1], ro = sinfo[4 * di + 2];
+            const bool own = m >= s0 && m < s0 + na;
+            const u64* src = own ? d + b * d_stride + (long)m * n + i
+                                 : ext + b * ext_stride + (long)(ro + (m < s0 ? m : m - na)) * n + i;
+            xw[u] = __ldg(src);
+            bw[u] = __ldg(key + ((long)(2 * di) * keyL + p) * n + i);
+            aw[u] = __ldg(key + ((long)(2 * di + 1) * keyL + p) * n + i);
+          }
         }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          if (d0 + u < D) {
+            const double x = fp_from_u52(xw[u]);
+            const double kbv = fp_from_u52(bw[u]), kav = fp_from_u52(aw[u]);
+            sb = __dadd_rn(sb, fp_mulmod(x, make_double2(kbv, __dmul_rn(kbv, qd.y)), qd.x));
+            sa = __dadd_rn(sa, fp_mulmod(x, make_double2(kav, __dmul_rn(kav, qd.y)), qd.x));
+          }
+        }
+        sb = fp_reduce(sb, qd);
+        sa = fp_reduce(sa, qd);
       }
       const u64 rb = fp_canon_half(fp_reduce(sb, qd), qd.x);
       const u64 ra = fp_canon_half(fp_reduce(sa, qd), qd.x);
