@@ -49,3 +49,19 @@ def test_rejection_heavy_ranges():
     for lo, hi, n in ((0, (1 << 31) + 1, 3000), (0, (1 << 62) + 1, 100)):
         got = r.integers_device(lo, hi, n).cpu().numpy().view(np.uint64)
         assert np.array_equal(got, g.integers(lo, hi, size=n, dtype=np.uint64))
+
+
+def test_cbd_pair_draw_equals_two_host_draws():
+    """cbd_error_pair_device (one flip draw for e0 and e1, ckks_encrypt) gives
+    the words of two consecutive host cbd_error draws and leaves the stream
+    where they leave it."""
+    from paper_2503_22227_b200.coremath.sampling import Rng
+
+    for seed, n in ((11, 4096), (12, 1 << 16), (13, 17)):
+        a = Rng(int(seed).to_bytes(32, "little"))
+        b = Rng(int(seed).to_bytes(32, "little"))
+        assert np.array_equal(a.ternary_device(n).cpu().numpy(), b.ternary(n))
+        e0, e1 = a.cbd_error_pair_device(n)
+        assert np.array_equal(e0.cpu().numpy(), b.cbd_error(n))
+        assert np.array_equal(e1.cpu().numpy(), b.cbd_error(n))
+        assert np.array_equal(a.ternary(n), b.ternary(n))  # same state afterwards
