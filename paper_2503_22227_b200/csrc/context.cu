@@ -140,17 +140,28 @@ int build_chain(const u64* primes, int count, int log_n, FheChain* ch) {
     const u64 w1 = n >= 2 ? itw[p * n + 1].w : 1;
     ninv_w1[p] = wpair(mulmod_h(w1, ni, q), q);
   }
-  bool fp64 = true;
-  for (int p = 0; p < count; ++p) fp64 &= primes[p] < ((u64)1 << 50);
+  // FP64 tables are built for every prime below 2^50; the chain is an FP64
+  // chain (fp64_ok) when all are.  A mixed chain (e.g. 50-bit Q, 60-bit P)
+  // still runs the transforms whose rows all use eligible primes on the FP64
+  // path (launch_ntt); everything else stays on the integer path.
+  bool fp64 = true, fp64_any = false;
+  ch->fp64_prime.assign(count, 0);
+  for (int p = 0; p < count; ++p) {
+    const bool e = primes[p] < ((u64)1 << 50);
+    ch->fp64_prime[p] = e ? 1 : 0;
+    fp64 &= e;
+    fp64_any |= e;
+  }
   std::vector<double2> twd, itwd, tws, qd(count), nid(count), nwd(count);
   // staged tables: per prime and direction N1 column pairs + N chunk pairs
   // (N <= 2^12: the whole-row plan's table, n pairs per direction)
   const size_t tws_dir = log_n >= 13 ? n + ((size_t)1 << split_log_n1(log_n)) : n;
-  if (fp64) {
-    twd.resize(count * n);
-    itwd.resize(count * n);
+  if (fp64_any) {
+    twd.assign(count * n, make_double2(0.0, 0.0));
+    itwd.assign(count * n, make_double2(0.0, 0.0));
     tws.assign(count * 2 * tws_dir, make_double2(0.0, 0.0));
     for (int p = 0; p < count; ++p) {
+      if (!ch->fp64_prime[p]) continue;
       const double q = (double)primes[p];
       // signed representatives |w| <= q/2: |x w / q| <= |x| / 2, so the FP64
       // butterflies accept inputs up to 2^52 (lazier reductions, ntt.cu)
@@ -217,12 +228,13 @@ int build_chain(const u64* primes, int count, int log_n, FheChain* ch) {
   ch->dev.lazy_ok = true;
   for (int p = 0; p < count; ++p) ch->dev.lazy_ok &= primes[p] < ((u64)1 << 58);
   ch->dev.fp64_ok = fp64;
-  ch->dev.twd = fp64 ? (const double2*)(b + o_twd) : nullptr;
-  ch->dev.itwd = fp64 ? (const double2*)(b + o_itwd) : nullptr;
-  ch->dev.qd = fp64 ? (const double2*)(b + o_qd) : nullptr;
-  ch->dev.ninv_d = fp64 ? (const double2*)(b + o_nid) : nullptr;
-  ch->dev.ninv_w1_d = fp64 ? (const double2*)(b + o_nwd) : nullptr;
-  ch->dev.tws = fp64 ? (const double2*)(b + o_tws) : nullptr;
+  ch->dev.twd = fp64_any ? (const double2*)(b + o_twd) : nullptr;
+  ch->dev.itwd = fp64_any ? (const double2*)(b + o_itwd) : nullptr;
+  ch->dev.qd = fp64_any ? (const double2*)(b + o_qd) : nullptr;
+  ch->dev.ninv_d = fp64_any ? (const double2*)(b + o_nid) : nullptr;
+  ch->dev.ninv_w1_d = fp64_any ? (const double2*)(b + o_nwd) : nullptr;
+  ch->dev.tws = fp64_any ? (const double2*)(b + o_tws) : nullptr;
+  ch->dev.fp64_prime_host = ch->fp64_prime.data();
   ch->dev.tws_dir = (long)tws_dir;
   ch->dev.fuse = fuse_scratch_new(log_n);
   if (!ch->dev.fuse) {

@@ -12,6 +12,7 @@ struct FheChain {
   int log_n = 0;
   std::vector<u64> primes;
   std::vector<u64> psi;  // smallest primitive 2N-th root per prime
+  std::vector<unsigned char> fp64_prime;  // per prime: < 2^50 (FP64 tables valid)
   void* dmem = nullptr;  // one allocation for all tables
   size_t dbytes = 0;
 };

@@ -42,6 +42,10 @@ struct DevChain {
   long tws_dir;
   // host-side scratch of the fused four-step NTT (FuseScratch*, ntt.cu)
   void* fuse;
+  // HOST pointer (never read on the device): per prime, 1 when its FP64
+  // tables are valid (< 2^50); lets a mixed chain run FP64 transforms on
+  // rows that only use such primes (launch_ntt)
+  const unsigned char* fp64_prime_host;
 };
 
 // Row -> chain position mapping used by every batched kernel.  The

@@ -1281,8 +1281,37 @@ int launch_split(const DevChain& ch, const NttArgs& a, bool inverse, bool lazy,
 
 }  // namespace
 
+static int launch_ntt_chain(const DevChain& ch, const NttArgs& a, bool inverse, cudaStream_t st);
+
+// FHE_NTT_MIXED_FP64=0: a mixed chain's transforms all stay on the integer path
+static bool mixed_fp64_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("FHE_NTT_MIXED_FP64");
+    on = (e && e[0] == '0') ? 0 : 1;
+  }
+  return on == 1;
+}
+
 int launch_ntt(const DevChain& ch, const NttArgs& a, bool inverse, cudaStream_t st) {
   if (a.rows <= 0) return 0;
+  // mixed chain (some prime >= 2^50): a transform whose rows only use primes
+  // below 2^50 (identity map over a prime range) runs on the FP64 path --
+  // same canonical words as the integer path
+  if (!ch.fp64_ok && ch.twd && ch.fp64_prime_host && a.map.idx == nullptr &&
+      mixed_fp64_enabled()) {
+    bool ok = a.map.offset >= 0 && a.map.limbs > 0 && a.map.offset + a.map.limbs <= ch.count;
+    for (int j = 0; ok && j < a.map.limbs; ++j) ok = ch.fp64_prime_host[a.map.offset + j] != 0;
+    if (ok) {
+      DevChain c2 = ch;
+      c2.fp64_ok = true;
+      return launch_ntt_chain(c2, a, inverse, st);
+    }
+  }
+  return launch_ntt_chain(ch, a, inverse, st);
+}
+
+static int launch_ntt_chain(const DevChain& ch, const NttArgs& a, bool inverse, cudaStream_t st) {
   const bool lazy = !inverse && ch.lazy_ok;
   switch (ch.log_n) {
     case 1: return launch_rows<1>(ch, a, inverse, lazy, st);
