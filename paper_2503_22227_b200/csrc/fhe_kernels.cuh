@@ -55,6 +55,9 @@ struct NttArgs {
   const double2* rs_inv_d = nullptr;
   int rs_level = 0;
   bool* rs_done = nullptr;
+  // caller's assertion: every row's prime is < 2^50 (a mixed chain may then
+  // run this transform on the FP64 path; launch_ntt)
+  bool fp64_rows = false;
 };
 int launch_ntt(const DevChain& ch, const NttArgs& a, bool inverse, cudaStream_t st);
 unsigned long long ntt_path_count(int path);

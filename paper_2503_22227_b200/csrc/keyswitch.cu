@@ -1201,7 +1201,27 @@ int run_keyswitch(const FheContext& ctx, int level, const u64* d, long d_stride,
                                                  lp.up_w, level, K, L, chunk);
       FHE_LAUNCH_CHECK();
     }
-    if (lp.ext_rows > 0) {
+    // mixed chain (Q < 2^50, P >= 2^50): per digit, the Q-target rows (the
+    // first level - na of its block) transform on the FP64 path and the K
+    // P-target rows on the integer path, instead of the whole ext block on
+    // the integer path
+    bool q_fp64 = !ch.fp64_ok && ch.twd && K > 0;
+    for (int j = 0; q_fp64 && j < level; ++j) q_fp64 = ctx.chain->fp64_prime[j] != 0;
+    if (lp.ext_rows > 0 && q_fp64) {
+      const long bs = (long)lp.ext_rows * n;
+      for (int di = 0; di < lp.digits; ++di) {
+        const int ro = lp.dig_row_off[di], nq = level - lp.dig_na[di];
+        for (int part = 0; part < 2; ++part) {
+          const int r0 = part ? ro + nq : ro, cnt = part ? K : nq;
+          if (cnt <= 0) continue;
+          NttArgs na{ext + (long)r0 * n, ext + (long)r0 * n, batch * cnt,
+                     RowMap{lp.ext_prime + r0, cnt, 0}, bs, bs};
+          na.fp64_rows = part == 0;
+          rc = launch_ntt(ch, na, false, st);
+          if (rc) return rc;
+        }
+      }
+    } else if (lp.ext_rows > 0) {
       rc = launch_ntt(ch, ext, ext, batch * lp.ext_rows,
                       RowMap{lp.ext_prime, lp.ext_rows, 0}, false, st);
       if (rc) return rc;

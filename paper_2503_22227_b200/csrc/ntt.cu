@@ -1298,10 +1298,12 @@ int launch_ntt(const DevChain& ch, const NttArgs& a, bool inverse, cudaStream_t 
   // mixed chain (some prime >= 2^50): a transform whose rows only use primes
   // below 2^50 (identity map over a prime range) runs on the FP64 path --
   // same canonical words as the integer path
-  if (!ch.fp64_ok && ch.twd && ch.fp64_prime_host && a.map.idx == nullptr &&
+  if (!ch.fp64_ok && ch.twd && ch.fp64_prime_host && (a.map.idx == nullptr || a.fp64_rows) &&
       mixed_fp64_enabled()) {
-    bool ok = a.map.offset >= 0 && a.map.limbs > 0 && a.map.offset + a.map.limbs <= ch.count;
-    for (int j = 0; ok && j < a.map.limbs; ++j) ok = ch.fp64_prime_host[a.map.offset + j] != 0;
+    bool ok = a.fp64_rows ||
+              (a.map.offset >= 0 && a.map.limbs > 0 && a.map.offset + a.map.limbs <= ch.count);
+    for (int j = 0; ok && !a.fp64_rows && j < a.map.limbs; ++j)
+      ok = ch.fp64_prime_host[a.map.offset + j] != 0;
     if (ok) {
       DevChain c2 = ch;
       c2.fp64_ok = true;
