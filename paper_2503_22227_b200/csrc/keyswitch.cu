@@ -126,14 +126,14 @@ __global__ void __launch_bounds__(kThreads)
                     int keyL, const int* __restrict__ dig_info, int D, int level, int K, int L,
                     u64* __restrict__ accQ, u64* __restrict__ accP, const u64* add0,
                     const u64* add1, long add_stride, u64* out0, u64* out1, long out_stride,
-                    int batch, int chunk) {
+                    int batch, int chunk, int m_begin = 0, int m_end = -1) {
   extern __shared__ int sinfo[];
   for (int i = threadIdx.x; i < 4 * D; i += blockDim.x) sinfo[i] = dig_info[i];
   __syncthreads();
   const int log_n = ch.log_n;
   const long n = 1L << log_n;
-  const long total = (long)(level + K) << log_n;
-  for (long t = blockIdx.x * (long)blockDim.x + threadIdx.x; t < total;
+  const long total = (long)(m_end < 0 ? level + K : m_end) << log_n;
+  for (long t = ((long)m_begin << log_n) + blockIdx.x * (long)blockDim.x + threadIdx.x; t < total;
        t += (long)gridDim.x * blockDim.x) {
     const int m = (int)(t >> log_n);
     const long i = t & (n - 1);
@@ -1000,6 +1000,16 @@ static bool rescale_fin_fused_enabled() {
   return on == 1;
 }
 
+// FHE_MIXED_KS=0: a mixed chain's key switch stays entirely on the integer path
+static bool mixed_keyswitch_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("FHE_MIXED_KS");
+    on = (e && e[0] == '0') ? 0 : 1;
+  }
+  return on == 1;
+}
+
 // FHE_BCAST_MODUP=0: per-prime gadget ModUp through the conversion kernel
 static bool bcast_modup_enabled() {
   static int on = -1;
@@ -1142,6 +1152,11 @@ int run_keyswitch(const FheContext& ctx, int level, const u64* d, long d_stride,
   // re-read).  The words c_d < 2^50 enter the FP64 butterflies unreduced,
   // which stay below 2^52 until the first lazy reduction (stage 3); the
   // transform's canonical output is NTT_m(c_d mod q_m) word for word.
+  // mixed chain whose Q primes are all < 2^50 (P >= 2^50): the Q-limb parts
+  // of the ext transform and of the inner product take the FP64 pipe
+  bool mixed_q_fp64 = !ch.fp64_ok && ch.twd && K > 0 && mixed_keyswitch_enabled();
+  for (int j = 0; mixed_q_fp64 && j < level; ++j)
+    mixed_q_fp64 = ctx.chain->fp64_prime[j] != 0;
   bool modup_done = false;
   if (lp.max_na == 1 && K == 0 && ch.fp64_ok && log_n <= 12 && lp.ext_rows > 0 &&
       bcast_modup_enabled()) {
@@ -1205,9 +1220,7 @@ int run_keyswitch(const FheContext& ctx, int level, const u64* d, long d_stride,
     // first level - na of its block) transform on the FP64 path and the K
     // P-target rows on the integer path, instead of the whole ext block on
     // the integer path
-    bool q_fp64 = !ch.fp64_ok && ch.twd && K > 0;
-    for (int j = 0; q_fp64 && j < level; ++j) q_fp64 = ctx.chain->fp64_prime[j] != 0;
-    if (lp.ext_rows > 0 && q_fp64) {
+    if (lp.ext_rows > 0 && mixed_q_fp64) {
       const long bs = (long)lp.ext_rows * n;
       for (int di = 0; di < lp.digits; ++di) {
         const int ro = lp.dig_row_off[di], nq = level - lp.dig_na[di];
@@ -1266,7 +1279,25 @@ int run_keyswitch(const FheContext& ctx, int level, const u64* d, long d_stride,
                  4 * lp.digits * sizeof(int), st, ch, d, d_stride, ext, (long)lp.ext_rows * n, key,
                  L + K, lp.dig_info, lp.digits, level, K, L, accQ, accP, add0, add1, add_stride,
                  out0, out1, out_stride, batch);
-    else
+    else if (mixed_q_fp64 && lp.digits <= 4 && K > 0 && !fin_inner) {
+      // mixed chain: the Q limbs' inner product on the FP64 pipe, the P
+      // limbs' on the integer pipe (same words)
+      const long wq = (long)level << log_n, wp = (long)K << log_n;
+      auto goq = [&](auto kern) {
+        kern<<<grid_for(wq), kThreads, 4 * lp.digits * sizeof(int), st>>>(
+            ch, d, d_stride, ext, (long)lp.ext_rows * n, key, L + K, lp.dig_info, lp.digits,
+            level, K, L, accQ, accP, add0, add1, add_stride, out0, out1, out_stride, batch, 0,
+            level, nullptr, nullptr);
+      };
+      if (lp.digits <= 2) goq(ks_inner_fp_kernel<2>);
+      else if (lp.digits == 3) goq(ks_inner_fp_kernel<3>);
+      else goq(ks_inner_fp_kernel<4>);
+      FHE_LAUNCH_CHECK();
+      ks_inner_kernel<<<grid_for(wp), kThreads, 4 * lp.digits * sizeof(int), st>>>(
+          ch, d, d_stride, ext, (long)lp.ext_rows * n, key, L + K, lp.dig_info, lp.digits, level,
+          K, L, accQ, accP, add0, add1, add_stride, out0, out1, out_stride, batch, chunk, level,
+          level + K);
+    } else
       ks_inner_kernel<<<grid_for(work), kThreads, 4 * lp.digits * sizeof(int), st>>>(
           ch, d, d_stride, ext, (long)lp.ext_rows * n, key, L + K, lp.dig_info, lp.digits, level,
           K, L, accQ, accP, add0, add1, add_stride, out0, out1, out_stride, batch, chunk);
