@@ -62,10 +62,26 @@ inline size_t bconv_umma_smem(int max_nt, int ks) {
          (size_t)(4 + 2 * kBuNbuf) * 8 + 16;
 }
 
-template <int KS, bool FPPRO>
+// 79-bit form of bc_combine71 for targets p >= 2^56 (8 byte columns, sh >=
+// 56): V = sum_{b<8} P_b 2^(8b) < 2^79, x = V >> sh < 2^23, mu = floor(2^79
+// / p) < 2^23, qe = (x mu) >> (79 - sh) short of V / p by at most 2, r < 3p <
+// 2^64 from the low words.
+__device__ __forceinline__ u64 bc_combine79(const unsigned (&a)[8], const BcTarget& tg) {
+  const u64 v = (u64)a[0] + ((u64)a[1] << 8) + ((u64)a[2] << 16) + ((u64)a[3] << 24);
+  const u64 h = (u64)a[4] + ((u64)a[5] << 8) + ((u64)a[6] << 16) + ((u64)a[7] << 24);
+  const u64 lo = v + (h << 32);
+  const u64 hi = (h >> 32) + (lo < v ? 1 : 0);
+  const u64 x = (hi << (64 - tg.sh)) | (lo >> tg.sh);
+  const u64 qe = (x * (u64)tg.mu) >> (79 - tg.sh);
+  u64 r = lo - qe * tg.p;
+  r = csub(r, tg.p);
+  return csub(r, tg.p);
+}
+
+template <int KS, bool FPPRO, int SB = 7>
 __global__ void __launch_bounds__(kBuThreads, FHE_BU_MINB)
     bconv_umma_kernel(const DevChain ch, const BconvArgs a) {
-  constexpr int SMAX = (32 * KS) / 7;
+  constexpr int SMAX = (32 * KS) / SB;
   constexpr int AB = bu_abytes(KS);
   extern __shared__ __align__(128) unsigned char bu_smem[];
   int ns = a.ns, nt = a.nt, s0 = 0, row_off = 0, buo = 0;
@@ -100,7 +116,8 @@ __global__ void __launch_bounds__(kBuThreads, FHE_BU_MINB)
   for (int t = tid; t < ng; t += kBuThreads) {
     if (t < nt) {
       const ModConst m = ch.mc[a.tgt_prime ? a.tgt_prime[row_off + t] : t];
-      tgs[t] = BcTarget{m.q, (u32)(m.mu >> (m.s - 7)), (u32)m.s};
+      // mu = floor(2^71 / p), or floor(2^79 / p) for a wide target (sh >= 56)
+      tgs[t] = BcTarget{m.q, (u32)(m.mu >> (m.s >= 56 ? m.s - 15 : m.s - 7)), (u32)m.s};
     } else {
       tgs[t] = BcTarget{1, 0, 39};
     }
@@ -164,11 +181,16 @@ __global__ void __launch_bounds__(kBuThreads, FHE_BU_MINB)
             const WPair iv = sinvi[k];
             y = shoup_mul(xs[k], iv.w, iv.sh, sqi[k]);
           }
-          const int bit = 56 * k, wi = bit >> 5, sh = bit & 31;
-          const u64 lo64 = y << sh;
-          w[wi] |= (unsigned)lo64;
-          w[wi + 1] |= (unsigned)(lo64 >> 32);
-          if (sh > 8) w[wi + 2] |= (unsigned)(y >> (64 - sh));
+          if constexpr (SB == 8) {
+            w[2 * k] = (unsigned)y;
+            w[2 * k + 1] = (unsigned)(y >> 32);
+          } else {
+            const int bit = 56 * k, wi = bit >> 5, sh = bit & 31;
+            const u64 lo64 = y << sh;
+            w[wi] |= (unsigned)lo64;
+            w[wi + 1] |= (unsigned)(lo64 >> 32);
+            if (sh > 8) w[wi + 2] |= (unsigned)(y >> (64 - sh));
+          }
         }
       }
       umma_mbar_wait(&a_empty[s], ((it >> 1) & 1) ^ 1);  // stage s free (MMAs done)
@@ -204,8 +226,9 @@ __global__ void __launch_bounds__(kBuThreads, FHE_BU_MINB)
         for (int tl = 0; tl < TH; ++tl) {
           if (tb + tl < nt) {
             const BcTarget tg = tgs[tb + tl];  // one LDS.128
-            *o = bc_combine71(r[tl][0], r[tl][1], r[tl][2], r[tl][3], r[tl][4], r[tl][5],
-                              r[tl][6], tg);
+            *o = tg.sh >= 56 ? bc_combine79(r[tl], tg)
+                             : bc_combine71(r[tl][0], r[tl][1], r[tl][2], r[tl][3], r[tl][4],
+                                            r[tl][5], r[tl][6], tg);
           }
           o += n;
         }
@@ -247,7 +270,7 @@ __global__ void __launch_bounds__(kBuThreads, FHE_BU_MINB)
   }
 }
 
-template <int KS>
+template <int KS, int SB>
 int launch_bconv_umma_ks(const DevChain& ch, const BconvArgs& a, int max_nt, dim3 grid,
                          cudaStream_t st) {
   const size_t smem = bconv_umma_smem(max_nt, KS);
@@ -259,18 +282,30 @@ int launch_bconv_umma_ks(const DevChain& ch, const BconvArgs& a, int max_nt, dim
     FHE_LAUNCH_CHECK();
     return 0;
   };
-  return (ch.fp64_ok && a.inv_d) ? go(bconv_umma_kernel<KS, true>)
-                                 : go(bconv_umma_kernel<KS, false>);
+  return (ch.fp64_ok && a.inv_d) ? go(bconv_umma_kernel<KS, true, SB>)
+                                 : go(bconv_umma_kernel<KS, false, SB>);
 }
 
-// grid.x CTAs per job, each looping over 128-coefficient tiles (n >= 128)
+// grid.x CTAs per job, each looping over 128-coefficient tiles (n >= 128);
+// sb bytes per source word (7, or 8 for sources >= 2^56)
 int launch_bconv_umma(const DevChain& ch, const BconvArgs& a, int max_ns, int max_nt, dim3 grid,
-                      cudaStream_t st) {
+                      cudaStream_t st, int sb = 7) {
+  if (sb == 8) {
+    switch ((8 * max_ns + 31) / 32) {
+      case 1: return launch_bconv_umma_ks<1, 8>(ch, a, max_nt, grid, st);
+      case 2: return launch_bconv_umma_ks<2, 8>(ch, a, max_nt, grid, st);
+      case 3: return launch_bconv_umma_ks<3, 8>(ch, a, max_nt, grid, st);
+      case 4: return launch_bconv_umma_ks<4, 8>(ch, a, max_nt, grid, st);
+      default:
+        fhe_set_error("tcgen05 base conversion: more than 16 wide source limbs");
+        return -1;
+    }
+  }
   switch (bconv_ks(max_ns)) {
-    case 1: return launch_bconv_umma_ks<1>(ch, a, max_nt, grid, st);
-    case 2: return launch_bconv_umma_ks<2>(ch, a, max_nt, grid, st);
-    case 3: return launch_bconv_umma_ks<3>(ch, a, max_nt, grid, st);
-    case 4: return launch_bconv_umma_ks<4>(ch, a, max_nt, grid, st);
+    case 1: return launch_bconv_umma_ks<1, 7>(ch, a, max_nt, grid, st);
+    case 2: return launch_bconv_umma_ks<2, 7>(ch, a, max_nt, grid, st);
+    case 3: return launch_bconv_umma_ks<3, 7>(ch, a, max_nt, grid, st);
+    case 4: return launch_bconv_umma_ks<4, 7>(ch, a, max_nt, grid, st);
     default:
       fhe_set_error("tcgen05 base conversion: more than 16 source limbs");
       return -1;

@@ -327,19 +327,21 @@ static void pack_bfrag2(std::vector<uint2>& out, int ns, int nt, int ks, W w, P 
 // k = 7 s + a, in the canonical no-swizzle layout [k16 chunk][t][b][16 B]
 // with the target count padded to a multiple of 8 (whole MMA chunks).
 template <class W, class P>
-static void pack_bumma(std::vector<uint4>& out, int ns, int nt, int ks, W w, P p) {
-  std::vector<u64> v((size_t)ns * 7 * nt);
+static void pack_bumma(std::vector<uint4>& out, int ns, int nt, int ks, W w, P p, int sb = 7) {
+  // sb bytes per source word (7: sources < 2^56, 8: wider); byte columns b =
+  // 0..7 of each target ([w 2^(8a)]_p has a nonzero byte 7 only for p >= 2^56)
+  std::vector<u64> v((size_t)ns * sb * nt);
   for (int s = 0; s < ns; ++s)
     for (int t = 0; t < nt; ++t) {
       const u64 pt = p(t);
       u64 x = w(s, t) % pt;
-      for (int a = 0; a < 7; ++a) {
-        v[((size_t)s * 7 + a) * nt + t] = x;
+      for (int a = 0; a < sb; ++a) {
+        v[((size_t)s * sb + a) * nt + t] = x;
         x = mulmod_h(x, 256 % pt, pt);
       }
     }
   auto byte = [&](int k, int t, int b) -> unsigned {
-    if (k >= 7 * ns || t >= nt || b >= 7) return 0;
+    if (k >= sb * ns || t >= nt) return 0;
     return (unsigned)((v[(size_t)k * nt + t] >> (8 * b)) & 0xff);
   };
   const int ng = (nt + 7) & ~7;
@@ -444,36 +446,51 @@ int build_levels(FheContext* ctx) {
           down_w_d.push_back(make_double2((double)w, (double)w / (double)pr[j]));
         }
     }
-    // tensor-core base conversion tables (every chain prime < 2^56)
-    bool bf_ok = K <= 16;
-    for (u64 q : pr) bf_ok &= q < ((u64)1 << 56) && q >= ((u64)1 << 39);  // bc_reduce71 domain
+    // tensor-core base conversion tables: every prime in [2^39, 2^62); the
+    // mma.sync kernels need all < 2^56 (narrow), the tcgen05 kernel also takes
+    // wider primes (8-byte source words, 79-bit sums before the reduction)
+    bool bf_ok = K <= 16, narrow = true, q_narrow = true, p_narrow = true;
+    for (int j = 0; j < L + K; ++j) {
+      const u64 q = pr[j];
+      bf_ok &= q < ((u64)1 << 62) && q >= ((u64)1 << 39);
+      const bool nq = q < ((u64)1 << 56);
+      narrow &= nq;
+      (j < L ? q_narrow : p_narrow) &= nq;
+    }
+    lp.bf_wide = !narrow;
+    lp.up_sb = q_narrow ? 7 : 8;
+    lp.down_sb = p_narrow ? 7 : 8;
     std::vector<uint2> up_bf, down_bf, up_bf2, down_bf2;
     std::vector<int> up_bf_off, up_bf2_off, up_bu_off;
     std::vector<uint4> up_bu, down_bu;
     if (bf_ok) {
       int max_na = 0;
       for (int di = 0; di < D; ++di) max_na = std::max(max_na, lp.dig_na[di]);
-      bf_ok = max_na <= 16;
+      bf_ok = lp.up_sb * max_na <= 128 && lp.down_sb * K <= 128;  // <= 4 K-steps
       lp.max_na = max_na;
-      lp.up_ks = (7 * max_na + 31) / 32;
-      lp.down_ks = (7 * K + 31) / 32;
+      lp.up_ks = (lp.up_sb * max_na + 31) / 32;
+      lp.down_ks = (lp.down_sb * K + 31) / 32;
       for (int di = 0; bf_ok && di < D; ++di) {
         const int s0 = lp.dig_s0[di], na = lp.dig_na[di], nt = l + K - na;
         up_bf_off.push_back((int)up_bf.size());
         up_bf2_off.push_back((int)up_bf2.size());
         auto wf = [&](int s, int t) { return up_w[lp.dig_w_off[di] + s * nt + t]; };
         auto pf = [&](int t) { return pr[cp(t < s0 ? t : t + na)]; };
-        pack_bfrag(up_bf, na, nt, lp.up_ks, wf, pf);
-        pack_bfrag2(up_bf2, na, nt, lp.up_ks, wf, pf);
+        if (narrow) {
+          pack_bfrag(up_bf, na, nt, lp.up_ks, wf, pf);
+          pack_bfrag2(up_bf2, na, nt, lp.up_ks, wf, pf);
+        }
         up_bu_off.push_back((int)up_bu.size());
-        pack_bumma(up_bu, na, nt, lp.up_ks, wf, pf);
+        pack_bumma(up_bu, na, nt, lp.up_ks, wf, pf, lp.up_sb);
       }
       if (K > 0) {
         auto wf = [&](int k, int j) { return down_w[(size_t)k * l + j]; };
         auto pf = [&](int j) { return pr[j]; };
-        pack_bfrag(down_bf, K, l, lp.down_ks, wf, pf);
-        pack_bfrag2(down_bf2, K, l, lp.down_ks, wf, pf);
-        pack_bumma(down_bu, K, l, lp.down_ks, wf, pf);
+        if (narrow) {
+          pack_bfrag(down_bf, K, l, lp.down_ks, wf, pf);
+          pack_bfrag2(down_bf2, K, l, lp.down_ks, wf, pf);
+        }
+        pack_bumma(down_bu, K, l, lp.down_ks, wf, pf, lp.down_sb);
       }
     }
     lp.bf_ok = bf_ok;
@@ -542,13 +559,15 @@ int build_levels(FheContext* ctx) {
     lp.crt_Qh = (const u64*)(b + o19);
     lp.crt_inv = (const WPair*)(b + o20);
     lp.crt_qinv = (const double*)(b + o21);
-    if (bf_ok) {
+    if (bf_ok && !lp.bf_wide) {  // mma.sync fragments: narrow chains only
       lp.up_bf = (const uint2*)(b + o14);
       lp.up_bf_off = (const int*)(b + o15);
       lp.down_bf = K > 0 ? (const uint2*)(b + o16) : nullptr;
       lp.up_bf2 = (const uint2*)(b + o22);
       lp.up_bf2_off = (const int*)(b + o23);
       lp.down_bf2 = K > 0 ? (const uint2*)(b + o24) : nullptr;
+    }
+    if (bf_ok) {
       lp.up_bu = (const uint4*)(b + o25);
       lp.up_bu_off = (const int*)(b + o26);
       lp.down_bu = K > 0 ? (const uint4*)(b + o27) : nullptr;

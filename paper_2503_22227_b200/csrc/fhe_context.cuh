@@ -57,6 +57,10 @@ struct LevelPlan {
   int crt_qdrop = 0;
   bool bf_ok = false;
   int up_ks = 0, down_ks = 0, max_na = 0;
+  // wide conversion (some prime >= 2^56): source words of 8 bytes where the
+  // sources are that wide, targets reduced from 79-bit sums; tcgen05 only
+  bool bf_wide = false;
+  int up_sb = 7, down_sb = 7;  // bytes per source word, ModUp / ModDown
   const uint2* up_bf = nullptr;
   const int* up_bf_off = nullptr;
   const uint2* down_bf = nullptr;

@@ -1175,18 +1175,20 @@ int run_keyswitch(const FheContext& ctx, int level, const u64* d, long d_stride,
       max_w = std::max(max_w, lp.dig_na[di] * (level + K - lp.dig_na[di]));
     const size_t smem = (size_t)max_w * sizeof(u64);
     dim3 grid((unsigned)std::max<long>(1, std::min<long>(n / kThreads, 1024)), lp.digits, batch);
-    if (lp.bf_ok && lp.max_na >= 4 && bconv_imma_enabled()) {
+    const bool umma_up = bconv_umma_enabled() && n >= kBuTile && lp.up_bu;
+    if (lp.bf_ok && lp.max_na >= 4 && bconv_imma_enabled() && (umma_up || !lp.bf_wide)) {
       const bool l2 = bconv_layout2();
       BconvArgs ba{c, (long)level * n, ext, (long)lp.ext_rows * n, lp.dig_info,
                    l2 ? lp.up_bf2_off : lp.up_bf_off, l2 ? lp.up_bf2 : lp.up_bf, lp.up_inv,
                    lp.up_inv_d, lp.ext_prime, 0, 0, 0, level, K, l2};
       int max_nt = 0;
       for (int di = 0; di < lp.digits; ++di) max_nt = std::max(max_nt, level + K - lp.dig_na[di]);
-      if (bconv_umma_enabled() && n >= kBuTile && lp.up_bu) {
+      if (umma_up) {
         ba.bumma = lp.up_bu;
         ba.bu_off = lp.up_bu_off;
         rc = launch_bconv_umma(ch, ba, lp.max_na, max_nt,
-                               dim3(bu_grid_x(n, lp.digits * batch), lp.digits, batch), st);
+                               dim3(bu_grid_x(n, lp.digits * batch), lp.digits, batch), st,
+                               lp.up_sb);
       } else {
         dim3 g((unsigned)std::max<long>(1, std::min<long>(n / (32 * kBcWarps), 64)), lp.digits,
                batch);
@@ -1310,7 +1312,24 @@ int run_keyswitch(const FheContext& ctx, int level, const u64* d, long d_stride,
   {
     const size_t smem = (size_t)K * level * sizeof(u64);
     dim3 grid((unsigned)std::max<long>(1, std::min<long>(n / kThreads, 1024)), batch * 2);
-    if (ch.fp64_ok && lp.down_w_d) {
+    const bool umma_down = bconv_umma_enabled() && n >= kBuTile && lp.down_bu;
+    if (lp.bf_ok && K >= 4 && bconv_imma_enabled() && (umma_down || lp.down_bf)) {
+      // tensor-core conversion (tcgen05; mma.sync on narrow chains without it)
+      const bool l2 = bconv_layout2();
+      BconvArgs ba{accP, (long)K * n, conv, (long)level * n, nullptr, nullptr,
+                   l2 ? lp.down_bf2 : lp.down_bf, lp.down_inv, lp.down_inv_d, nullptr, K, level,
+                   L, level, K, l2};
+      if (umma_down) {
+        ba.bumma = lp.down_bu;
+        rc = launch_bconv_umma(ch, ba, K, level, dim3(bu_grid_x(n, batch * 2), 1, batch * 2), st,
+                               lp.down_sb);
+      } else {
+        dim3 g((unsigned)std::max<long>(1, std::min<long>(n / (32 * kBcWarps), 64)), 1,
+               batch * 2);
+        rc = launch_bconv(ch, ba, K, level, g, st);
+      }
+      if (rc) return rc;
+    } else if (ch.fp64_ok && lp.down_w_d) {
       const size_t smem_d = ((size_t)K * level + level) * sizeof(double2);
       auto go = [&](auto kern) {
         if (smem_d > 48 * 1024)
@@ -1318,27 +1337,10 @@ int run_keyswitch(const FheContext& ctx, int level, const u64* d, long d_stride,
         kern<<<grid, kThreads, smem_d, st>>>(ch, accP, conv, lp.down_inv_d, lp.down_w_d, level,
                                              K, L);
       };
-      if (lp.bf_ok && lp.down_bf && K >= 4 && bconv_imma_enabled()) {
-        const bool l2 = bconv_layout2();
-        BconvArgs ba{accP, (long)K * n, conv, (long)level * n, nullptr, nullptr,
-                     l2 ? lp.down_bf2 : lp.down_bf, lp.down_inv, lp.down_inv_d, nullptr, K, level,
-                     L, level, K, l2};
-        if (bconv_umma_enabled() && n >= kBuTile && lp.down_bu) {
-          ba.bumma = lp.down_bu;
-          rc = launch_bconv_umma(ch, ba, K, level, dim3(bu_grid_x(n, batch * 2), 1, batch * 2),
-                                 st);
-        } else {
-          dim3 g((unsigned)std::max<long>(1, std::min<long>(n / (32 * kBcWarps), 64)), 1,
-                 batch * 2);
-          rc = launch_bconv(ch, ba, K, level, g, st);
-        }
-        if (rc) return rc;
-      } else {
-        if (K <= 4) go(moddown_conv_fp_kernel<4, FHE_MODUP_U>);
-        else if (K <= 12) go(moddown_conv_fp_kernel<12, FHE_MODUP_U>);
-        else go(moddown_conv_fp_kernel<16, FHE_MODUP_U>);
-        FHE_LAUNCH_CHECK();
-      }
+      if (K <= 4) go(moddown_conv_fp_kernel<4, FHE_MODUP_U>);
+      else if (K <= 12) go(moddown_conv_fp_kernel<12, FHE_MODUP_U>);
+      else go(moddown_conv_fp_kernel<16, FHE_MODUP_U>);
+      FHE_LAUNCH_CHECK();
     } else {
       moddown_conv_kernel<<<grid, kThreads, smem, st>>>(ch, accP, conv, lp.down_inv, lp.down_w,
                                                         level, K, L, chunk);
