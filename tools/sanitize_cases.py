@@ -26,7 +26,7 @@ n = 1 << 16
 # conversion (csrc/bconv_umma.cuh) and the finish on the staged kernel;
 # ntt12: the N=2^12 row-per-cluster NTT (plain rows and the rescale
 # correction's broadcast input)
-KS_SHAPE = {"ks": (6, 2), "ks_tc": (12, 4)}
+KS_SHAPE = {"ks": (6, 2), "ks_tc": (12, 4), "ks_p60": (12, 4)}  # ks_p60: 60-bit P (wide tcgen05)
 if which in ("all", "ntt"):
     L, rows = 2, 16
     primes = [m.value for m in gen_ntt_prime_chain(50, n, L)]
@@ -62,9 +62,10 @@ if which in ("ntt12",):
     torch.cuda.synchronize()
     print("ntt paths", {k: v - p0[k] for k, v in _native.ntt_path_counts().items() if v != p0[k]},
           "rescale level", r.level)
-if which in ("all", "ks", "ks_tc"):
+if which in ("all", "ks", "ks_tc", "ks_p60"):
     Lk, Kk = KS_SHAPE.get(which, KS_SHAPE["ks"])
-    ctx = Context(hybrid_params(n, Lk, special=Kk, dnum=3, scale=float(2 ** 49)),
+    ctx = Context(hybrid_params(n, Lk, special=Kk, dnum=3, scale=float(2 ** 49),
+                                special_bits=60 if which == "ks_p60" else 50),
                   PoolConfig(unit_mb=64, cap_mb=2048))
     seed = lambda s: Rng(int(s).to_bytes(32, "little"))  # noqa: E731
     sk = keygen(ctx, seed(1))
