@@ -420,12 +420,18 @@ int build_levels(FheContext* ctx) {
     }
     // FP64 pairs (value, value / modulus) for the FP64-pipe base conversions
     const bool fp64 = ctx->chain->dev.fp64_ok;
+    // Q-side FP64 constants (rescale and ModDown finish) also on a mixed chain
+    // whose level-l Q primes are all < 2^50
+    bool q_fp64 = true;
+    for (int j = 0; j < l; ++j) q_fp64 &= ctx->chain->fp64_prime[j] != 0;
     std::vector<double2> up_inv_d, up_w_d, down_inv_d, down_w_d, p_inv_d, rs_inv_d;
-    if (fp64) {
+    if (fp64 || q_fp64) {
       for (int j = 0; j + 1 < l; ++j)
         rs_inv_d.push_back(make_double2((double)rs_inv[j].w, (double)rs_inv[j].w / (double)pr[j]));
       for (int j = 0; j < l; ++j)
         p_inv_d.push_back(make_double2((double)p_inv[j].w, (double)p_inv[j].w / (double)pr[j]));
+    }
+    if (fp64) {
       for (int s = 0; s < l; ++s)
         up_inv_d.push_back(make_double2((double)up_inv[s].w, (double)up_inv[s].w / (double)pr[s]));
       for (int di = 0; di < D; ++di) {
@@ -577,6 +583,8 @@ int build_levels(FheContext* ctx) {
       lp.up_w_d = (const double2*)(b + o11);
       lp.down_inv_d = (const double2*)(b + o12);
       lp.down_w_d = (const double2*)(b + o13);
+    }
+    if (fp64 || q_fp64) {
       lp.p_inv_d = (const double2*)(b + o28);
       lp.rs_inv_d = l > 1 ? (const double2*)(b + o29) : nullptr;
     }

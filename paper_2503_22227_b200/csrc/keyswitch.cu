@@ -1109,9 +1109,14 @@ size_t keyswitch_workspace(const FheContext& ctx, int level, int batch) {
 
 // The fused inner-product/finish kernel handles this level (FP64 chain, hybrid
 // key with at most 4 digits, not disabled by FHE_FUSE_INNER_FINISH=0).
+// the fused Q-limb inner product + ModDown finish (FP64 pipe): FP64 chains,
+// and mixed chains whose level Q primes are < 2^50 (their P-limb inner
+// product then runs on the integer pipe)
 static bool fin_inner_path(const FheContext& ctx, int level) {
-  return ctx.K > 0 && ctx.chain->dev.fp64_ok && ctx.levels[level].digits <= 4 &&
-         fin_inner_enabled();
+  const LevelPlan& lp = ctx.levels[level];
+  const bool fp = ctx.chain->dev.fp64_ok ||
+                  (lp.p_inv_d && ctx.chain->dev.twd && mixed_keyswitch_enabled());
+  return ctx.K > 0 && fp && lp.digits <= 4 && fin_inner_enabled();
 }
 
 int run_keyswitch(const FheContext& ctx, int level, const u64* d, long d_stride, const u64* key,
@@ -1302,7 +1307,8 @@ int run_keyswitch(const FheContext& ctx, int level, const u64* d, long d_stride,
     } else
       ks_inner_kernel<<<grid_for(work), kThreads, 4 * lp.digits * sizeof(int), st>>>(
           ch, d, d_stride, ext, (long)lp.ext_rows * n, key, L + K, lp.dig_info, lp.digits, level,
-          K, L, accQ, accP, add0, add1, add_stride, out0, out1, out_stride, batch, chunk);
+          K, L, accQ, accP, add0, add1, add_stride, out0, out1, out_stride, batch, chunk, m_begin,
+          m_end);
     FHE_LAUNCH_CHECK();
   }
   if (K == 0) return 0;
