@@ -78,7 +78,8 @@ __device__ __forceinline__ u64 bc_combine79(const unsigned (&a)[8], const BcTarg
   return csub(r, tg.p);
 }
 
-template <int KS, bool FPPRO, int SB = 7>
+// WT: some target may be >= 2^56 (79-bit reduction branch compiled in)
+template <int KS, bool FPPRO, int SB = 7, bool WT = false>
 __global__ void __launch_bounds__(kBuThreads, FHE_BU_MINB)
     bconv_umma_kernel(const DevChain ch, const BconvArgs a) {
   constexpr int SMAX = (32 * KS) / SB;
@@ -226,9 +227,11 @@ __global__ void __launch_bounds__(kBuThreads, FHE_BU_MINB)
         for (int tl = 0; tl < TH; ++tl) {
           if (tb + tl < nt) {
             const BcTarget tg = tgs[tb + tl];  // one LDS.128
-            *o = tg.sh >= 56 ? bc_combine79(r[tl], tg)
-                             : bc_combine71(r[tl][0], r[tl][1], r[tl][2], r[tl][3], r[tl][4],
-                                            r[tl][5], r[tl][6], tg);
+            if (WT && tg.sh >= 56)
+              *o = bc_combine79(r[tl], tg);
+            else
+              *o = bc_combine71(r[tl][0], r[tl][1], r[tl][2], r[tl][3], r[tl][4], r[tl][5],
+                                r[tl][6], tg);
           }
           o += n;
         }
@@ -270,7 +273,7 @@ __global__ void __launch_bounds__(kBuThreads, FHE_BU_MINB)
   }
 }
 
-template <int KS, int SB>
+template <int KS, int SB, bool WT>
 int launch_bconv_umma_ks(const DevChain& ch, const BconvArgs& a, int max_nt, dim3 grid,
                          cudaStream_t st) {
   const size_t smem = bconv_umma_smem(max_nt, KS);
@@ -282,30 +285,39 @@ int launch_bconv_umma_ks(const DevChain& ch, const BconvArgs& a, int max_nt, dim
     FHE_LAUNCH_CHECK();
     return 0;
   };
-  return (ch.fp64_ok && a.inv_d) ? go(bconv_umma_kernel<KS, true, SB>)
-                                 : go(bconv_umma_kernel<KS, false, SB>);
+  return (ch.fp64_ok && a.inv_d) ? go(bconv_umma_kernel<KS, true, SB, WT>)
+                                 : go(bconv_umma_kernel<KS, false, SB, WT>);
 }
 
 // grid.x CTAs per job, each looping over 128-coefficient tiles (n >= 128);
 // sb bytes per source word (7, or 8 for sources >= 2^56)
 int launch_bconv_umma(const DevChain& ch, const BconvArgs& a, int max_ns, int max_nt, dim3 grid,
-                      cudaStream_t st, int sb = 7) {
+                      cudaStream_t st, int sb = 7, bool wide_targets = false) {
   if (sb == 8) {
     switch ((8 * max_ns + 31) / 32) {
-      case 1: return launch_bconv_umma_ks<1, 8>(ch, a, max_nt, grid, st);
-      case 2: return launch_bconv_umma_ks<2, 8>(ch, a, max_nt, grid, st);
-      case 3: return launch_bconv_umma_ks<3, 8>(ch, a, max_nt, grid, st);
-      case 4: return launch_bconv_umma_ks<4, 8>(ch, a, max_nt, grid, st);
+      case 1: return launch_bconv_umma_ks<1, 8, true>(ch, a, max_nt, grid, st);
+      case 2: return launch_bconv_umma_ks<2, 8, true>(ch, a, max_nt, grid, st);
+      case 3: return launch_bconv_umma_ks<3, 8, true>(ch, a, max_nt, grid, st);
+      case 4: return launch_bconv_umma_ks<4, 8, true>(ch, a, max_nt, grid, st);
       default:
         fhe_set_error("tcgen05 base conversion: more than 16 wide source limbs");
         return -1;
     }
   }
+  if (wide_targets) {
+    switch (bconv_ks(max_ns)) {
+      case 1: return launch_bconv_umma_ks<1, 7, true>(ch, a, max_nt, grid, st);
+      case 2: return launch_bconv_umma_ks<2, 7, true>(ch, a, max_nt, grid, st);
+      case 3: return launch_bconv_umma_ks<3, 7, true>(ch, a, max_nt, grid, st);
+      case 4: return launch_bconv_umma_ks<4, 7, true>(ch, a, max_nt, grid, st);
+      default: break;
+    }
+  }
   switch (bconv_ks(max_ns)) {
-    case 1: return launch_bconv_umma_ks<1, 7>(ch, a, max_nt, grid, st);
-    case 2: return launch_bconv_umma_ks<2, 7>(ch, a, max_nt, grid, st);
-    case 3: return launch_bconv_umma_ks<3, 7>(ch, a, max_nt, grid, st);
-    case 4: return launch_bconv_umma_ks<4, 7>(ch, a, max_nt, grid, st);
+    case 1: return launch_bconv_umma_ks<1, 7, false>(ch, a, max_nt, grid, st);
+    case 2: return launch_bconv_umma_ks<2, 7, false>(ch, a, max_nt, grid, st);
+    case 3: return launch_bconv_umma_ks<3, 7, false>(ch, a, max_nt, grid, st);
+    case 4: return launch_bconv_umma_ks<4, 7, false>(ch, a, max_nt, grid, st);
     default:
       fhe_set_error("tcgen05 base conversion: more than 16 source limbs");
       return -1;

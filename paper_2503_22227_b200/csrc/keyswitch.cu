@@ -1193,7 +1193,7 @@ int run_keyswitch(const FheContext& ctx, int level, const u64* d, long d_stride,
         ba.bu_off = lp.up_bu_off;
         rc = launch_bconv_umma(ch, ba, lp.max_na, max_nt,
                                dim3(bu_grid_x(n, lp.digits * batch), lp.digits, batch), st,
-                               lp.up_sb);
+                               lp.up_sb, lp.bf_wide);
       } else {
         dim3 g((unsigned)std::max<long>(1, std::min<long>(n / (32 * kBcWarps), 64)), lp.digits,
                batch);
@@ -1328,7 +1328,7 @@ int run_keyswitch(const FheContext& ctx, int level, const u64* d, long d_stride,
       if (umma_down) {
         ba.bumma = lp.down_bu;
         rc = launch_bconv_umma(ch, ba, K, level, dim3(bu_grid_x(n, batch * 2), 1, batch * 2), st,
-                               lp.down_sb);
+                               lp.down_sb, lp.bf_wide);
       } else {
         dim3 g((unsigned)std::max<long>(1, std::min<long>(n / (32 * kBcWarps), 64)), 1,
                batch * 2);
